@@ -1,0 +1,201 @@
+/*
+ * quadb200.h -- C-ABI of libquadb200.so, the sm_100a hot path of the
+ * VisFly/quadsim batched simulator.
+ *
+ * The reference (/root/reference/pkg/src/quadsim) has no FFI of its own: its
+ * hot path is entered through Python functions plus one flat-array numba
+ * kernel.  Each entry point below replaces one of those call sites; the
+ * citation names the reference interface it stands in for.  The Python
+ * package paper_2407_14783_b200 binds these with ctypes (INTEGRATION.md shows
+ * the binding a maintainer of the reference would add).
+ *
+ * Conventions
+ *   - plain pointers + sizes; all per-step buffers are caller-owned DEVICE
+ *     memory, passed with the cudaStream_t (as void*) to enqueue on;
+ *   - the library allocates only scene handles (qb_scene_create/destroy) and
+ *     never allocates, frees or synchronises inside a per-step call;
+ *   - states are field-major planes: plane k (0..16, dynamics.py:3-8 order
+ *     p v q omega rotor) of env i lives at state[k*ld + i];
+ *   - every call returns 0 (QB_OK) or a QB_E* status; qb_last_error() gives a
+ *     thread-local message.  Per-env failures (non-finite state, spawn
+ *     failure) are written to caller buffers, never raised mid-stream;
+ *   - dtype: QB_F32 (production) or QB_F64 (exact-double validation build,
+ *     bit-identical to the reference wherever the reference evaluates only
+ *     + - * / sqrt).
+ */
+#ifndef QUADB200_H
+#define QUADB200_H
+
+#include <stdint.h>
+
+#include "qb_params.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum qb_status { QB_OK = 0, QB_EINVAL = 1, QB_ECUDA = 2, QB_ENOMEM = 3, QB_EEMPTY = 4 };
+enum qb_dtype { QB_F32 = 0, QB_F64 = 1 };
+enum qb_task_kind { QB_TASK_FREE = 0, QB_TASK_NAVIGATION = 1, QB_TASK_LANDING = 2 };
+enum qb_dist_kind { QB_DIST_FIXED = 0, QB_DIST_UNIFORM = 1, QB_DIST_NORMAL = 2 };
+
+const char *qb_last_error(void);
+int qb_version(void);
+int qb_device_sm_count(int32_t *out); /* SMs of the current device */
+
+/* ---------------------------------------------------------------- dynamics */
+
+/* control.command_to_rotor_speeds (control.py:242-252) followed by
+ * dynamics.step (dynamics.py:231-253) for n envs.  action: (n,4) row-major in
+ * the Command.as_array() layout of cmd_kind (qb_cmd_kind; QB_CMD_ROTOR =
+ * desired rotor speeds as in gradients.step_jacobian).  rotor_cmd_out (n,4)
+ * and nonfinite (n) may be NULL.  tape: when non-NULL the post-step state is
+ * also written to tape (same plane layout, stride ld). */
+int qb_dynamics_step(const qb_params *p, int32_t cmd_kind, int32_t dtype, int64_t n, int64_t ld, void *state,
+                     const void *action, void *rotor_cmd_out, uint8_t *nonfinite, void *stream);
+
+/* control.command_to_rotor_speeds alone (control.py:242-252): out (n,4). */
+int qb_command_to_rotor_speeds(const qb_params *p, int32_t cmd_kind, int32_t dtype, int64_t n, int64_t ld,
+                               const void *state, const void *action, void *out, void *stream);
+
+/* Horizon rollout (gradients.rollout, gradients.py:200-215, batched and
+ * tape-only): states_tape is (T+1) blocks of 17 planes (block stride 17*ld);
+ * block 0 must hold the initial state.  actions (T, n, 4). */
+int qb_rollout_forward(const qb_params *p, int32_t cmd_kind, int32_t dtype, int64_t n, int64_t ld, int32_t T,
+                       void *states_tape, const void *actions, uint8_t *nonfinite, void *stream);
+
+/* Reverse accumulation (gradients.rollout_grad, gradients.py:218-237),
+ * matrix-free: per step lambda <- J^T lambda + g[t], grad_a[t] = Ja^T lambda.
+ * g_traj (T+1) blocks of 17 planes (dL/dstate), grad_actions (T, n, 4),
+ * grad_init 17 planes.  Only QB_CMD_ROTOR and QB_CMD_CTBR/QB_CMD_SRT are
+ * differentiable.  action_grad_sum (4*T floats, may be NULL) receives the
+ * env-summed action gradient for shared-parameter reductions. */
+int qb_rollout_backward(const qb_params *p, int32_t cmd_kind, int32_t dtype, int64_t n, int64_t ld, int32_t T,
+                        const void *states_tape, const void *actions, const void *g_traj, void *grad_actions,
+                        void *grad_init, void *stream);
+
+/* One-step VJP (the per-step factor of rollout_grad): given state (pre-step),
+ * action and lam_next (17 planes, dL/dnext_state), writes lam_prev (17
+ * planes) and grad_action (n,4). */
+int qb_dynamics_vjp(const qb_params *p, int32_t cmd_kind, int32_t dtype, int64_t n, int64_t ld, const void *state,
+                    const void *action, const void *lam_next, void *lam_prev, void *grad_action, void *stream);
+
+/* ------------------------------------------------------------------ scenes */
+
+typedef struct qb_scene qb_scene;
+
+/* Flattened primitive tables of S scenes concatenated (shapes.py:139-212
+ * SceneArrays rows; type 0 sphere [c,r], 1 box [c,h,R(9)], 2 triangle
+ * [a,b,c]); prim_offsets has S+1 entries.  Builds one binned-SAH BVH per
+ * scene on the host and uploads float + double copies to the current
+ * device (replaces Scene.arrays / build_bvh, shapes.py:197-212,
+ * bvh.py:16-70). */
+int qb_scene_create(int32_t n_scenes, const int64_t *prim_offsets, const int64_t *prim_type, const double *prim_data,
+                    const int64_t *prim_oid, const double *prim_lo, const double *prim_hi, qb_scene **out);
+int qb_scene_destroy(qb_scene *s);
+/* stats: [n_nodes, n_prims, max_depth, n_scenes] */
+int qb_scene_stats(const qb_scene *s, int64_t *out4);
+/* raw bounds of scene k: lo.xyz hi.xyz (Scene.bounds, shapes.py:214-217) */
+int qb_scene_bounds(const qb_scene *s, int32_t k, double *out6);
+
+/* queries.nearest_point (queries.py:28-38 / kernels.py:120-182), exact
+ * double, batched: q (n,3) f64 device; pt (n,3), d (n) distance, oid (n). */
+int qb_nearest_point(const qb_scene *s, const int32_t *env_scene, int64_t n, const double *q, double *pt, double *dist,
+                     int32_t *oid, void *stream);
+
+/* queries.raycast (queries.py:56-71 / kernels.py:389-399), batched; t=-1 on
+ * miss.  o, d (n,3) in dtype; t (n) in dtype. */
+int qb_raycast(const qb_scene *s, int32_t dtype, const int32_t *env_scene, int64_t n, const void *o, const void *d,
+               double tmin, double tmax, void *t, int32_t *oid, void *stream);
+
+/* ------------------------------------------------------------------ camera */
+
+typedef struct qb_camera {
+    int32_t width, height;
+    double tan_half_h, tan_half_v, max_range; /* CameraModel, sensing.py:32-63 */
+    double rotation[9];                       /* camera -> body, row-major */
+    double translation[3];                    /* camera origin in body */
+} qb_camera;
+
+/* sensing.render_frames (sensing.py:77-100) -> kernels.render_batch
+ * (kernels.py:402-451) for n envs whose poses are read from the state
+ * planes.  depth (n,H,W) in dtype, seg (n,H,W) int32 (either may be NULL).
+ * env_scene (n) selects the scene of each env (NULL = scene 0).  When
+ * centroid_id > 0, centroid (n,2) receives the (col,row) pixel centroid of
+ * that id or (-1,-1) (tasks._id_centroid, tasks.py:121-128).  extra (n,K,4)
+ * spheres + extra_ids (n,K): swarm agents (kernels.py:438-445). */
+int qb_render(const qb_scene *s, const qb_camera *cam, int32_t dtype, int64_t n, int64_t ld, const void *state,
+              const int32_t *env_scene, void *depth, int32_t *seg, int32_t centroid_id, float *centroid,
+              const float *extra, const int32_t *extra_ids, int32_t n_extra, void *stream);
+
+/* Same renderer from explicit camera poses (render_batch's own inputs):
+ * origins (n,3), rotations (n,3,3) camera->world, in dtype. */
+int qb_render_poses(const qb_scene *s, const qb_camera *cam, int32_t dtype, int64_t n, const void *origins,
+                    const void *rotations, const int32_t *env_scene, void *depth, int32_t *seg, void *stream);
+
+/* --------------------------------------------------------------------- env */
+
+typedef struct qb_dist {
+    int32_t kind; /* qb_dist_kind (config.py:20-46) */
+    int32_t pad_;
+    double a[3]; /* fixed: value; uniform: low; normal: mean */
+    double b[3]; /* uniform: high; normal: sigma */
+} qb_dist;
+
+typedef struct qb_task {
+    int32_t task; /* qb_task_kind */
+    int32_t auto_reset;
+    int32_t episode_max_steps;
+    int32_t n_scene_perm; /* entries of scene_perm (= number of scenes) */
+    const int32_t *scene_perm; /* DEVICE (base.py:97-100) */
+    double collision_radius, min_spawn_clearance, bounds_margin;
+    qb_dist spawn[4]; /* position, velocity, orientation (rpy), angvel (config.py:57-61) */
+    /* navigation (tasks.py:34-62) */
+    double target[3];
+    double success_radius, w_progress, w_speed, w_obstacle, safe_distance;
+    /* landing (tasks.py:78-118) */
+    double pad_center[2];
+    double pad_half, success_height, success_speed, w_height, w_speed_landing, w_collision, pad_top;
+} qb_task;
+
+typedef struct qb_env_buffers {
+    int64_t n, ld, index_offset; /* envs in this shard, plane stride, global index of env 0 */
+    int32_t dtype, pad_;
+    void *state;       /* 17 planes */
+    void *prev_state;  /* 17 planes or NULL */
+    const void *action; /* (n,4) */
+    int32_t *step_count, *agent_scene, *reset_count;
+    uint8_t *needs_respawn, *terminated, *truncated, *success, *collision, *out_of_bounds, *nonfinite;
+    float *reward;
+    double *nearest_dist; /* (n) */
+    double *nearest_pt;   /* (n,3) */
+    uint64_t *rng;        /* (n,4): pcg64 state hi/lo, inc hi/lo */
+    int32_t *error_count; /* [1] spawn failures (SpawnFailure) */
+} qb_env_buffers;
+
+/* QuadEnvBase.reset(seed) (base.py:93-112) for a shard: per-env generators
+ * default_rng(seed + index_offset + i), spawn sampling with clearance
+ * rejection, proximity refresh. */
+int qb_env_reset(const qb_params *p, const qb_task *task, const qb_scene *s, const qb_env_buffers *b, uint64_t seed,
+                 void *stream);
+
+/* QuadEnvBase.step (base.py:156-210) minus observation rendering, fused in
+ * one kernel: lazy auto-reset of last step's finished envs, controller,
+ * dynamics, non-finite freeze, proximity/collision/out-of-bounds, task
+ * success + reward, terminated/truncated. */
+int qb_env_step(const qb_params *p, int32_t cmd_kind, const qb_task *task, const qb_scene *s, const qb_env_buffers *b,
+                void *stream);
+
+/* Proximity refresh alone (base.py:214-224) on the current state. */
+int qb_env_refresh(const qb_task *task, const qb_scene *s, const qb_env_buffers *b, void *stream);
+
+/* numpy.random.default_rng(seed + i) seeding for i in [0,n): out (n,4). */
+int qb_rng_seed(uint64_t seed, int64_t n, uint64_t *out, void *stream);
+/* n draws of next_double from each stream (testing hook): out (n, k). */
+int qb_rng_doubles(int64_t n, uint64_t *rng, int32_t k, double *out, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* QUADB200_H */

@@ -1,0 +1,246 @@
+"""ORACLE restatement of the reference env step (TEST INFRASTRUCTURE ONLY).
+
+Follows env/base.py:93-232 (reset, _spawn_agent, step, _refresh_proximity)
+and env/tasks.py:19-128 (free / navigation / landing hooks) for parallel
+mode, with the heavy kernels in oracle/quadsim_oracle.c.  Per-agent numpy
+generators (default_rng(seed + i), base.py:95) are used exactly as the
+reference uses them, so spawns are bit-identical.
+
+Configs are duck-typed: anything with the reference EnvConfig fields works
+(the reference's own dataclasses or paper_2407_14783_b200.env.config).
+Scenes are passed in already flattened (OracleScene), one per config scene.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from . import (DOWNWARD, FORWARD, CMD_KINDS, OracleScene, camera_pose_world, command_to_rotor_speeds, dynamics_step,
+               pack_params)
+
+PAD_ID = 9  # generate.py:15
+PAD_TOP = 0.02  # generate.py:91
+
+
+def _quat_from_rpy(rpy):
+    """base.py:313-319 via quatmath.from_axis_angle / multiply."""
+
+    def aa(axis, angle):
+        axis = np.asarray(axis, dtype=float)
+        axis = axis / np.linalg.norm(axis)
+        half = 0.5 * angle
+        return np.concatenate([[np.cos(half)], np.sin(half) * axis])
+
+    def mul(q, p):
+        qw, qx, qy, qz = q
+        pw, px, py, pz = p
+        return np.array([qw * pw - qx * px - qy * py - qz * pz, qw * px + qx * pw + qy * pz - qz * py,
+                         qw * py - qx * pz + qy * pw + qz * px, qw * pz + qx * py - qy * px + qz * pw])
+
+    roll, pitch, yaw = rpy
+    return mul(aa([0, 0, 1.0], yaw), mul(aa([0, 1.0, 0], pitch), aa([1.0, 0, 0], roll)))
+
+
+def _sample(dist, rng):
+    """config.py:41-46 DistSpec.sample."""
+    if dist.kind == "fixed":
+        return np.asarray(dist.value, float).copy()
+    if dist.kind == "uniform":
+        return rng.uniform(np.asarray(dist.low, float), np.asarray(dist.high, float))
+    return np.asarray(dist.mean, float) + np.asarray(dist.sigma, float) * rng.standard_normal(3)
+
+
+class OracleEnv:
+    def __init__(self, config, scenes, params, sim, gains):
+        self.config = config
+        self.scenes = list(scenes)
+        self.P = pack_params(params, sim, gains)
+        self.n = config.num_agents
+        self.task = config.task
+        tp = dict(config.task_params)
+        if self.task == "navigation":  # tasks.py:34-43
+            self.target = np.asarray(tp.get("target", [4.2, 0.0, 2.0]), float).reshape(3)
+            self.success_radius = float(tp.get("success_radius", 0.5))
+            self.w_progress = float(tp.get("w_progress", 10.0))
+            self.w_speed = float(tp.get("w_speed", 0.02))
+            self.w_obstacle = float(tp.get("w_obstacle", 0.5))
+            self.safe_distance = float(tp.get("safe_distance", 1.0))
+        elif self.task == "landing":  # tasks.py:78-95
+            spec = config.scenes[0]
+            self.pad_center = np.asarray(tp.get("pad_center", spec.pad_center), float).reshape(2)
+            self.pad_half = float(spec.pad_size) / 2.0
+            self.success_height = float(tp.get("success_height", 0.1))
+            self.success_speed = float(tp.get("success_speed", 0.1))
+            self.w_height = float(tp.get("w_height", 0.1))
+            self.w_speed = float(tp.get("w_speed", 0.5))
+            self.w_collision = float(tp.get("w_collision", 1.0))
+            self.seg_sensor = [s.name for s in config.sensors if s.kind == "segmentation"][-1]
+        elif self.task != "free":
+            raise NotImplementedError(self.task)
+        self.bounds = [(sc.bounds_lo - config.bounds_margin, sc.bounds_hi + config.bounds_margin) for sc in self.scenes]
+        self.state = np.zeros((self.n, 17))
+        self.agent_scene = np.zeros(self.n, int)
+        self.step_counts = np.zeros(self.n, int)
+        self.needs_respawn = np.zeros(self.n, bool)
+        self.nearest_dist = np.full(self.n, np.inf)
+        self.nearest_pt = np.zeros((self.n, 3))
+        self.collision = np.zeros(self.n, bool)
+        self.oob = np.zeros(self.n, bool)
+        self.nonfinite = np.zeros(self.n, bool)
+        self.seg_cache = {}
+
+    # ----------------------------------------------------------------- reset
+    def reset(self, seed=0):
+        """base.py:93-112."""
+        self.rngs = [np.random.default_rng(int(seed) + i) for i in range(self.n)]
+        ns = len(self.scenes)
+        if self.config.scene_sampling == "shuffled":
+            self.scene_perm = np.random.default_rng(int(seed)).permutation(ns)
+        else:
+            self.scene_perm = np.arange(ns)
+        self.reset_counts = np.zeros(self.n, int)
+        self.state[:] = 0.0
+        self.state[:, 6] = 1.0
+        self.state[:, 13:17] = self.P.hover_speed
+        for i in range(self.n):
+            self._spawn(i)
+        self.prev_state = self.state.copy()
+        self.step_counts[:] = 0
+        self.needs_respawn[:] = False
+        self.collision[:] = False
+        self.oob[:] = False
+        self.nonfinite[:] = False
+        self._refresh_proximity()
+        return self.observe()
+
+    def _spawn(self, i):
+        """base.py:114-147."""
+        self.agent_scene[i] = self.scene_perm[(i + self.reset_counts[i]) % len(self.scenes)]
+        self.reset_counts[i] += 1
+        rng = self.rngs[i]
+        rand = self.config.randomization
+        scene = self.scenes[self.agent_scene[i]]
+        pos = None
+        for _ in range(1000):
+            cand = _sample(rand.position, rng)
+            _, d, _ = scene.nearest_point(cand[None])
+            if d[0] < self.config.min_spawn_clearance:
+                continue
+            pos = cand
+            break
+        if pos is None:
+            raise RuntimeError(f"SpawnFailure agent {i}")
+        vel = _sample(rand.velocity, rng)
+        quat = _quat_from_rpy(_sample(rand.orientation, rng))
+        ang = _sample(rand.angvel, rng)
+        self.state[i, 0:3] = pos
+        self.state[i, 3:6] = vel
+        self.state[i, 6:10] = quat
+        self.state[i, 10:13] = ang
+        self.state[i, 13:17] = self.P.hover_speed
+        self.step_counts[i] = 0
+
+    # ------------------------------------------------------------------ step
+    def step(self, action):
+        """base.py:156-210 (parallel mode). `action` is the (N,4) as_array()."""
+        action = np.asarray(action, float).reshape(self.n, 4)
+        if self.config.auto_reset and self.needs_respawn.any():
+            for i in np.nonzero(self.needs_respawn)[0]:
+                self._spawn(int(i))
+            self.needs_respawn[:] = False
+        self.prev_state = self.state.copy()
+        cmds = command_to_rotor_speeds(self.P, self.config.command_type, self.state, action)
+        nxt, bad = dynamics_step(self.P, self.state, cmds)
+        nxt[bad] = self.prev_state[bad]
+        self.state = nxt
+        self.nonfinite = bad
+        self.step_counts += 1
+        self._refresh_proximity()
+        success = self.get_success()
+        reward = self.get_reward()
+        obs = self.observe()
+        terminated = success | self.collision | self.oob | self.nonfinite
+        truncated = ~terminated & (self.step_counts >= self.config.episode_max_steps)
+        self.needs_respawn = terminated | truncated
+        return obs, reward, terminated, truncated, success
+
+    def _refresh_proximity(self):
+        """base.py:214-224."""
+        for s in range(len(self.scenes)):
+            m = self.agent_scene == s
+            if not m.any():
+                continue
+            pt, d, _ = self.scenes[s].nearest_point(self.state[m, 0:3])
+            self.nearest_pt[m] = pt
+            self.nearest_dist[m] = d
+            lo, hi = self.bounds[s]
+            p = self.state[m, 0:3]
+            self.oob[m] = ~(np.all(p >= lo, axis=1) & np.all(p <= hi, axis=1))
+        self.collision = self.nearest_dist < self.config.collision_radius
+
+    # ----------------------------------------------------------------- tasks
+    def _dist(self, x):
+        d = x[:, 0:3] - self.target[None, :]
+        return np.sqrt(d[:, 0] ** 2 + d[:, 1] ** 2 + d[:, 2] ** 2)
+
+    def _height(self):
+        return np.maximum(self.state[:, 2] - PAD_TOP - self.config.collision_radius, 0.0)
+
+    def get_success(self):
+        if self.task == "navigation":  # tasks.py:49-50
+            return self._dist(self.state) < self.success_radius
+        if self.task == "landing":  # tasks.py:101-106
+            speed = np.linalg.norm(self.state[:, 3:6], axis=1)
+            off = np.abs(self.state[:, 0:2] - self.pad_center[None, :])
+            centered = (off[:, 0] <= self.pad_half) & (off[:, 1] <= self.pad_half)
+            return (self._height() < self.success_height) & (speed < self.success_speed) & centered
+        return np.zeros(self.n, bool)
+
+    def get_reward(self):
+        if self.task == "navigation":  # tasks.py:52-56
+            progress = self._dist(self.prev_state) - self._dist(self.state)
+            speed2 = (self.state[:, 3:6] ** 2).sum(axis=1)
+            prox = np.clip(1.0 - self.nearest_dist / self.safe_distance, 0.0, 1.0)
+            return self.w_progress * progress - self.w_speed * speed2 - self.w_obstacle * prox
+        if self.task == "landing":  # tasks.py:108-111
+            speed2 = (self.state[:, 3:6] ** 2).sum(axis=1)
+            return -self.w_height * self._height() + self.w_speed * np.exp(-speed2) - self.w_collision * self.collision
+        return np.zeros(self.n)
+
+    # ----------------------------------------------------------- observation
+    def render(self, sensor):
+        """base.py:256-277 for one camera sensor."""
+        H, W = sensor.height, sensor.width
+        rot = FORWARD if sensor.orientation == "forward" else DOWNWARD
+        depth = np.empty((self.n, H, W))
+        seg = np.empty((self.n, H, W), np.int64)
+        tv = math.tan(sensor.vertical_fov / 2.0)
+        th = tv * W / H
+        for s in np.unique(self.agent_scene):
+            m = np.nonzero(self.agent_scene == s)[0]
+            o, r = camera_pose_world(self.state[m, 0:3], self.state[m, 6:10], rot, sensor.translation)
+            d, i = self.scenes[s].render(o, r, W, H, th, tv, sensor.max_range)
+            depth[m] = d
+            seg[m] = i
+        return depth, seg
+
+    def observe(self):
+        """base.py:287-310 + tasks.py:58-62, 113-118 (batched form)."""
+        obs = {"state": self.state[:, 0:13].copy()}
+        for sensor in self.config.sensors:
+            depth, seg = self.render(sensor)
+            obs[sensor.name] = depth if sensor.kind == "depth" else seg.astype(float)
+            self.seg_cache[sensor.name] = seg
+        if self.task == "navigation":
+            obs["target"] = np.broadcast_to(self.target, (self.n, 3)).copy()
+        elif self.task == "landing":  # tasks.py:121-128
+            seg = self.seg_cache[self.seg_sensor]
+            tgt = np.full((self.n, 2), -1.0)
+            for i in range(self.n):
+                rows, cols = np.nonzero(seg[i] == PAD_ID)
+                if len(rows):
+                    tgt[i] = [cols.mean(), rows.mean()]
+            obs["target"] = tgt
+        return obs

@@ -1,0 +1,503 @@
+// qb_abi.cu -- extern "C" surface of libquadb200.so (include/quadb200.h):
+// argument validation, thread-local error strings, scene construction
+// (host binned-SAH BVH + float/double device copies) and the launch calls.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "qb_internal.h"
+
+namespace {
+thread_local char g_err[512] = "";
+}
+
+namespace qb {
+
+void set_error(const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+int check_launch(const char *what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        set_error("%s: %s", what, cudaGetErrorString(e));
+        return QB_ECUDA;
+    }
+    return QB_OK;
+}
+
+int sm_count() {
+    int dev = 0, n = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+}
+
+// ------------------------------------------------------------------ BVH
+// Binned-SAH binary BVH over primitive AABBs.  Children of an internal node
+// are adjacent (left = a, right = a + 1) and leaf primitives are contiguous,
+// like the reference layout (bvh.py:1-8), but the split is the SAH-optimal
+// bin boundary instead of the centroid median: fewer node visits per ray.
+struct BNode {
+    double lo[3], hi[3];
+    int a, b;  // leaf: first, count (>0); internal: left child, -axis (<=0)
+};
+
+static double half_area(const double *lo, const double *hi) {
+    double dx = hi[0] - lo[0], dy = hi[1] - lo[1], dz = hi[2] - lo[2];
+    return dx * dy + dy * dz + dz * dx;
+}
+
+static int build_bvh(int n, const double *plo, const double *phi, std::vector<BNode> &nodes, std::vector<int> &order,
+                     int &max_depth) {
+    const int LEAF = 4, BINS = 16, DEPTH_CAP = 56;
+    order.resize(n);
+    for (int i = 0; i < n; ++i) order[i] = i;
+    std::vector<double> cen(3 * (size_t)n);
+    for (int i = 0; i < n; ++i)
+        for (int k = 0; k < 3; ++k) cen[3 * i + k] = 0.5 * (plo[3 * i + k] + phi[3 * i + k]);
+    nodes.clear();
+    nodes.push_back(BNode{});
+    struct Item {
+        int node, begin, end, depth;
+    };
+    std::vector<Item> stack{{0, 0, n, 1}};
+    max_depth = 1;
+    while (!stack.empty()) {
+        Item it = stack.back();
+        stack.pop_back();
+        max_depth = std::max(max_depth, it.depth);
+        BNode &nd = nodes[it.node];
+        double clo[3] = {INFINITY, INFINITY, INFINITY}, chi[3] = {-INFINITY, -INFINITY, -INFINITY};
+        for (int k = 0; k < 3; ++k) {
+            nd.lo[k] = INFINITY;
+            nd.hi[k] = -INFINITY;
+        }
+        for (int i = it.begin; i < it.end; ++i) {
+            int p = order[i];
+            for (int k = 0; k < 3; ++k) {
+                nd.lo[k] = std::min(nd.lo[k], plo[3 * p + k]);
+                nd.hi[k] = std::max(nd.hi[k], phi[3 * p + k]);
+                clo[k] = std::min(clo[k], cen[3 * p + k]);
+                chi[k] = std::max(chi[k], cen[3 * p + k]);
+            }
+        }
+        int count = it.end - it.begin;
+        if (count <= LEAF) {
+            nd.a = it.begin;
+            nd.b = count;
+            continue;
+        }
+        // binned SAH over the three axes
+        int best_axis = -1, best_bin = -1;
+        double best_cost = INFINITY;
+        if (it.depth < DEPTH_CAP) {
+            for (int ax = 0; ax < 3; ++ax) {
+                double ext = chi[ax] - clo[ax];
+                if (!(ext > 0.0)) continue;
+                double blo[BINS][3], bhi[BINS][3];
+                int bcnt[BINS] = {0};
+                for (int b = 0; b < BINS; ++b)
+                    for (int k = 0; k < 3; ++k) {
+                        blo[b][k] = INFINITY;
+                        bhi[b][k] = -INFINITY;
+                    }
+                double scale = BINS / ext;
+                for (int i = it.begin; i < it.end; ++i) {
+                    int p = order[i];
+                    int b = std::min(BINS - 1, (int)((cen[3 * p + ax] - clo[ax]) * scale));
+                    ++bcnt[b];
+                    for (int k = 0; k < 3; ++k) {
+                        blo[b][k] = std::min(blo[b][k], plo[3 * p + k]);
+                        bhi[b][k] = std::max(bhi[b][k], phi[3 * p + k]);
+                    }
+                }
+                // suffix areas
+                double rarea[BINS];
+                int rcnt[BINS];
+                double alo[3] = {INFINITY, INFINITY, INFINITY}, ahi[3] = {-INFINITY, -INFINITY, -INFINITY};
+                int c = 0;
+                for (int b = BINS - 1; b > 0; --b) {
+                    for (int k = 0; k < 3; ++k) {
+                        alo[k] = std::min(alo[k], blo[b][k]);
+                        ahi[k] = std::max(ahi[k], bhi[b][k]);
+                    }
+                    c += bcnt[b];
+                    rcnt[b] = c;
+                    rarea[b] = c ? half_area(alo, ahi) : 0.0;
+                }
+                for (int k = 0; k < 3; ++k) {
+                    alo[k] = INFINITY;
+                    ahi[k] = -INFINITY;
+                }
+                c = 0;
+                for (int b = 0; b < BINS - 1; ++b) {  // split between bin b and b+1
+                    for (int k = 0; k < 3; ++k) {
+                        alo[k] = std::min(alo[k], blo[b][k]);
+                        ahi[k] = std::max(ahi[k], bhi[b][k]);
+                    }
+                    c += bcnt[b];
+                    if (c == 0 || rcnt[b + 1] == 0) continue;
+                    double cost = half_area(alo, ahi) * c + rarea[b + 1] * rcnt[b + 1];
+                    if (cost < best_cost) {
+                        best_cost = cost;
+                        best_axis = ax;
+                        best_bin = b;
+                    }
+                }
+            }
+        }
+        int mid;
+        int axis;
+        if (best_axis >= 0) {
+            axis = best_axis;
+            double scale = BINS / (chi[axis] - clo[axis]);
+            double c0 = clo[axis];
+            auto pivot = std::partition(order.begin() + it.begin, order.begin() + it.end, [&](int p) {
+                return std::min(BINS - 1, (int)((cen[3 * p + axis] - c0) * scale)) <= best_bin;
+            });
+            mid = (int)(pivot - order.begin());
+        } else {  // degenerate centroids (or depth cap): median split on the widest axis
+            axis = 0;
+            double ext = -1.0;
+            for (int k = 0; k < 3; ++k)
+                if (chi[k] - clo[k] > ext) {
+                    ext = chi[k] - clo[k];
+                    axis = k;
+                }
+            mid = it.begin + count / 2;
+            std::nth_element(order.begin() + it.begin, order.begin() + mid, order.begin() + it.end,
+                             [&](int x, int y) { return cen[3 * x + axis] < cen[3 * y + axis]; });
+        }
+        if (mid <= it.begin || mid >= it.end) mid = it.begin + count / 2;
+        int left = (int)nodes.size();
+        nodes.push_back(BNode{});
+        nodes.push_back(BNode{});
+        nodes[it.node].a = left;  // (re-index: push_back may have moved nd)
+        nodes[it.node].b = -axis;
+        stack.push_back({left + 1, mid, it.end, it.depth + 1});
+        stack.push_back({left, it.begin, mid, it.depth + 1});
+    }
+    return max_depth <= 62 ? 0 : -1;
+}
+
+static float f_down(double v) {
+    double m = v - 1e-6 * (1.0 + std::fabs(v));
+    float f = (float)m;
+    if ((double)f > m) f = std::nextafter(f, -INFINITY);
+    return f;
+}
+static float f_up(double v) {
+    double m = v + 1e-6 * (1.0 + std::fabs(v));
+    float f = (float)m;
+    if ((double)f < m) f = std::nextafter(f, INFINITY);
+    return f;
+}
+
+static float4 f4(float x, float y, float z, float w) { return make_float4(x, y, z, w); }
+static float i2f(int a) {
+    float f;
+    std::memcpy(&f, &a, 4);
+    return f;
+}
+
+static void pack_prim(int type, const double *d, float4 *o) {
+    for (int k = 0; k < 4; ++k) o[k] = f4(0, 0, 0, 0);
+    if (type == QB_SPHERE) {
+        o[0] = f4((float)d[0], (float)d[1], (float)d[2], (float)d[3]);
+        o[1] = f4((float)(d[3] * d[3]), 0, 0, 0);
+    } else if (type == QB_BOX) {
+        o[0] = f4((float)d[0], (float)d[1], (float)d[2], (float)d[3]);
+        o[1] = f4((float)d[4], (float)d[5], (float)d[6], (float)d[7]);
+        o[2] = f4((float)d[8], (float)d[9], (float)d[10], (float)d[11]);
+        o[3] = f4((float)d[12], (float)d[13], (float)d[14], 0);
+    } else {
+        double e1[3] = {d[3] - d[0], d[4] - d[1], d[5] - d[2]}, e2[3] = {d[6] - d[0], d[7] - d[1], d[8] - d[2]};
+        o[0] = f4((float)d[0], (float)d[1], (float)d[2], (float)e1[0]);
+        o[1] = f4((float)e1[1], (float)e1[2], (float)e2[0], (float)e2[1]);
+        o[2] = f4((float)e2[2], 0, 0, 0);
+    }
+}
+
+template <class T> static T *dev_upload(qb_scene *s, const std::vector<T> &v) {
+    void *p = nullptr;
+    size_t bytes = std::max<size_t>(v.size() * sizeof(T), 16);
+    if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
+    s->allocs[s->n_allocs++] = p;
+    if (!v.empty() && cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
+    return static_cast<T *>(p);
+}
+
+}  // namespace qb
+
+extern "C" {
+
+const char *qb_last_error(void) { return g_err; }
+
+int qb_version(void) { return 1; }
+
+int qb_device_sm_count(int32_t *out) {
+    QB_REQUIRE(out, "out is NULL");
+    *out = qb::sm_count();
+    return QB_OK;
+}
+
+int qb_dynamics_step(const qb_params *p, int32_t cmd_kind, int32_t dtype, int64_t n, int64_t ld, void *state,
+                     const void *action, void *rotor_cmd_out, uint8_t *nonfinite, void *stream) {
+    QB_REQUIRE(p && state && action, "qb_dynamics_step: NULL argument");
+    QB_REQUIRE(n >= 0 && ld >= n, "qb_dynamics_step: bad n=%lld ld=%lld", (long long)n, (long long)ld);
+    QB_REQUIRE(dtype == QB_F32 || dtype == QB_F64, "bad dtype %d", dtype);
+    return qb::launch_dynamics_step(p, cmd_kind, dtype, n, ld, state, action, rotor_cmd_out, nonfinite, 0, nullptr,
+                                    qb::as_stream(stream));
+}
+
+int qb_command_to_rotor_speeds(const qb_params *p, int32_t cmd_kind, int32_t dtype, int64_t n, int64_t ld,
+                               const void *state, const void *action, void *out, void *stream) {
+    QB_REQUIRE(p && state && action && out, "qb_command_to_rotor_speeds: NULL argument");
+    QB_REQUIRE(n >= 0 && ld >= n, "bad n/ld");
+    QB_REQUIRE(dtype == QB_F32 || dtype == QB_F64, "bad dtype %d", dtype);
+    return qb::launch_command(p, cmd_kind, dtype, n, ld, state, action, out, qb::as_stream(stream));
+}
+
+int qb_rollout_forward(const qb_params *p, int32_t cmd_kind, int32_t dtype, int64_t n, int64_t ld, int32_t T,
+                       void *states_tape, const void *actions, uint8_t *nonfinite, void *stream) {
+    QB_REQUIRE(p && states_tape && actions, "qb_rollout_forward: NULL argument");
+    QB_REQUIRE(n >= 0 && ld >= n && T >= 1, "bad n/ld/T");
+    QB_REQUIRE(dtype == QB_F32 || dtype == QB_F64, "bad dtype %d", dtype);
+    return qb::launch_dynamics_step(p, cmd_kind, dtype, n, ld, states_tape, nullptr, nullptr, nonfinite, T, actions,
+                                    qb::as_stream(stream));
+}
+
+int qb_rollout_backward(const qb_params *p, int32_t cmd_kind, int32_t dtype, int64_t n, int64_t ld, int32_t T,
+                        const void *states_tape, const void *actions, const void *g_traj, void *grad_actions,
+                        void *grad_init, void *stream) {
+    QB_REQUIRE(p && states_tape && actions && g_traj && grad_actions && grad_init, "qb_rollout_backward: NULL argument");
+    QB_REQUIRE(n >= 0 && ld >= n && T >= 1, "bad n/ld/T");
+    QB_REQUIRE(dtype == QB_F32 || dtype == QB_F64, "bad dtype %d", dtype);
+    return qb::launch_vjp(p, cmd_kind, dtype, n, ld, T, states_tape, actions, g_traj, grad_actions, grad_init,
+                          qb::as_stream(stream));
+}
+
+int qb_dynamics_vjp(const qb_params *p, int32_t cmd_kind, int32_t dtype, int64_t n, int64_t ld, const void *state,
+                    const void *action, const void *lam_next, void *lam_prev, void *grad_action, void *stream) {
+    QB_REQUIRE(p && state && action && lam_next && lam_prev && grad_action, "qb_dynamics_vjp: NULL argument");
+    QB_REQUIRE(n >= 0 && ld >= n, "bad n/ld");
+    QB_REQUIRE(dtype == QB_F32 || dtype == QB_F64, "bad dtype %d", dtype);
+    // T = -1: single step, g_traj = lam_next, grad_init = lam_prev
+    return qb::launch_vjp(p, cmd_kind, dtype, n, ld, -1, state, action, lam_next, grad_action, lam_prev,
+                          qb::as_stream(stream));
+}
+
+int qb_scene_create(int32_t n_scenes, const int64_t *prim_offsets, const int64_t *prim_type, const double *prim_data,
+                    const int64_t *prim_oid, const double *prim_lo, const double *prim_hi, qb_scene **out) {
+    QB_REQUIRE(out && prim_offsets && n_scenes >= 1, "qb_scene_create: bad arguments");
+    *out = nullptr;
+    for (int s = 0; s < n_scenes; ++s)
+        if (prim_offsets[s + 1] <= prim_offsets[s]) {
+            qb::set_error("scene %d has no primitives", s);
+            return QB_EEMPTY;
+        }
+    const long long P = prim_offsets[n_scenes];
+    QB_REQUIRE(prim_type && prim_data && prim_oid && prim_lo && prim_hi, "qb_scene_create: NULL prim arrays");
+    QB_REQUIRE(P < (1LL << 30), "too many primitives");
+    for (long long i = 0; i < P; ++i) QB_REQUIRE(prim_type[i] >= 0 && prim_type[i] <= 2, "bad prim type at %lld", i);
+
+    std::vector<int> roots(n_scenes);
+    std::vector<double> bounds(6 * (size_t)n_scenes);
+    std::vector<float4> nodef;
+    std::vector<double> noded;
+    std::vector<int2> nodei;
+    std::vector<float4> primf(4 * (size_t)P);
+    std::vector<double> primd(16 * (size_t)P);
+    std::vector<int2> meta(P);
+    int max_depth = 0;
+    for (int s = 0; s < n_scenes; ++s) {
+        const long long off = prim_offsets[s], cnt = prim_offsets[s + 1] - off;
+        std::vector<qb::BNode> nodes;
+        std::vector<int> order;
+        int depth = 0;
+        if (qb::build_bvh((int)cnt, prim_lo + 3 * off, prim_hi + 3 * off, nodes, order, depth) != 0) {
+            qb::set_error("BVH of scene %d too deep (%d)", s, depth);
+            return QB_EINVAL;
+        }
+        max_depth = std::max(max_depth, depth);
+        const int node_off = (int)nodei.size();
+        roots[s] = node_off;
+        for (int k = 0; k < 3; ++k) {
+            double lo = INFINITY, hi = -INFINITY;
+            for (long long i = off; i < off + cnt; ++i) {
+                lo = std::min(lo, prim_lo[3 * i + k]);
+                hi = std::max(hi, prim_hi[3 * i + k]);
+            }
+            bounds[6 * s + k] = lo;
+            bounds[6 * s + 3 + k] = hi;
+        }
+        for (const qb::BNode &nd : nodes) {
+            int a = nd.b > 0 ? (int)(nd.a + off) : nd.a + node_off;
+            nodef.push_back(make_float4(qb::f_down(nd.lo[0]), qb::f_down(nd.lo[1]), qb::f_down(nd.lo[2]), qb::i2f(a)));
+            nodef.push_back(make_float4(qb::f_up(nd.hi[0]), qb::f_up(nd.hi[1]), qb::f_up(nd.hi[2]), qb::i2f(nd.b)));
+            for (int k = 0; k < 3; ++k) noded.push_back(nd.lo[k]);
+            for (int k = 0; k < 3; ++k) noded.push_back(nd.hi[k]);
+            nodei.push_back(make_int2(a, nd.b));
+        }
+        for (long long j = 0; j < cnt; ++j) {
+            long long src = off + order[j], dst = off + j;
+            qb::pack_prim((int)prim_type[src], prim_data + 16 * src, &primf[4 * dst]);
+            std::memcpy(&primd[16 * dst], prim_data + 16 * src, 16 * sizeof(double));
+            QB_REQUIRE(prim_oid[src] > 0 && prim_oid[src] < (1LL << 31), "object ids must be positive int32");
+            meta[dst] = make_int2((int)prim_type[src], (int)prim_oid[src]);
+        }
+    }
+    qb_scene *sc = new qb_scene();
+    sc->n_allocs = 0;
+    cudaGetDevice(&sc->device);
+    sc->n_nodes = (long long)nodei.size();
+    sc->n_prims = P;
+    sc->max_depth = max_depth;
+    sc->host_bounds = new double[6 * n_scenes];
+    std::memcpy(sc->host_bounds, bounds.data(), sizeof(double) * 6 * n_scenes);
+    DevScene &d = sc->dev;
+    d.n_scenes = n_scenes;
+    d.n_prims = (int)P;
+    d.root = qb::dev_upload(sc, roots);
+    d.bounds = qb::dev_upload(sc, bounds);
+    d.nodef = qb::dev_upload(sc, nodef);
+    d.noded = qb::dev_upload(sc, noded);
+    d.nodei = qb::dev_upload(sc, nodei);
+    d.primf = qb::dev_upload(sc, primf);
+    d.primd = qb::dev_upload(sc, primd);
+    d.meta = qb::dev_upload(sc, meta);
+    if (!d.root || !d.bounds || !d.nodef || !d.noded || !d.nodei || !d.primf || !d.primd || !d.meta) {
+        qb::set_error("scene upload failed: %s", cudaGetErrorString(cudaGetLastError()));
+        qb_scene_destroy(sc);
+        return QB_ENOMEM;
+    }
+    *out = sc;
+    return QB_OK;
+}
+
+int qb_scene_destroy(qb_scene *s) {
+    if (!s) return QB_OK;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(s->device);
+    for (int i = 0; i < s->n_allocs; ++i) cudaFree(s->allocs[i]);
+    cudaSetDevice(prev);
+    delete[] s->host_bounds;
+    delete s;
+    return QB_OK;
+}
+
+int qb_scene_stats(const qb_scene *s, int64_t *out4) {
+    QB_REQUIRE(s && out4, "NULL argument");
+    out4[0] = s->n_nodes;
+    out4[1] = s->n_prims;
+    out4[2] = s->max_depth;
+    out4[3] = s->dev.n_scenes;
+    return QB_OK;
+}
+
+int qb_scene_bounds(const qb_scene *s, int32_t k, double *out6) {
+    QB_REQUIRE(s && out6 && k >= 0 && k < s->dev.n_scenes, "bad arguments");
+    std::memcpy(out6, s->host_bounds + 6 * k, 6 * sizeof(double));
+    return QB_OK;
+}
+
+int qb_nearest_point(const qb_scene *s, const int32_t *env_scene, int64_t n, const double *q, double *pt, double *dist,
+                     int32_t *oid, void *stream) {
+    QB_REQUIRE(s && q && n >= 0, "qb_nearest_point: bad arguments");
+    return qb::launch_nearest(s, env_scene, n, q, pt, dist, oid, qb::as_stream(stream));
+}
+
+int qb_raycast(const qb_scene *s, int32_t dtype, const int32_t *env_scene, int64_t n, const void *o, const void *d,
+               double tmin, double tmax, void *t, int32_t *oid, void *stream) {
+    QB_REQUIRE(s && o && d && t && n >= 0, "qb_raycast: bad arguments");
+    QB_REQUIRE(dtype == QB_F32 || dtype == QB_F64, "bad dtype %d", dtype);
+    return qb::launch_raycast(s, dtype, env_scene, n, o, d, tmin, tmax, t, oid, qb::as_stream(stream));
+}
+
+static int check_cam(const qb_camera *cam) {
+    QB_REQUIRE(cam && cam->width >= 1 && cam->height >= 1, "camera resolution must be >= 1");
+    QB_REQUIRE(cam->max_range > 0, "max_range must be > 0");
+    return QB_OK;
+}
+
+int qb_render(const qb_scene *s, const qb_camera *cam, int32_t dtype, int64_t n, int64_t ld, const void *state,
+              const int32_t *env_scene, void *depth, int32_t *seg, int32_t centroid_id, float *centroid,
+              const float *extra, const int32_t *extra_ids, int32_t n_extra, void *stream) {
+    QB_REQUIRE(s && state && n >= 0 && ld >= n, "qb_render: bad arguments");
+    int rc = check_cam(cam);
+    if (rc) return rc;
+    QB_REQUIRE(dtype == QB_F32 || dtype == QB_F64, "bad dtype %d", dtype);
+    QB_REQUIRE(centroid_id <= 0 || centroid, "centroid buffer missing");
+    QB_REQUIRE(n_extra == 0 || (extra && extra_ids), "extra spheres missing");
+    return qb::launch_render(s, cam, dtype, n, ld, state, nullptr, nullptr, env_scene, depth, seg, centroid_id, centroid,
+                             extra, extra_ids, n_extra, qb::as_stream(stream));
+}
+
+int qb_render_poses(const qb_scene *s, const qb_camera *cam, int32_t dtype, int64_t n, const void *origins,
+                    const void *rotations, const int32_t *env_scene, void *depth, int32_t *seg, void *stream) {
+    QB_REQUIRE(s && origins && rotations && n >= 0, "qb_render_poses: bad arguments");
+    int rc = check_cam(cam);
+    if (rc) return rc;
+    QB_REQUIRE(dtype == QB_F32 || dtype == QB_F64, "bad dtype %d", dtype);
+    return qb::launch_render(s, cam, dtype, n, n, nullptr, origins, rotations, env_scene, depth, seg, 0, nullptr, nullptr,
+                             nullptr, 0, qb::as_stream(stream));
+}
+
+static int check_env(const qb_task *task, const qb_scene *s, const qb_env_buffers *b) {
+    QB_REQUIRE(task && s && b, "env: NULL argument");
+    QB_REQUIRE(b->n >= 0 && b->ld >= b->n, "env: bad n/ld");
+    QB_REQUIRE(b->dtype == QB_F32 || b->dtype == QB_F64, "env: bad dtype");
+    QB_REQUIRE(b->state && b->step_count && b->agent_scene && b->reset_count && b->needs_respawn && b->terminated &&
+                   b->truncated && b->success && b->collision && b->out_of_bounds && b->nonfinite && b->reward &&
+                   b->nearest_dist && b->nearest_pt && b->rng && b->error_count,
+               "env: a required buffer is NULL");
+    QB_REQUIRE(task->scene_perm && task->n_scene_perm >= 1, "env: scene_perm missing");
+    QB_REQUIRE(task->task >= 0 && task->task <= 2, "env: unknown task %d", task->task);
+    return QB_OK;
+}
+
+int qb_env_reset(const qb_params *p, const qb_task *task, const qb_scene *s, const qb_env_buffers *b, uint64_t seed,
+                 void *stream) {
+    QB_REQUIRE(p, "env: NULL params");
+    int rc = check_env(task, s, b);
+    if (rc) return rc;
+    return qb::launch_env(0, p, 0, task, s, b, seed, qb::as_stream(stream));
+}
+
+int qb_env_step(const qb_params *p, int32_t cmd_kind, const qb_task *task, const qb_scene *s, const qb_env_buffers *b,
+                void *stream) {
+    QB_REQUIRE(p, "env: NULL params");
+    int rc = check_env(task, s, b);
+    if (rc) return rc;
+    QB_REQUIRE(b->action, "env: NULL action");
+    return qb::launch_env(1, p, cmd_kind, task, s, b, 0, qb::as_stream(stream));
+}
+
+int qb_env_refresh(const qb_task *task, const qb_scene *s, const qb_env_buffers *b, void *stream) {
+    int rc = check_env(task, s, b);
+    if (rc) return rc;
+    qb_params dummy;
+    std::memset(&dummy, 0, sizeof(dummy));
+    dummy.substeps = 1;
+    dummy.mass = 1.0;
+    for (int k = 0; k < 3; ++k) dummy.inertia[k] = 1.0;
+    dummy.thrust_coeffs[0] = 1.0;
+    return qb::launch_env(2, &dummy, 0, task, s, b, 0, qb::as_stream(stream));
+}
+
+int qb_rng_seed(uint64_t seed, int64_t n, uint64_t *out, void *stream) {
+    QB_REQUIRE(out && n >= 0, "qb_rng_seed: bad arguments");
+    return qb::launch_rng_seed(seed, n, out, qb::as_stream(stream));
+}
+
+int qb_rng_doubles(int64_t n, uint64_t *rng, int32_t k, double *out, void *stream) {
+    QB_REQUIRE(rng && out && n >= 0 && k >= 0, "qb_rng_doubles: bad arguments");
+    return qb::launch_rng_doubles(n, rng, k, out, qb::as_stream(stream));
+}
+
+}  // extern "C"

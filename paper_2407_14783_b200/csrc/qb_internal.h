@@ -1,0 +1,72 @@
+// qb_internal.h -- shared host-side plumbing of libquadb200.so (not public).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+
+#include "../../include/quadb200.h"
+#include "qb_geometry.cuh"
+
+namespace qb {
+
+void set_error(const char *fmt, ...);
+
+inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// grid for a one-env-per-thread kernel: enough blocks for n, at least a
+// couple of waves, never beyond what n needs
+inline int env_grid(long long n, int block) {
+    long long g = (n + block - 1) / block;
+    return (int)(g < 1 ? 1 : (g > 2147483647LL ? 2147483647LL : g));
+}
+
+int check_launch(const char *what);
+
+int sm_count();
+
+}  // namespace qb
+
+#define QB_REQUIRE(cond, ...)          \
+    do {                               \
+        if (!(cond)) {                 \
+            qb::set_error(__VA_ARGS__); \
+            return QB_EINVAL;          \
+        }                              \
+    } while (0)
+
+// scene handle (opaque in the public header)
+struct qb_scene {
+    int device;
+    DevScene dev;
+    long long n_nodes, n_prims;
+    int max_depth;
+    std::string err;
+    void *allocs[16];
+    int n_allocs;
+    double *host_bounds;  // [S][6]
+};
+
+// kernel launchers implemented in the per-kernel translation units
+namespace qb {
+int launch_dynamics_step(const qb_params *p, int kind, int dtype, long long n, long long ld, void *state,
+                         const void *action, void *rotor_out, uint8_t *nonfinite, int T, const void *actions_seq,
+                         cudaStream_t st);
+int launch_command(const qb_params *p, int kind, int dtype, long long n, long long ld, const void *state,
+                   const void *action, void *out, cudaStream_t st);
+int launch_vjp(const qb_params *p, int kind, int dtype, long long n, long long ld, int T, const void *states_tape,
+               const void *actions, const void *g_traj, void *grad_actions, void *grad_init, cudaStream_t st);
+int launch_render(const qb_scene *s, const qb_camera *cam, int dtype, long long n, long long ld, const void *state,
+                  const void *origins, const void *rotations, const int32_t *env_scene, void *depth, int32_t *seg,
+                  int32_t centroid_id, float *centroid, const float *extra, const int32_t *extra_ids, int n_extra,
+                  cudaStream_t st);
+int launch_nearest(const qb_scene *s, const int32_t *env_scene, long long n, const double *q, double *pt, double *dist,
+                   int32_t *oid, cudaStream_t st);
+int launch_raycast(const qb_scene *s, int dtype, const int32_t *env_scene, long long n, const void *o, const void *d,
+                   double tmin, double tmax, void *t, int32_t *oid, cudaStream_t st);
+int launch_env(int mode, const qb_params *p, int kind, const qb_task *task, const qb_scene *s, const qb_env_buffers *b,
+               uint64_t seed, cudaStream_t st);
+int launch_rng_seed(uint64_t seed, long long n, uint64_t *out, cudaStream_t st);
+int launch_rng_doubles(long long n, uint64_t *rng, int k, double *out, cudaStream_t st);
+}  // namespace qb

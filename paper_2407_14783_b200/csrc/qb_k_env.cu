@@ -1,0 +1,314 @@
+// qb_k_env.cu -- K1+K3 fused env step and the device-side reset.
+//
+// One thread per env runs QuadEnvBase.step (env/base.py:156-210) minus the
+// observation render, in reference order:
+//   lazy auto-reset of envs finished last step  base.py:170-173 (+_spawn_agent :114-147)
+//   prev_state <- state                          base.py:175
+//   controller -> dynamics (K1)                  base.py:176-179
+//   non-finite -> freeze at prev_state           base.py:180-185
+//   step_count += 1                              base.py:186
+//   proximity / collision / out-of-bounds        base.py:214-224 (kernels.py:120-182)
+//   task success + reward                        tasks.py:45-56, 97-111
+//   terminated / truncated / needs_respawn       base.py:193-209
+// Proximity, flags and rewards are evaluated in exact double (qb_real.cuh xd)
+// on the stored state, so collision/done flags are bit-identical to the
+// reference evaluated on the same state.  Spawns draw from per-env PCG64
+// streams identical to default_rng(seed + i) (qb_rng.cuh).
+#include "qb_dynamics.cuh"
+#include "qb_geometry.cuh"
+#include "qb_internal.h"
+#include "qb_rng.cuh"
+
+namespace {
+
+template <class R> struct EnvArgs {
+    DynConsts<R> C;
+    qb_task T;
+    qb_env_buffers B;
+    DevScene S;
+};
+
+__device__ __forceinline__ void sample_dist(const qb_dist &d, Pcg64 &r, double *out) {
+    if (d.kind == QB_DIST_FIXED) {
+        for (int k = 0; k < 3; ++k) out[k] = d.a[k];
+    } else if (d.kind == QB_DIST_UNIFORM) {
+        for (int k = 0; k < 3; ++k) out[k] = uniform_draw(r, d.a[k], d.b[k]);
+    } else {
+        for (int k = 0; k < 3; ++k) out[k] = __dadd_rn(d.a[k], __dmul_rn(d.b[k], normal_draw(r)));
+    }
+}
+
+// base.py:313-319 -- qz (x) qy (x) qx from intrinsic roll-pitch-yaw
+__device__ __forceinline__ void quat_from_rpy(const double *rpy, double *q) {
+    double cr = cos(0.5 * rpy[0]), sr = sin(0.5 * rpy[0]);
+    double cp = cos(0.5 * rpy[1]), sp = sin(0.5 * rpy[1]);
+    double cyw = cos(0.5 * rpy[2]), syw = sin(0.5 * rpy[2]);
+    // qy (x) qx with qx = (cr, sr, 0, 0), qy = (cp, 0, sp, 0)
+    xd a0 = xd(cp) * xd(cr), a1 = xd(cp) * xd(sr), a2 = xd(sp) * xd(cr), a3 = -(xd(sp) * xd(sr));
+    // qz (x) a with qz = (cyw, 0, 0, syw)
+    xd w(cyw), z(syw);
+    q[0] = (w * a0 - z * a3).v;
+    q[1] = (w * a1 - z * a2).v;
+    q[2] = (w * a2 + z * a1).v;
+    q[3] = (w * a3 + z * a0).v;
+}
+
+template <class R> __device__ __forceinline__ void hover_state(const DynConsts<R> &C, R *x) {
+#pragma unroll
+    for (int k = 0; k < 17; ++k) x[k] = R(0.0);
+    x[6] = R(1.0);
+#pragma unroll
+    for (int k = 13; k < 17; ++k) x[k] = C.hover_speed;
+}
+
+// base.py:114-147 for env i (shard-local index); returns false on SpawnFailure
+template <class R> __device__ bool spawn(const EnvArgs<R> &A, long long i, R *x) {
+    const qb_task &T = A.T;
+    const qb_env_buffers &B = A.B;
+    const long long gi = B.index_offset + i;
+    const int rc = B.reset_count[i];
+    const int scene = T.scene_perm[(int)((gi + rc) % T.n_scene_perm)];
+    B.agent_scene[i] = scene;
+    B.reset_count[i] = rc + 1;
+    Pcg64 r = pcg_load(B.rng + 4 * i);
+    double pos[3] = {0.0, 0.0, 0.0};
+    bool found = false;
+    for (int k = 0; k < 1000; ++k) {
+        sample_dist(T.spawn[0], r, pos);
+        NearestResult nr = nearest_point(A.S, scene, pos[0], pos[1], pos[2]);
+        if (__dsqrt_rn(nr.d2) < T.min_spawn_clearance) continue;
+        found = true;
+        break;
+    }
+    if (!found) atomicAdd(B.error_count, 1);
+    double vel[3], rpy[3], ang[3], q[4];
+    sample_dist(T.spawn[1], r, vel);
+    sample_dist(T.spawn[2], r, rpy);
+    sample_dist(T.spawn[3], r, ang);
+    quat_from_rpy(rpy, q);
+    for (int k = 0; k < 3; ++k) {
+        x[k] = from_dbl<R>(pos[k]);
+        x[3 + k] = from_dbl<R>(vel[k]);
+        x[10 + k] = from_dbl<R>(ang[k]);
+    }
+    for (int k = 0; k < 4; ++k) {
+        x[6 + k] = from_dbl<R>(q[k]);
+        x[13 + k] = A.C.hover_speed;
+    }
+    B.step_count[i] = 0;
+    pcg_store(B.rng + 4 * i, r);
+    return found;
+}
+
+struct Proximity {
+    double dist, px, py, pz;
+    bool collision, oob;
+};
+
+// base.py:214-224 in exact double
+template <class R> __device__ __forceinline__ Proximity proximity(const EnvArgs<R> &A, int scene, const R *x) {
+    double p[3] = {r_dbl(x[0]), r_dbl(x[1]), r_dbl(x[2])};
+    NearestResult nr = nearest_point(A.S, scene, p[0], p[1], p[2]);
+    Proximity out;
+    out.dist = __dsqrt_rn(nr.d2);
+    out.px = nr.px;
+    out.py = nr.py;
+    out.pz = nr.pz;
+    out.collision = out.dist < A.T.collision_radius;
+    const double *b = A.S.bounds + 6 * scene;
+    bool inside = true;
+    for (int k = 0; k < 3; ++k) {
+        double lo = __dsub_rn(b[k], A.T.bounds_margin), hi = __dadd_rn(b[3 + k], A.T.bounds_margin);
+        inside &= (p[k] >= lo) && (p[k] <= hi);
+    }
+    out.oob = !inside;
+    return out;
+}
+
+__device__ __forceinline__ xd norm3(xd a, xd b, xd c) { return r_sqrt(a * a + b * b + c * c); }
+
+// tasks.py:45-56 (navigation), 97-111 (landing); free: zero reward, no success
+__device__ __forceinline__ void task_eval(const qb_task &T, const double *pp, const double *p, const double *v, double nd,
+                                          bool collision, bool &success, double &reward) {
+    success = false;
+    reward = 0.0;
+    if (T.task == QB_TASK_NAVIGATION) {
+        xd dc = norm3(xd(p[0]) - xd(T.target[0]), xd(p[1]) - xd(T.target[1]), xd(p[2]) - xd(T.target[2]));
+        xd dp = norm3(xd(pp[0]) - xd(T.target[0]), xd(pp[1]) - xd(T.target[1]), xd(pp[2]) - xd(T.target[2]));
+        success = dc < xd(T.success_radius);
+        xd speed2 = xd(v[0]) * xd(v[0]) + xd(v[1]) * xd(v[1]) + xd(v[2]) * xd(v[2]);
+        xd prox = np_clip(xd(1.0) - xd(nd) / xd(T.safe_distance), xd(0.0), xd(1.0));
+        reward = (xd(T.w_progress) * (dp - dc) - xd(T.w_speed) * speed2 - xd(T.w_obstacle) * prox).v;
+    } else if (T.task == QB_TASK_LANDING) {
+        xd h = np_max(xd(p[2]) - xd(T.pad_top) - xd(T.collision_radius), xd(0.0));
+        xd speed2 = xd(v[0]) * xd(v[0]) + xd(v[1]) * xd(v[1]) + xd(v[2]) * xd(v[2]);
+        xd speed = r_sqrt(speed2);
+        xd ox = r_abs(xd(p[0]) - xd(T.pad_center[0])), oy = r_abs(xd(p[1]) - xd(T.pad_center[1]));
+        bool centered = (ox <= xd(T.pad_half)) && (oy <= xd(T.pad_half));
+        success = (h < xd(T.success_height)) && (speed < xd(T.success_speed)) && centered;
+        reward = (xd(-T.w_height) * h + xd(T.w_speed_landing) * r_exp(-speed2) -
+                  xd(T.w_collision) * xd(collision ? 1.0 : 0.0))
+                     .v;
+    }
+}
+
+template <class R> __device__ __forceinline__ void load_state(const EnvArgs<R> &A, long long i, R *x) {
+    using S = typename storage_of<R>::type;
+    const S *st = static_cast<const S *>(A.B.state);
+#pragma unroll
+    for (int k = 0; k < 17; ++k) x[k] = R(st[k * A.B.ld + i]);
+}
+
+template <class R> __device__ __forceinline__ void store_planes(void *dst, long long ld, long long i, const R *x) {
+    using S = typename storage_of<R>::type;
+    S *st = static_cast<S *>(dst);
+#pragma unroll
+    for (int k = 0; k < 17; ++k) st[k * ld + i] = to_store(x[k]);
+}
+
+template <class R>
+__device__ __forceinline__ void write_post(const EnvArgs<R> &A, long long i, const Proximity &pr) {
+    const qb_env_buffers &B = A.B;
+    B.nearest_dist[i] = pr.dist;
+    B.nearest_pt[3 * i] = pr.px;
+    B.nearest_pt[3 * i + 1] = pr.py;
+    B.nearest_pt[3 * i + 2] = pr.pz;
+    B.collision[i] = pr.collision;
+    B.out_of_bounds[i] = pr.oob;
+}
+
+// mode 0: reset, mode 1: proximity refresh only
+template <class R> __global__ void __launch_bounds__(128) k_env_reset(EnvArgs<R> A, uint64_t seed, int mode) {
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const qb_env_buffers &B = A.B;
+    if (i >= B.n) return;
+    R x[17];
+    if (mode == 0) {
+        pcg_store(B.rng + 4 * i, pcg64_from_seed(seed + (uint64_t)(B.index_offset + i)));
+        B.reset_count[i] = 0;
+        hover_state(A.C, x);
+        spawn(A, i, x);
+        store_planes(B.state, B.ld, i, x);
+        if (B.prev_state) store_planes(B.prev_state, B.ld, i, x);
+        B.step_count[i] = 0;
+        B.needs_respawn[i] = 0;
+        B.terminated[i] = 0;
+        B.truncated[i] = 0;
+        B.success[i] = 0;
+        B.nonfinite[i] = 0;
+        B.reward[i] = 0.0f;
+    } else {
+        load_state(A, i, x);
+    }
+    write_post(A, i, proximity(A, B.agent_scene[i], x));
+}
+
+template <class R, int KIND> __global__ void __launch_bounds__(128) k_env_step(EnvArgs<R> A) {
+    using S = typename storage_of<R>::type;
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const qb_env_buffers &B = A.B;
+    const qb_task &T = A.T;
+    if (i >= B.n) return;
+    R x[17];
+    load_state(A, i, x);
+    if (T.auto_reset && B.needs_respawn[i]) spawn(A, i, x);
+    R prev[17];
+#pragma unroll
+    for (int k = 0; k < 17; ++k) prev[k] = x[k];
+    if (B.prev_state) store_planes(B.prev_state, B.ld, i, x);
+
+    R a[4], cmd[4];
+    const S *act = static_cast<const S *>(B.action) + 4 * i;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) a[k] = R(act[k]);
+    command_to_speeds<R, KIND>(A.C, x, a, cmd);
+    const bool ok = dyn_step(A.C, x, cmd);
+    if (!ok) {
+#pragma unroll
+        for (int k = 0; k < 17; ++k) x[k] = prev[k];
+    }
+    const int steps = B.step_count[i] + 1;
+    const int scene = B.agent_scene[i];
+    Proximity pr = proximity(A, scene, x);
+
+    double pp[3] = {r_dbl(prev[0]), r_dbl(prev[1]), r_dbl(prev[2])};
+    double p[3] = {r_dbl(x[0]), r_dbl(x[1]), r_dbl(x[2])};
+    double v[3] = {r_dbl(x[3]), r_dbl(x[4]), r_dbl(x[5])};
+    bool success;
+    double reward;
+    task_eval(T, pp, p, v, pr.dist, pr.collision, success, reward);
+    const bool terminated = success || pr.collision || pr.oob || !ok;
+    const bool truncated = !terminated && steps >= T.episode_max_steps;
+
+    store_planes(B.state, B.ld, i, x);
+    B.step_count[i] = steps;
+    B.nonfinite[i] = !ok;
+    write_post(A, i, pr);
+    B.success[i] = success;
+    B.reward[i] = (float)reward;
+    B.terminated[i] = terminated;
+    B.truncated[i] = truncated;
+    B.needs_respawn[i] = terminated || truncated;
+}
+
+__global__ void k_rng_seed(uint64_t seed, long long n, uint64_t *out) {
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) pcg_store(out + 4 * i, pcg64_from_seed(seed + (uint64_t)i));
+}
+
+__global__ void k_rng_doubles(long long n, uint64_t *rng, int k, double *out) {
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    Pcg64 r = pcg_load(rng + 4 * i);
+    for (int j = 0; j < k; ++j) out[i * k + j] = pcg64_next_double(r);
+    pcg_store(rng + 4 * i, r);
+}
+
+template <class R>
+int dispatch_env(int mode, const qb_params *p, int kind, const qb_task *task, const qb_scene *s, const qb_env_buffers *b,
+                 uint64_t seed, cudaStream_t st) {
+    EnvArgs<R> A;
+    A.C = make_consts<R>(*p);
+    A.T = *task;
+    A.B = *b;
+    A.S = s->dev;
+    const int BS = 128;
+    dim3 g(qb::env_grid(b->n, BS));
+    if (mode == 0 || mode == 2) {
+        k_env_reset<R><<<g, BS, 0, st>>>(A, seed, mode == 0 ? 0 : 1);
+        return qb::check_launch("env_reset");
+    }
+    switch (kind) {
+        case QB_CMD_SRT: k_env_step<R, QB_CMD_SRT><<<g, BS, 0, st>>>(A); break;
+        case QB_CMD_CTBR: k_env_step<R, QB_CMD_CTBR><<<g, BS, 0, st>>>(A); break;
+        case QB_CMD_PS: k_env_step<R, QB_CMD_PS><<<g, BS, 0, st>>>(A); break;
+        case QB_CMD_LV: k_env_step<R, QB_CMD_LV><<<g, BS, 0, st>>>(A); break;
+        case QB_CMD_ROTOR: k_env_step<R, QB_CMD_ROTOR><<<g, BS, 0, st>>>(A); break;
+        default: qb::set_error("unknown command kind %d", kind); return QB_EINVAL;
+    }
+    return qb::check_launch("env_step");
+}
+
+}  // namespace
+
+namespace qb {
+// mode 0 reset, 1 step, 2 refresh
+int launch_env(int mode, const qb_params *p, int kind, const qb_task *task, const qb_scene *s, const qb_env_buffers *b,
+               uint64_t seed, cudaStream_t st) {
+    if (b->n == 0) return QB_OK;
+    if (b->dtype == QB_F32) return dispatch_env<float>(mode, p, kind, task, s, b, seed, st);
+    return dispatch_env<xd>(mode, p, kind, task, s, b, seed, st);
+}
+
+int launch_rng_seed(uint64_t seed, long long n, uint64_t *out, cudaStream_t st) {
+    if (n == 0) return QB_OK;
+    k_rng_seed<<<env_grid(n, 128), 128, 0, st>>>(seed, n, out);
+    return check_launch("rng_seed");
+}
+
+int launch_rng_doubles(long long n, uint64_t *rng, int k, double *out, cudaStream_t st) {
+    if (n == 0) return QB_OK;
+    k_rng_doubles<<<env_grid(n, 128), 128, 0, st>>>(n, rng, k, out);
+    return check_launch("rng_doubles");
+}
+}  // namespace qb

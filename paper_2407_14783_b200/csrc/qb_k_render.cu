@@ -1,0 +1,352 @@
+// qb_k_render.cu -- K2: batched pinhole depth + segmentation ray caster
+// (sensing.render_frames -> kernels.render_batch, kernels.py:402-451), plus
+// the batched nearest-point / raycast queries (kernels.py:120-182, 389-399).
+//
+// FP32 production kernel: one warp renders one camera, tile by tile; a tile
+// is an 8x4 block of pixels, so the warp's 32 rays are coherent and the BVH
+// is walked as a PACKET: the traversal stack and the node sequence are
+// warp-uniform, every lane slab-tests the node against its own ray and the
+// warp descends while any lane still needs the node (__any_sync).  Node and
+// primitive records are warp-broadcast loads through the read-only path, so
+// a small scene lives in L1 and a large one in L2.  Depth (z-depth = t*cz)
+// and the object id come from the same ray and are written together.  The
+// landing task's pad centroid (tasks.py:121-128) is a warp reduction in the
+// epilogue.  No tensor cores: nothing here is a contraction.
+//
+// FP64 validation kernel: one thread per pixel, the reference's exact
+// operation order (qb_real.cuh xd), bit-identical to render_batch except
+// where traversal-order-dependent pruning could matter at the last ulp.
+#include "qb_dynamics.cuh"
+#include "qb_geometry.cuh"
+#include "qb_internal.h"
+
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int TILE_W = 8, TILE_H = 4;
+
+struct CamF {
+    int W, H;
+    float th, tv, max_range;
+    float rot[9];
+    float trans[3];
+};
+
+struct CamD {
+    int W, H;
+    double th, tv, max_range;
+    double rot[9];
+    double trans[3];
+};
+
+// camera pose from the body pose (sensing.py:66-74): origin = p + R(q) t,
+// R_cam->world = to_matrix(q) @ R_cam->body
+template <class R>
+__device__ __forceinline__ void camera_pose(const R *p, const R *q, const R *crot, const R *ctr, R *o, R *Rw) {
+    R m[3][3];
+    q_matrix(q, m);
+    R ox, oy, oz;
+    q_rot<R, 1>(q, ctr[0], ctr[1], ctr[2], ox, oy, oz);
+    o[0] = p[0] + ox;
+    o[1] = p[1] + oy;
+    o[2] = p[2] + oz;
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) Rw[3 * i + k] = m[i][0] * crot[k] + m[i][1] * crot[3 + k] + m[i][2] * crot[6 + k];
+}
+
+template <bool FROM_STATE>
+__global__ void __launch_bounds__(256) k_render_f(DevScene S, CamF cam, long long n, long long ld, const float *state,
+                                                  const float *origins, const float *rotations, const int32_t *env_scene,
+                                                  float *depth, int32_t *seg, int centroid_id, float *centroid,
+                                                  const float *extra, const int32_t *extra_ids, int n_extra) {
+    const int lane = threadIdx.x & 31;
+    const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+    const int W = cam.W, H = cam.H;
+    const int tiles_x = (W + TILE_W - 1) / TILE_W, tiles_y = (H + TILE_H - 1) / TILE_H;
+    const float tmin = 1e-9f;
+
+    for (long long c = warp; c < n; c += nwarps) {
+        float o[3], Rw[9];
+        if (FROM_STATE) {
+            float p[3] = {state[0 * ld + c], state[1 * ld + c], state[2 * ld + c]};
+            float q[4] = {state[6 * ld + c], state[7 * ld + c], state[8 * ld + c], state[9 * ld + c]};
+            camera_pose<float>(p, q, cam.rot, cam.trans, o, Rw);
+        } else {
+#pragma unroll
+            for (int k = 0; k < 3; ++k) o[k] = origins[3 * c + k];
+#pragma unroll
+            for (int k = 0; k < 9; ++k) Rw[k] = rotations[9 * c + k];
+        }
+        const int scene = env_scene ? env_scene[c] : 0;
+        const int root = S.root[scene];
+        long long cnt = 0, sum_col = 0, sum_row = 0;
+
+        for (int tile = 0; tile < tiles_x * tiles_y; ++tile) {
+            const int j = (tile % tiles_x) * TILE_W + (lane & 7);
+            const int i = (tile / tiles_x) * TILE_H + (lane >> 3);
+            const bool valid = (j < W) && (i < H);
+            const float y = (2.0f * (i + 0.5f) / H - 1.0f) * cam.tv;
+            const float x = (2.0f * (j + 0.5f) / W - 1.0f) * cam.th;
+            const float n2 = x * x + y * y + 1.0f;
+            const float cz = rsqrtf(n2);
+            const float cx = x * cz, cy = y * cz;
+            const float dx = Rw[0] * cx + Rw[1] * cy + Rw[2] * cz;
+            const float dy = Rw[3] * cx + Rw[4] * cy + Rw[5] * cz;
+            const float dz = Rw[6] * cx + Rw[7] * cy + Rw[8] * cz;
+            const float ix = 1.0f / dx, iy = 1.0f / dy, iz = 1.0f / dz;
+            const float tmax = cam.max_range * sqrtf(n2);
+            float best = tmax;
+            int bid = -1;
+            bool hit = false;
+
+            int stk[64];
+            int sp = 0;
+            stk[sp++] = root;
+            while (sp > 0) {
+                const int node = stk[--sp];
+                const float4 lo = __ldg(S.nodef + 2 * node), hi = __ldg(S.nodef + 2 * node + 1);
+                const float e = slab_enter_f(lo, hi, o[0], o[1], o[2], ix, iy, iz, best);
+                if (!__any_sync(FULL, valid && e <= best)) continue;
+                const int a = __float_as_int(lo.w), b = __float_as_int(hi.w);
+                if (b > 0) {
+                    for (int p = a; p < a + b; ++p) {
+                        const int2 m = __ldg(S.meta + p);
+                        const float4 *pr = S.primf + 4 * p;
+                        float t;
+                        if (m.x == QB_SPHERE)
+                            t = ray_sphere_f(pr, o[0], o[1], o[2], dx, dy, dz, tmin, best);
+                        else if (m.x == QB_BOX)
+                            t = ray_box_f(pr, o[0], o[1], o[2], dx, dy, dz, tmin, best);
+                        else
+                            t = ray_triangle_f(pr, o[0], o[1], o[2], dx, dy, dz, tmin, best);
+                        if (t > 0.0f && (t < best || !hit || (t == best && m.y < bid))) {
+                            best = t;
+                            bid = m.y;
+                            hit = true;
+                        }
+                    }
+                } else {
+                    const int axis = -b;
+                    const float dc = axis == 0 ? dx : (axis == 1 ? dy : dz);
+                    const bool left_first = __popc(__ballot_sync(FULL, dc >= 0.0f)) >= 16;
+                    stk[sp++] = left_first ? a + 1 : a;  // far child first
+                    stk[sp++] = left_first ? a : a + 1;
+                }
+            }
+            float t = hit ? best : -1.0f;
+            int oid = hit ? bid : -1;
+            if (n_extra > 0) {  // swarm agents as spheres (kernels.py:438-445)
+                for (int k = 0; k < n_extra; ++k) {
+                    const float4 sph = *reinterpret_cast<const float4 *>(extra + (c * n_extra + k) * 4);
+                    float4 rec[2] = {sph, make_float4(sph.w * sph.w, 0.f, 0.f, 0.f)};
+                    float ts = ray_sphere_f(rec, o[0], o[1], o[2], dx, dy, dz, tmin, tmax);
+                    if (ts > 0.0f && (t < 0.0f || ts < t)) {
+                        t = ts;
+                        oid = extra_ids[c * n_extra + k];
+                    }
+                }
+            }
+            const int out_id = t > 0.0f ? oid : 0;
+            if (valid) {
+                const long long off = (c * H + i) * (long long)W + j;
+                if (depth) depth[off] = t > 0.0f ? t * cz : cam.max_range;
+                if (seg) seg[off] = out_id;
+                if (centroid_id > 0 && out_id == centroid_id) {
+                    cnt += 1;
+                    sum_col += j;
+                    sum_row += i;
+                }
+            }
+        }
+        if (centroid_id > 0) {
+#pragma unroll
+            for (int s = 16; s > 0; s >>= 1) {
+                cnt += __shfl_xor_sync(FULL, cnt, s);
+                sum_col += __shfl_xor_sync(FULL, sum_col, s);
+                sum_row += __shfl_xor_sync(FULL, sum_row, s);
+            }
+            if (lane == 0) {
+                centroid[2 * c] = cnt ? (float)((double)sum_col / (double)cnt) : -1.0f;
+                centroid[2 * c + 1] = cnt ? (float)((double)sum_row / (double)cnt) : -1.0f;
+            }
+        }
+    }
+}
+
+// exact-double validation renderer: one thread per pixel, reference order
+template <bool FROM_STATE>
+__global__ void __launch_bounds__(128) k_render_x(DevScene S, CamD cam, long long n, long long ld, const double *state,
+                                                  const double *origins, const double *rotations,
+                                                  const int32_t *env_scene, double *depth, int32_t *seg,
+                                                  int centroid_id, float *centroid) {
+    const long long pix = (long long)cam.W * cam.H;
+    const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid >= n * pix) return;
+    const long long c = gid / pix;
+    const int i = (int)((gid % pix) / cam.W), j = (int)(gid % cam.W);
+    xd o[3], Rw[9];
+    if (FROM_STATE) {
+        xd p[3] = {xd(state[0 * ld + c]), xd(state[1 * ld + c]), xd(state[2 * ld + c])};
+        xd q[4] = {xd(state[6 * ld + c]), xd(state[7 * ld + c]), xd(state[8 * ld + c]), xd(state[9 * ld + c])};
+        xd cr[9], ct[3];
+        for (int k = 0; k < 9; ++k) cr[k] = xd(cam.rot[k]);
+        for (int k = 0; k < 3; ++k) ct[k] = xd(cam.trans[k]);
+        camera_pose<xd>(p, q, cr, ct, o, Rw);
+    } else {
+        for (int k = 0; k < 3; ++k) o[k] = xd(origins[3 * c + k]);
+        for (int k = 0; k < 9; ++k) Rw[k] = xd(rotations[9 * c + k]);
+    }
+    // kernels.py:423-437
+    xd y = (xd(2.0) * (xd((double)i) + xd(0.5)) / xd((double)cam.H) - xd(1.0)) * xd(cam.tv);
+    xd x = (xd(2.0) * (xd((double)j) + xd(0.5)) / xd((double)cam.W) - xd(1.0)) * xd(cam.th);
+    xd norm = r_sqrt(x * x + y * y + xd(1.0));
+    xd cz = xd(1.0) / norm;
+    xd cx = x * cz, cy = y * cz;
+    xd dx = Rw[0] * cx + Rw[1] * cy + Rw[2] * cz;
+    xd dy = Rw[3] * cx + Rw[4] * cy + Rw[5] * cz;
+    xd dz = Rw[6] * cx + Rw[7] * cy + Rw[8] * cz;
+    xd tmax = xd(cam.max_range) / cz;
+    int oid;
+    double t = raycast_x(S, env_scene ? env_scene[c] : 0, o[0].v, o[1].v, o[2].v, dx.v, dy.v, dz.v, 1e-9, tmax.v, oid);
+    const long long off = c * pix + (long long)i * cam.W + j;
+    if (depth) depth[off] = t > 0.0 ? (xd(t) * cz).v : cam.max_range;
+    if (seg) seg[off] = t > 0.0 ? oid : 0;
+    (void)centroid_id;
+    (void)centroid;
+}
+
+// centroid pass for the validation renderer (reads back its own seg)
+__global__ void k_centroid(long long n, int W, int H, const int32_t *seg, int id, float *centroid) {
+    long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= n) return;
+    long long cnt = 0, sc = 0, sr = 0;
+    for (int i = 0; i < H; ++i)
+        for (int j = 0; j < W; ++j)
+            if (seg[(c * H + i) * (long long)W + j] == id) {
+                ++cnt;
+                sc += j;
+                sr += i;
+            }
+    centroid[2 * c] = cnt ? (float)((double)sc / (double)cnt) : -1.0f;
+    centroid[2 * c + 1] = cnt ? (float)((double)sr / (double)cnt) : -1.0f;
+}
+
+__global__ void k_nearest(DevScene S, const int32_t *env_scene, long long n, const double *q, double *pt, double *dist,
+                          int32_t *oid) {
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    NearestResult r = nearest_point(S, env_scene ? env_scene[i] : 0, q[3 * i], q[3 * i + 1], q[3 * i + 2]);
+    if (pt) {
+        pt[3 * i] = r.px;
+        pt[3 * i + 1] = r.py;
+        pt[3 * i + 2] = r.pz;
+    }
+    if (dist) dist[i] = __dsqrt_rn(r.d2);
+    if (oid) oid[i] = r.oid;
+}
+
+template <class S_>
+__global__ void k_raycast(DevScene S, const int32_t *env_scene, long long n, const S_ *o, const S_ *d, double tmin,
+                          double tmax, S_ *t, int32_t *oid) {
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int id;
+    int sc = env_scene ? env_scene[i] : 0;
+    if constexpr (sizeof(S_) == 4) {
+        t[i] = raycast_f(S, sc, o[3 * i], o[3 * i + 1], o[3 * i + 2], d[3 * i], d[3 * i + 1], d[3 * i + 2], (float)tmin,
+                         (float)tmax, id);
+    } else {
+        t[i] = raycast_x(S, sc, o[3 * i], o[3 * i + 1], o[3 * i + 2], d[3 * i], d[3 * i + 1], d[3 * i + 2], tmin, tmax, id);
+    }
+    if (oid) oid[i] = id;
+}
+
+}  // namespace
+
+namespace qb {
+
+int launch_render(const qb_scene *s, const qb_camera *cam, int dtype, long long n, long long ld, const void *state,
+                  const void *origins, const void *rotations, const int32_t *env_scene, void *depth, int32_t *seg,
+                  int32_t centroid_id, float *centroid, const float *extra, const int32_t *extra_ids, int n_extra,
+                  cudaStream_t st) {
+    if (n == 0) return QB_OK;
+    if (dtype == QB_F32) {
+        CamF c;
+        c.W = cam->width;
+        c.H = cam->height;
+        c.th = (float)cam->tan_half_h;
+        c.tv = (float)cam->tan_half_v;
+        c.max_range = (float)cam->max_range;
+        for (int k = 0; k < 9; ++k) c.rot[k] = (float)cam->rotation[k];
+        for (int k = 0; k < 3; ++k) c.trans[k] = (float)cam->translation[k];
+        const int B = 256;
+        long long warps_needed = n;
+        long long max_blocks = (long long)sm_count() * 8;  // 8 blocks x 8 warps resident per SM
+        long long blocks = (warps_needed * 32 + B - 1) / B;
+        if (blocks > max_blocks) blocks = max_blocks;
+        if (state)
+            k_render_f<true><<<(int)blocks, B, 0, st>>>(s->dev, c, n, ld, (const float *)state, nullptr, nullptr, env_scene,
+                                                        (float *)depth, seg, centroid_id, centroid, extra, extra_ids, n_extra);
+        else
+            k_render_f<false><<<(int)blocks, B, 0, st>>>(s->dev, c, n, ld, nullptr, (const float *)origins,
+                                                         (const float *)rotations, env_scene, (float *)depth, seg, 0, nullptr,
+                                                         nullptr, nullptr, 0);
+        return check_launch("render_f32");
+    }
+    CamD c;
+    c.W = cam->width;
+    c.H = cam->height;
+    c.th = cam->tan_half_h;
+    c.tv = cam->tan_half_v;
+    c.max_range = cam->max_range;
+    for (int k = 0; k < 9; ++k) c.rot[k] = cam->rotation[k];
+    for (int k = 0; k < 3; ++k) c.trans[k] = cam->translation[k];
+    long long total = n * (long long)c.W * c.H;
+    const int B = 128;
+    int blocks = (int)((total + B - 1) / B);
+    if (n_extra > 0) {
+        set_error("extra spheres are only supported by the FP32 renderer");
+        return QB_EINVAL;
+    }
+    if (state)
+        k_render_x<true><<<blocks, B, 0, st>>>(s->dev, c, n, ld, (const double *)state, nullptr, nullptr, env_scene,
+                                              (double *)depth, seg, centroid_id, centroid);
+    else
+        k_render_x<false><<<blocks, B, 0, st>>>(s->dev, c, n, ld, nullptr, (const double *)origins,
+                                               (const double *)rotations, env_scene, (double *)depth, seg, 0, nullptr);
+    int rc = check_launch("render_f64");
+    if (rc) return rc;
+    if (centroid_id > 0) {
+        if (!seg) {
+            set_error("centroid needs a seg buffer in the FP64 renderer");
+            return QB_EINVAL;
+        }
+        k_centroid<<<env_grid(n, 128), 128, 0, st>>>(n, c.W, c.H, seg, centroid_id, centroid);
+        return check_launch("centroid");
+    }
+    return QB_OK;
+}
+
+int launch_nearest(const qb_scene *s, const int32_t *env_scene, long long n, const double *q, double *pt, double *dist,
+                   int32_t *oid, cudaStream_t st) {
+    if (n == 0) return QB_OK;
+    k_nearest<<<env_grid(n, 128), 128, 0, st>>>(s->dev, env_scene, n, q, pt, dist, oid);
+    return check_launch("nearest_point");
+}
+
+int launch_raycast(const qb_scene *s, int dtype, const int32_t *env_scene, long long n, const void *o, const void *d,
+                   double tmin, double tmax, void *t, int32_t *oid, cudaStream_t st) {
+    if (n == 0) return QB_OK;
+    if (dtype == QB_F32)
+        k_raycast<float><<<env_grid(n, 128), 128, 0, st>>>(s->dev, env_scene, n, (const float *)o, (const float *)d, tmin,
+                                                           tmax, (float *)t, oid);
+    else
+        k_raycast<double><<<env_grid(n, 128), 128, 0, st>>>(s->dev, env_scene, n, (const double *)o, (const double *)d,
+                                                            tmin, tmax, (double *)t, oid);
+    return check_launch("raycast");
+}
+
+}  // namespace qb

@@ -261,7 +261,20 @@ template <class R> QB_D void mixer(const DynConsts<R> &C, R force, const R *tq, 
     }
     R scale = np_max(np_min(np_min(up_min, dn_min), R(1.0)), R(0.0));
 #pragma unroll
-    for (int i = 0; i < 4; ++i) thr[i] = np_clip(base[i] + scale * tp[i], C.flo, C.fhi);
+    for (int i = 0; i < 4; ++i) {
+        R f = base[i] + scale * tp[i];
+        if constexpr (!is_exact<R>::value) {
+            // A rotor the torque scale saturates lands on its thrust bound up to
+            // the rounding of base + s*tp (~1e-7 N in FP32), and the thrust-curve
+            // inverse sqrt(f/k2) turns that into ~0.2 rad/s near f_lo = 0.  Snap
+            // values within a few ulps of the operands onto the bound: exact in
+            // real arithmetic, and what FP64 rounding gives the reference.
+            R tol = R(4e-7) * (r_abs(base[i]) + r_abs(scale * tp[i]));
+            if (r_abs(f - C.flo) <= tol) f = C.flo;
+            if (r_abs(f - C.fhi) <= tol) f = C.fhi;
+        }
+        thr[i] = np_clip(f, C.flo, C.fhi);
+    }
 }
 
 // control.py:138-158

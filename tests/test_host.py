@@ -1,0 +1,143 @@
+"""CPU-only tests of the host side: generators, constant folding, configs,
+and the C-ABI library surface (loads and exports every declared symbol; no
+compute calls without a GPU)."""
+
+import ctypes
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import ROOT, golden
+from paper_2407_14783_b200 import _native as nat
+from paper_2407_14783_b200.errors import ConfigError
+from paper_2407_14783_b200.geometry import (AABB, Box, Scene, SceneObject, Sphere, TriMesh, gap_scene, garage_scene,
+                                            generate_cluttered_scene, indoor_mesh_scene, landing_scene)
+from paper_2407_14783_b200.params import ControllerGains, QuadParams, SimConfig, native_params
+
+
+@pytest.mark.parametrize("name,make", [
+    ("nav", lambda: generate_cluttered_scene(0, AABB([-5, -5, 0], [5, 5, 4]), 0.15)),
+    ("landing", landing_scene), ("garage", garage_scene), ("gap", lambda: gap_scene(1.0)),
+    ("garage10", lambda: garage_scene(AABB([-5, -5, 0], [5, 5, 4]))),
+])
+def test_scene_generators_reproduce_reference(ggeo, name, make):
+    t = make().arrays
+    for ours, key in ((t.prim_type, "prim_type"), (t.prim_data, "prim_data"), (t.prim_object_id, "prim_oid"),
+                      (t.prim_aabb_lo, "prim_lo"), (t.prim_aabb_hi, "prim_hi")):
+        assert np.array_equal(ours, ggeo[f"{name}_{key}"]), key
+    b = make().bounds
+    assert np.array_equal(np.stack([b.lo, b.hi]), ggeo[f"{name}_bounds"])
+
+
+def test_trimesh_flatten_matches_reference(ggeo):
+    # the golden "tess" scene is TriMesh-only; re-flatten its triangles through our Scene
+    tri = ggeo["tess_prim_data"][:, :9].reshape(-1, 3, 3)
+    oid = ggeo["tess_prim_oid"]
+    objs = []
+    for o in np.unique(oid):
+        t = tri[oid == o]
+        objs.append(SceneObject(int(o), TriMesh(t.reshape(-1, 3), np.arange(3 * len(t)).reshape(-1, 3))))
+    a = Scene(objs).arrays
+    assert np.array_equal(a.prim_data, ggeo["tess_prim_data"])
+    assert np.array_equal(a.prim_aabb_lo, ggeo["tess_prim_lo"]) and np.array_equal(a.prim_aabb_hi, ggeo["tess_prim_hi"])
+
+
+def test_indoor_mesh_scene_size():
+    s = indoor_mesh_scene(seed=0, target_triangles=60_000)
+    n = len(s.arrays)
+    assert 55_000 <= n <= 60_000
+    assert 9 in {o.id for o in s.objects}  # landing pad id (generate.py PAD_ID)
+
+
+@pytest.mark.parametrize("sim", [SimConfig(), SimConfig(integrator="euler", substeps=4), SimConfig(control_dt=0.01, substeps=3)])
+def test_native_params_equal_oracle_folding(sim):
+    ours = native_params(QuadParams(), sim, ControllerGains())
+    ref = oracle.pack_params(QuadParams(), sim, ControllerGains())
+    assert bytes(ours) == bytes(ref)
+
+
+def test_hover_speed_matches_reference(gdyn):
+    assert QuadParams().hover_speed == float(gdyn["hover_speed"])
+
+
+def test_config_validation():
+    from paper_2407_14783_b200.env import DistSpec, EnvConfig, SceneSpec, SensorSpec, env_config_from_table
+
+    with pytest.raises(ConfigError):
+        EnvConfig(num_agents=0)
+    with pytest.raises(ConfigError):
+        EnvConfig(mode="swarm", scenes=(SceneSpec(), SceneSpec()))
+    with pytest.raises(ConfigError):
+        DistSpec("uniform", low=[1, 1, 1], high=[0, 0, 0])
+    with pytest.raises(ConfigError):
+        SensorSpec(kind="lidar")
+    with pytest.raises(ConfigError):
+        env_config_from_table({"num_agents": 2, "bogus": 1})
+    with pytest.raises(ConfigError):
+        QuadParams(mass=-1.0)
+    cfg = env_config_from_table({"num_agents": 3, "task": "navigation", "command_type": "lv",
+                                 "scenes": [{"kind": "cluttered", "seed": 2}],
+                                 "randomization": {"position": {"kind": "uniform", "low": [0, 0, 1], "high": [1, 1, 2]}},
+                                 "sensors": [{"kind": "depth", "width": 32, "height": 16}]})
+    assert cfg.num_agents == 3 and cfg.sensors[0].camera().width == 32
+
+
+def _header_functions():
+    text = open(os.path.join(ROOT, "include", "quadb200.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(qb_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    path = nat.LIB_PATH
+    assert os.path.exists(path), "build libquadb200.so first (python -m paper_2407_14783_b200.build)"
+    lib = ctypes.CDLL(path)  # loading needs no GPU
+    declared = _header_functions()
+    assert declared, "no declarations parsed"
+    for name in declared:
+        assert hasattr(lib, name), f"{name} declared in include/quadb200.h but not exported"
+        assert name in nat.SIGNATURES, f"{name} has no ctypes signature"
+    assert set(nat.SIGNATURES) == set(declared)
+    lib.qb_last_error.restype = ctypes.c_char_p
+    assert lib.qb_version() == 1
+
+
+def test_ctypes_struct_layouts_match_c():
+    src = os.path.join(ROOT, "include")
+    prog = ("#include <stdio.h>\n#include <stddef.h>\n#include \"quadb200.h\"\n"
+            "int main(){printf(\"%zu %zu %zu %zu %zu %zu %zu\\n\", sizeof(qb_params), sizeof(qb_task), sizeof(qb_env_buffers),"
+            " sizeof(qb_camera), sizeof(qb_dist), offsetof(qb_params, substeps), offsetof(qb_task, target));}\n")
+    exe = "/tmp/qb_layout"
+    cc = "/usr/bin/gcc" if os.path.exists("/usr/bin/gcc") else "gcc"
+    r = subprocess.run([cc, "-x", "c", "-I", src, "-o", exe, "-"], input=prog, text=True, capture_output=True)
+    assert r.returncode == 0, r.stderr
+    got = [int(x) for x in subprocess.run([exe], capture_output=True, text=True).stdout.split()]
+    want = [ctypes.sizeof(nat.QbParams), ctypes.sizeof(nat.QbTask), ctypes.sizeof(nat.QbEnvBuffers),
+            ctypes.sizeof(nat.QbCamera), ctypes.sizeof(nat.QbDist), nat.QbParams.substeps.offset, nat.QbTask.target.offset]
+    assert got == want
+
+
+def test_product_has_no_cpu_fallback(monkeypatch):
+    """The package must fail loudly (not silently fall back) without CUDA."""
+    import torch
+
+    from paper_2407_14783_b200.errors import NativeError
+
+    monkeypatch.setattr(torch.cuda, "is_available", lambda: False)
+    from paper_2407_14783_b200.env import make_env, navigation_config
+
+    with pytest.raises(NativeError):
+        make_env(navigation_config(num_agents=2))
+
+
+def test_oracle_is_not_imported_by_product():
+    pkg = os.path.join(ROOT, "paper_2407_14783_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith(".py"):
+                src = open(os.path.join(dirpath, f)).read()
+                assert not re.search(r"^\s*(import oracle|from oracle)", src, flags=re.M), f

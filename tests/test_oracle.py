@@ -125,8 +125,12 @@ def test_render_exact(ggeo, name, cam):
 
 def _replay(gname, config, seed, scene_names):
     g = golden(gname)
-    ggeo = golden("geometry")
-    scenes = [scene_from_golden(ggeo, n) for n in scene_names]
+    # the config's own scenes (SceneSpec volumes), flattened by the generator
+    # that test_host pins bit-exact to the reference generator
+    scenes = []
+    for spec in config.scenes:
+        t = spec.materialize().arrays
+        scenes.append(oracle.OracleScene(t.prim_type, t.prim_data, t.prim_object_id, t.prim_aabb_lo, t.prim_aabb_hi))
     env = OracleEnv(config, scenes, QuadParams(), SimConfig(), ControllerGains())
     obs = env.reset(seed=seed)
     assert np.array_equal(obs["state"], g["reset_state"])

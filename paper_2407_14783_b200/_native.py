@@ -64,6 +64,8 @@ class QbCamera(ctypes.Structure):
         ("max_range", ctypes.c_double),
         ("rotation", ctypes.c_double * 9),
         ("translation", c_double3),
+        ("mode", ctypes.c_int32),
+        ("pad_", ctypes.c_int32),
     ]
 
 

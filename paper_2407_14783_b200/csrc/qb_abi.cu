@@ -198,6 +198,28 @@ static float f_up(double v) {
 }
 
 static float4 f4(float x, float y, float z, float w) { return make_float4(x, y, z, w); }
+
+// conservative culling bounds of one primitive (see DevScene::primc)
+static void cull_record(int type, const double *d, float4 *o) {
+    for (int k = 0; k < 4; ++k) o[k] = f4(0, 0, 0, 0);
+    if (type == QB_SPHERE) {
+        o[0] = f4((float)d[0], (float)d[1], (float)d[2], (float)(d[3] * (1.0 + 1e-6)));
+    } else if (type == QB_BOX) {
+        o[0] = f4((float)d[0], (float)d[1], (float)d[2], 0.0f);
+        for (int k = 0; k < 3; ++k)  // column k of R scaled by h_k
+            o[1 + k] = f4((float)(d[6 + k] * d[3 + k] * (1.0 + 1e-6)), (float)(d[9 + k] * d[3 + k] * (1.0 + 1e-6)),
+                          (float)(d[12 + k] * d[3 + k] * (1.0 + 1e-6)), 0.0f);
+    } else {  // triangle: bounding sphere about the centroid
+        double c[3], r2 = 0.0;
+        for (int a = 0; a < 3; ++a) c[a] = (d[a] + d[3 + a] + d[6 + a]) / 3.0;
+        for (int v = 0; v < 3; ++v) {
+            double e = 0.0;
+            for (int a = 0; a < 3; ++a) e += (d[3 * v + a] - c[a]) * (d[3 * v + a] - c[a]);
+            r2 = std::max(r2, e);
+        }
+        o[0] = f4((float)c[0], (float)c[1], (float)c[2], (float)(std::sqrt(r2) * (1.0 + 1e-6)));
+    }
+}
 static float i2f(int a) {
     float f;
     std::memcpy(&f, &a, 4);
@@ -313,6 +335,9 @@ int qb_scene_create(int32_t n_scenes, const int64_t *prim_offsets, const int64_t
     std::vector<float4> primf(4 * (size_t)P);
     std::vector<double> primd(16 * (size_t)P);
     std::vector<int2> meta(P);
+    std::vector<float4> primc(4 * (size_t)P);
+    std::vector<int> prim_offset(n_scenes + 1);
+    for (int s = 0; s <= n_scenes; ++s) prim_offset[s] = (int)prim_offsets[s];
     int max_depth = 0;
     for (int s = 0; s < n_scenes; ++s) {
         const long long off = prim_offsets[s], cnt = prim_offsets[s + 1] - off;
@@ -346,6 +371,7 @@ int qb_scene_create(int32_t n_scenes, const int64_t *prim_offsets, const int64_t
         for (long long j = 0; j < cnt; ++j) {
             long long src = off + order[j], dst = off + j;
             qb::pack_prim((int)prim_type[src], prim_data + 16 * src, &primf[4 * dst]);
+            qb::cull_record((int)prim_type[src], prim_data + 16 * src, &primc[4 * dst]);
             std::memcpy(&primd[16 * dst], prim_data + 16 * src, 16 * sizeof(double));
             QB_REQUIRE(prim_oid[src] > 0 && prim_oid[src] < (1LL << 31), "object ids must be positive int32");
             meta[dst] = make_int2((int)prim_type[src], (int)prim_oid[src]);
@@ -357,6 +383,9 @@ int qb_scene_create(int32_t n_scenes, const int64_t *prim_offsets, const int64_t
     sc->n_nodes = (long long)nodei.size();
     sc->n_prims = P;
     sc->max_depth = max_depth;
+    sc->max_scene_prims = 0;
+    for (int s = 0; s < n_scenes; ++s)
+        sc->max_scene_prims = std::max(sc->max_scene_prims, (int)(prim_offsets[s + 1] - prim_offsets[s]));
     sc->host_bounds = new double[6 * n_scenes];
     std::memcpy(sc->host_bounds, bounds.data(), sizeof(double) * 6 * n_scenes);
     DevScene &d = sc->dev;
@@ -370,7 +399,10 @@ int qb_scene_create(int32_t n_scenes, const int64_t *prim_offsets, const int64_t
     d.primf = qb::dev_upload(sc, primf);
     d.primd = qb::dev_upload(sc, primd);
     d.meta = qb::dev_upload(sc, meta);
-    if (!d.root || !d.bounds || !d.nodef || !d.noded || !d.nodei || !d.primf || !d.primd || !d.meta) {
+    d.prim_offset = qb::dev_upload(sc, prim_offset);
+    d.primc = qb::dev_upload(sc, primc);
+    if (!d.root || !d.bounds || !d.nodef || !d.noded || !d.nodei || !d.primf || !d.primd || !d.meta || !d.prim_offset ||
+        !d.primc) {
         qb::set_error("scene upload failed: %s", cudaGetErrorString(cudaGetLastError()));
         qb_scene_destroy(sc);
         return QB_ENOMEM;

@@ -25,9 +25,12 @@ struct DevScene {
     const float4 *nodef;    // [M][2] (lo.xyz, a) (hi.xyz, b) -- float, bounds rounded outward
     const double *noded;    // [M][6] lo.xyz hi.xyz (exact double)
     const int2 *nodei;      // [M] (a, b): b>0 leaf {first=a,count=b}; b<=0 internal {left=a, axis=-b}
-    const float4 *primf;    // [P][4] float prim records (see qb_bvh.cpp pack_prims)
+    const float4 *primf;    // [P][4] float prim records (see qb_abi.cu pack_prim)
     const double *primd;    // [P][16] reference prim_data rows
     const int2 *meta;       // [P] (type, object id)
+    const int *prim_offset; // [S+1] first primitive of each scene (BVH order)
+    const float4 *primc;    // [P][4] culling bounds: (centre, r) (A0, 0) (A1, 0) (A2, 0);
+                            // support along unit n = r + sum_k |n . A_k| (A_k = box half-axes)
 };
 
 #ifdef __CUDACC__

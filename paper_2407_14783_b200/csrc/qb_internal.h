@@ -43,7 +43,8 @@ struct qb_scene {
     long long n_nodes, n_prims;
     int max_depth;
     std::string err;
-    void *allocs[16];
+    void *allocs[32];
+    int max_scene_prims;  // largest scene of the set (selects the culling renderer)
     int n_allocs;
     double *host_bounds;  // [S][6]
 };

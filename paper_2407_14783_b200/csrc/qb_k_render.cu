@@ -2,9 +2,12 @@
 // (sensing.render_frames -> kernels.render_batch, kernels.py:402-451), plus
 // the batched nearest-point / raycast queries (kernels.py:120-182, 389-399).
 //
-// FP32 production kernel: one warp renders one camera, tile by tile; a tile
-// is an 8x4 block of pixels, so the warp's 32 rays are coherent and the BVH
-// is walked as a PACKET: the traversal stack and the node sequence are
+// FP32 production kernels (one warp renders one camera, tile by tile; a tile
+// is an 8x4 block of pixels, so the warp's 32 rays are coherent):
+//   k_render_cull  scenes of <= 512 primitives: two-level frustum culling
+//                  (camera, then tile) and warp-uniform ray tests of the few
+//                  survivors -- see the comment above the kernel;
+//   k_render_f     any scene: the BVH is walked as a PACKET: the traversal stack and the node sequence are
 // warp-uniform, every lane slab-tests the node against its own ray and the
 // warp descends while any lane still needs the node (__any_sync).  Node and
 // primitive records are warp-broadcast loads through the read-only path, so
@@ -176,6 +179,188 @@ __global__ void __launch_bounds__(256) k_render_f(DevScene S, CamF cam, long lon
     }
 }
 
+// ---------------------------------------------------------------------------
+// Culling renderer for small scenes (<= CULL_MAX primitives per scene, e.g.
+// the 69-primitive navigation room): instead of walking a BVH per ray, a warp
+// culls the scene against its camera frustum once (lane-parallel over
+// primitives, 6 plane/support tests), then for every 8x4 tile culls that
+// candidate list against the tile's 4 side planes (lane-parallel again) and
+// ray-tests only the survivors, warp-uniformly.  The culling is
+// conservative (support functions of spheres / OBBs / triangle bounding
+// spheres, 1 mm margin), and the per-pixel result -- nearest t, ties to the
+// lowest id -- does not depend on the order primitives are tested in, so
+// the output is identical to the BVH kernel's.
+constexpr int CULL_MAX = 512;
+constexpr int CULL_WARPS = 8;
+constexpr float CULL_EPS = 1e-3f;
+
+struct Plane {
+    float x, y, z, off;
+};
+
+__device__ __forceinline__ Plane world_plane(const float *Rw, float cx, float cy, float cz, float off) {
+    const float inv = rsqrtf(cx * cx + cy * cy + cz * cz);
+    cx *= inv; cy *= inv; cz *= inv;
+    return {Rw[0] * cx + Rw[1] * cy + Rw[2] * cz, Rw[3] * cx + Rw[4] * cy + Rw[5] * cz, Rw[6] * cx + Rw[7] * cy + Rw[8] * cz,
+            off};
+}
+
+// keep unless the primitive's support along the plane normal is fully outside
+__device__ __forceinline__ bool keep(const Plane &P, float rx, float ry, float rz, float4 c, float4 a0, float4 a1, float4 a2) {
+    const float d = P.x * rx + P.y * ry + P.z * rz + P.off;
+    const float s = c.w + fabsf(P.x * a0.x + P.y * a0.y + P.z * a0.z) + fabsf(P.x * a1.x + P.y * a1.y + P.z * a1.z) +
+                    fabsf(P.x * a2.x + P.y * a2.y + P.z * a2.z);
+    return d + s >= -CULL_EPS;
+}
+
+template <bool FROM_STATE>
+__global__ void __launch_bounds__(CULL_WARPS * 32) k_render_cull(DevScene S, CamF cam, long long n, long long ld,
+                                                                 const float *state, const float *origins,
+                                                                 const float *rotations, const int32_t *env_scene,
+                                                                 float *depth, int32_t *seg, int centroid_id,
+                                                                 float *centroid, const float *extra,
+                                                                 const int32_t *extra_ids, int n_extra) {
+    __shared__ int cand_s[CULL_WARPS][CULL_MAX];
+    int *cand = cand_s[threadIdx.x >> 5];
+    const int lane = threadIdx.x & 31;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+    const int W = cam.W, H = cam.H;
+    const int tiles_x = (W + TILE_W - 1) / TILE_W, tiles_y = (H + TILE_H - 1) / TILE_H;
+    const float tmin = 1e-9f;
+
+    for (long long c = warp; c < n; c += nwarps) {
+        float o[3], Rw[9];
+        if (FROM_STATE) {
+            float p[3] = {state[0 * ld + c], state[1 * ld + c], state[2 * ld + c]};
+            float q[4] = {state[6 * ld + c], state[7 * ld + c], state[8 * ld + c], state[9 * ld + c]};
+            camera_pose<float>(p, q, cam.rot, cam.trans, o, Rw);
+        } else {
+#pragma unroll
+            for (int k = 0; k < 3; ++k) o[k] = origins[3 * c + k];
+#pragma unroll
+            for (int k = 0; k < 9; ++k) Rw[k] = rotations[9 * c + k];
+        }
+        const int scene = env_scene ? env_scene[c] : 0;
+        const int p0 = S.prim_offset[scene], p1 = S.prim_offset[scene + 1];
+
+        // ---- camera frustum culling (image frustum, near z >= 0, far z <= max_range)
+        const Plane cp[6] = {world_plane(Rw, 1.f, 0.f, cam.th, 0.f), world_plane(Rw, -1.f, 0.f, cam.th, 0.f),
+                             world_plane(Rw, 0.f, 1.f, cam.tv, 0.f), world_plane(Rw, 0.f, -1.f, cam.tv, 0.f),
+                             world_plane(Rw, 0.f, 0.f, 1.f, 0.f), world_plane(Rw, 0.f, 0.f, -1.f, cam.max_range)};
+        int ncand = 0;
+        for (int b = p0; b < p1; b += 32) {
+            const int p = b + lane;
+            bool k = false;
+            if (p < p1) {
+                const float4 *cr = S.primc + 4 * p;
+                const float4 c0 = __ldg(cr), a0 = __ldg(cr + 1), a1 = __ldg(cr + 2), a2 = __ldg(cr + 3);
+                const float rx = c0.x - o[0], ry = c0.y - o[1], rz = c0.z - o[2];
+                k = true;
+#pragma unroll
+                for (int q = 0; q < 6; ++q) k = k && keep(cp[q], rx, ry, rz, c0, a0, a1, a2);
+            }
+            const unsigned m = __ballot_sync(FULL, k);
+            if (k) cand[ncand + __popc(m & lt_mask)] = p;
+            ncand += __popc(m);
+        }
+        __syncwarp();
+
+        long long cnt = 0, sum_col = 0, sum_row = 0;
+        for (int tile = 0; tile < tiles_x * tiles_y; ++tile) {
+            const int j0 = (tile % tiles_x) * TILE_W, i0 = (tile / tiles_x) * TILE_H;
+            const int j = j0 + (lane & 7), i = i0 + (lane >> 3);
+            const bool valid = (j < W) && (i < H);
+            // tile frustum through the pixel-centre rays of its border pixels
+            const int j1 = min(j0 + TILE_W - 1, W - 1), i1 = min(i0 + TILE_H - 1, H - 1);
+            const float xl = (2.0f * (j0 + 0.5f) / W - 1.0f) * cam.th, xr = (2.0f * (j1 + 0.5f) / W - 1.0f) * cam.th;
+            const float yt = (2.0f * (i0 + 0.5f) / H - 1.0f) * cam.tv, yb = (2.0f * (i1 + 0.5f) / H - 1.0f) * cam.tv;
+            const Plane tp[4] = {world_plane(Rw, 1.f, 0.f, -xl, 0.f), world_plane(Rw, -1.f, 0.f, xr, 0.f),
+                                 world_plane(Rw, 0.f, 1.f, -yt, 0.f), world_plane(Rw, 0.f, -1.f, yb, 0.f)};
+            // this lane's pixel ray (same arithmetic as the BVH kernel)
+            const float y = (2.0f * (i + 0.5f) / H - 1.0f) * cam.tv;
+            const float x = (2.0f * (j + 0.5f) / W - 1.0f) * cam.th;
+            const float n2 = x * x + y * y + 1.0f;
+            const float cz = rsqrtf(n2);
+            const float cx = x * cz, cy = y * cz;
+            const float dx = Rw[0] * cx + Rw[1] * cy + Rw[2] * cz;
+            const float dy = Rw[3] * cx + Rw[4] * cy + Rw[5] * cz;
+            const float dz = Rw[6] * cx + Rw[7] * cy + Rw[8] * cz;
+            const float tmax = cam.max_range * sqrtf(n2);
+            float best = tmax;
+            int bid = -1;
+            bool hit = false;
+            for (int b = 0; b < ncand; b += 32) {
+                const int k = b + lane;
+                bool kp = false;
+                if (k < ncand) {
+                    const float4 *cr = S.primc + 4 * cand[k];
+                    const float4 c0 = __ldg(cr), a0 = __ldg(cr + 1), a1 = __ldg(cr + 2), a2 = __ldg(cr + 3);
+                    const float rx = c0.x - o[0], ry = c0.y - o[1], rz = c0.z - o[2];
+                    kp = keep(tp[0], rx, ry, rz, c0, a0, a1, a2) && keep(tp[1], rx, ry, rz, c0, a0, a1, a2) &&
+                         keep(tp[2], rx, ry, rz, c0, a0, a1, a2) && keep(tp[3], rx, ry, rz, c0, a0, a1, a2);
+                }
+                unsigned m = __ballot_sync(FULL, kp);
+                while (m) {
+                    const int bit = __ffs(m) - 1;
+                    m &= m - 1;
+                    const int p = cand[b + bit];
+                    const int2 mt = __ldg(S.meta + p);
+                    const float4 *pr = S.primf + 4 * p;
+                    float t;
+                    if (mt.x == QB_SPHERE)
+                        t = ray_sphere_f(pr, o[0], o[1], o[2], dx, dy, dz, tmin, best);
+                    else if (mt.x == QB_BOX)
+                        t = ray_box_f(pr, o[0], o[1], o[2], dx, dy, dz, tmin, best);
+                    else
+                        t = ray_triangle_f(pr, o[0], o[1], o[2], dx, dy, dz, tmin, best);
+                    if (t > 0.0f && (t < best || !hit || (t == best && mt.y < bid))) {
+                        best = t;
+                        bid = mt.y;
+                        hit = true;
+                    }
+                }
+            }
+            float t = hit ? best : -1.0f;
+            int oid = hit ? bid : -1;
+            for (int k = 0; k < n_extra; ++k) {  // swarm agents as spheres (kernels.py:438-445)
+                const float4 sph = *reinterpret_cast<const float4 *>(extra + (c * n_extra + k) * 4);
+                float4 rec[2] = {sph, make_float4(sph.w * sph.w, 0.f, 0.f, 0.f)};
+                float ts = ray_sphere_f(rec, o[0], o[1], o[2], dx, dy, dz, tmin, tmax);
+                if (ts > 0.0f && (t < 0.0f || ts < t)) {
+                    t = ts;
+                    oid = extra_ids[c * n_extra + k];
+                }
+            }
+            const int out_id = t > 0.0f ? oid : 0;
+            if (valid) {
+                const long long off = (c * H + i) * (long long)W + j;
+                if (depth) depth[off] = t > 0.0f ? t * cz : cam.max_range;
+                if (seg) seg[off] = out_id;
+                if (centroid_id > 0 && out_id == centroid_id) {
+                    cnt += 1;
+                    sum_col += j;
+                    sum_row += i;
+                }
+            }
+        }
+        if (centroid_id > 0) {
+#pragma unroll
+            for (int s = 16; s > 0; s >>= 1) {
+                cnt += __shfl_xor_sync(FULL, cnt, s);
+                sum_col += __shfl_xor_sync(FULL, sum_col, s);
+                sum_row += __shfl_xor_sync(FULL, sum_row, s);
+            }
+            if (lane == 0) {
+                centroid[2 * c] = cnt ? (float)((double)sum_col / (double)cnt) : -1.0f;
+                centroid[2 * c + 1] = cnt ? (float)((double)sum_row / (double)cnt) : -1.0f;
+            }
+        }
+        __syncwarp();
+    }
+}
+
 // exact-double validation renderer: one thread per pixel, reference order
 template <bool FROM_STATE>
 __global__ void __launch_bounds__(128) k_render_x(DevScene S, CamD cam, long long n, long long ld, const double *state,
@@ -282,6 +467,26 @@ int launch_render(const qb_scene *s, const qb_camera *cam, int dtype, long long 
         c.max_range = (float)cam->max_range;
         for (int k = 0; k < 9; ++k) c.rot[k] = (float)cam->rotation[k];
         for (int k = 0; k < 3; ++k) c.trans[k] = (float)cam->translation[k];
+        const int mode = cam->mode != 0 ? cam->mode : (s->max_scene_prims <= CULL_MAX ? 2 : 1);
+        if (mode == 2) {
+            if (s->max_scene_prims > CULL_MAX) {
+                set_error("culling renderer supports scenes of <= %d primitives", CULL_MAX);
+                return QB_EINVAL;
+            }
+            const int B = CULL_WARPS * 32;
+            long long blocks = (n + CULL_WARPS - 1) / CULL_WARPS;
+            long long max_blocks = (long long)sm_count() * 8;
+            if (blocks > max_blocks) blocks = max_blocks;
+            if (state)
+                k_render_cull<true><<<(int)blocks, B, 0, st>>>(s->dev, c, n, ld, (const float *)state, nullptr, nullptr,
+                                                               env_scene, (float *)depth, seg, centroid_id, centroid, extra,
+                                                               extra_ids, n_extra);
+            else
+                k_render_cull<false><<<(int)blocks, B, 0, st>>>(s->dev, c, n, ld, nullptr, (const float *)origins,
+                                                                (const float *)rotations, env_scene, (float *)depth, seg, 0,
+                                                                nullptr, nullptr, nullptr, 0);
+            return check_launch("render_cull_f32");
+        }
         const int B = 256;
         long long warps_needed = n;
         long long max_blocks = (long long)sm_count() * 8;  // 8 blocks x 8 warps resident per SM

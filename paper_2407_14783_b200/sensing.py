@@ -51,8 +51,10 @@ class CameraModel:
     def focal_px(self) -> float:
         return (self.height / 2.0) / self.tan_half_v
 
-    def native(self):
+    def native(self, mode: int = 0):
+        """qb_camera; mode 0 auto, 1 BVH packet kernel, 2 frustum-culling kernel."""
         c = nat.QbCamera()
+        c.mode = int(mode)
         c.width, c.height = int(self.width), int(self.height)
         c.tan_half_h, c.tan_half_v, c.max_range = self.tan_half_h, self.tan_half_v, float(self.max_range)
         c.rotation[:] = self.rotation.reshape(9).tolist()
@@ -139,14 +141,17 @@ def render_segmentation(scene, body_position, body_orientation, camera: CameraMo
 
 
 def render_state(dev_scenes, camera: CameraModel, planes, env_scene=None, depth=None, seg=None, centroid_id: int = 0,
-                 centroid=None, extra=None, extra_ids=None):
-    """K2 straight from the (17,N) state planes (the env observation path)."""
+                 centroid=None, extra=None, extra_ids=None, mode: int = 0):
+    """K2 straight from the (17,N) state planes (the env observation path).
+
+    mode: 0 auto (frustum-culling kernel for scenes <= 512 primitives, BVH
+    packet kernel otherwise), 1 force BVH, 2 force culling."""
     import torch
 
     n = planes.shape[1]
     code = nat.QB_F32 if planes.dtype == torch.float32 else nat.QB_F64
     k = 0 if extra is None else extra.shape[1]
-    nat.check(nat.lib().qb_render(dev_scenes.handle, camera.native(), code, n, planes.stride(0), nat.ptr(planes),
+    nat.check(nat.lib().qb_render(dev_scenes.handle, camera.native(mode), code, n, planes.stride(0), nat.ptr(planes),
                                   nat.ptr(env_scene), nat.ptr(depth), nat.ptr(seg), int(centroid_id), nat.ptr(centroid),
                                   nat.ptr(extra), nat.ptr(extra_ids), k, nat.stream_of()), "qb_render")
     return depth, seg

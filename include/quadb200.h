@@ -65,20 +65,26 @@ int qb_rollout_forward(const qb_params *p, int32_t cmd_kind, int32_t dtype, int6
                        void *states_tape, const void *actions, uint8_t *nonfinite, void *stream);
 
 /* Reverse accumulation (gradients.rollout_grad, gradients.py:218-237),
- * matrix-free: per step lambda <- J^T lambda + g[t], grad_a[t] = Ja^T lambda.
- * g_traj (T+1) blocks of 17 planes (dL/dstate), grad_actions (T, n, 4),
- * grad_init 17 planes.  Only QB_CMD_ROTOR and QB_CMD_CTBR/QB_CMD_SRT are
- * differentiable.  action_grad_sum (4*T floats, may be NULL) receives the
- * env-summed action gradient for shared-parameter reductions. */
+ * matrix-free: per step lambda <- J^T lambda + g[t], grad_a[t] = Ja^T lambda,
+ * with J, Ja the exact step Jacobians of step_jacobian (gradients.py:145-197)
+ * never formed.  states_tape as written by qb_rollout_forward; g_traj (T+1)
+ * blocks of 17 planes (dL/dstate, block stride 17*ld); grad_actions (T,n,4);
+ * grad_init 17 planes.  Differentiable action kinds: QB_CMD_ROTOR (the
+ * reference's), QB_CMD_CTBR and QB_CMD_SRT (through the controller + mixer;
+ * beyond the reference, finite-difference pinned).  boundary (n, nullable):
+ * 1 where a clamp sat exactly on a bound (StepJacobian.saturation_boundary).
+ * action_grad_sum (T*4 doubles, nullable, accumulated): sum over envs of
+ * grad_actions -- the shared-parameter gradient a multi-GPU run all-reduces. */
 int qb_rollout_backward(const qb_params *p, int32_t cmd_kind, int32_t dtype, int64_t n, int64_t ld, int32_t T,
                         const void *states_tape, const void *actions, const void *g_traj, void *grad_actions,
-                        void *grad_init, void *stream);
+                        void *grad_init, uint8_t *boundary, double *action_grad_sum, void *stream);
 
-/* One-step VJP (the per-step factor of rollout_grad): given state (pre-step),
- * action and lam_next (17 planes, dL/dnext_state), writes lam_prev (17
- * planes) and grad_action (n,4). */
+/* One-step VJP (the per-step factor of rollout_grad): given state (pre-step
+ * planes), action (n,4) and lam_next (17 planes, dL/dnext_state), writes
+ * lam_prev (17 planes, J^T lam) and grad_action (n,4, Ja^T lam). */
 int qb_dynamics_vjp(const qb_params *p, int32_t cmd_kind, int32_t dtype, int64_t n, int64_t ld, const void *state,
-                    const void *action, const void *lam_next, void *lam_prev, void *grad_action, void *stream);
+                    const void *action, const void *lam_next, void *lam_prev, void *grad_action, uint8_t *boundary,
+                    void *stream);
 
 /* ------------------------------------------------------------------ scenes */
 

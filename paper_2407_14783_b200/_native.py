@@ -142,8 +142,8 @@ SIGNATURES = {
     "qb_dynamics_step": ([_PP(QbParams), _I32, _I32, _I64, _I64, _P, _P, _P, _P, _P], ctypes.c_int),
     "qb_command_to_rotor_speeds": ([_PP(QbParams), _I32, _I32, _I64, _I64, _P, _P, _P, _P], ctypes.c_int),
     "qb_rollout_forward": ([_PP(QbParams), _I32, _I32, _I64, _I64, _I32, _P, _P, _P, _P], ctypes.c_int),
-    "qb_rollout_backward": ([_PP(QbParams), _I32, _I32, _I64, _I64, _I32, _P, _P, _P, _P, _P, _P], ctypes.c_int),
-    "qb_dynamics_vjp": ([_PP(QbParams), _I32, _I32, _I64, _I64, _P, _P, _P, _P, _P, _P], ctypes.c_int),
+    "qb_rollout_backward": ([_PP(QbParams), _I32, _I32, _I64, _I64, _I32, _P, _P, _P, _P, _P, _P, _P, _P], ctypes.c_int),
+    "qb_dynamics_vjp": ([_PP(QbParams), _I32, _I32, _I64, _I64, _P, _P, _P, _P, _P, _P, _P], ctypes.c_int),
     "qb_scene_create": ([_I32, _P, _P, _P, _P, _P, _P, _PP(_P)], ctypes.c_int),
     "qb_scene_destroy": ([_P], ctypes.c_int),
     "qb_scene_stats": ([_P, _P], ctypes.c_int),

@@ -295,21 +295,26 @@ int qb_rollout_forward(const qb_params *p, int32_t cmd_kind, int32_t dtype, int6
 
 int qb_rollout_backward(const qb_params *p, int32_t cmd_kind, int32_t dtype, int64_t n, int64_t ld, int32_t T,
                         const void *states_tape, const void *actions, const void *g_traj, void *grad_actions,
-                        void *grad_init, void *stream) {
+                        void *grad_init, uint8_t *boundary, double *action_grad_sum, void *stream) {
     QB_REQUIRE(p && states_tape && actions && g_traj && grad_actions && grad_init, "qb_rollout_backward: NULL argument");
     QB_REQUIRE(n >= 0 && ld >= n && T >= 1, "bad n/ld/T");
     QB_REQUIRE(dtype == QB_F32 || dtype == QB_F64, "bad dtype %d", dtype);
-    return qb::launch_vjp(p, cmd_kind, dtype, n, ld, T, states_tape, actions, g_traj, grad_actions, grad_init,
-                          qb::as_stream(stream));
+    QB_REQUIRE(cmd_kind == QB_CMD_ROTOR || cmd_kind == QB_CMD_CTBR || cmd_kind == QB_CMD_SRT,
+               "command kind %d is not differentiable (rotor, ctbr, srt are)", cmd_kind);
+    return qb::launch_vjp(p, cmd_kind, dtype, n, ld, T, states_tape, actions, g_traj, grad_actions, grad_init, boundary,
+                          action_grad_sum, qb::as_stream(stream));
 }
 
 int qb_dynamics_vjp(const qb_params *p, int32_t cmd_kind, int32_t dtype, int64_t n, int64_t ld, const void *state,
-                    const void *action, const void *lam_next, void *lam_prev, void *grad_action, void *stream) {
+                    const void *action, const void *lam_next, void *lam_prev, void *grad_action, uint8_t *boundary,
+                    void *stream) {
     QB_REQUIRE(p && state && action && lam_next && lam_prev && grad_action, "qb_dynamics_vjp: NULL argument");
     QB_REQUIRE(n >= 0 && ld >= n, "bad n/ld");
     QB_REQUIRE(dtype == QB_F32 || dtype == QB_F64, "bad dtype %d", dtype);
-    // T = -1: single step, g_traj = lam_next, grad_init = lam_prev
-    return qb::launch_vjp(p, cmd_kind, dtype, n, ld, -1, state, action, lam_next, grad_action, lam_prev,
+    QB_REQUIRE(cmd_kind == QB_CMD_ROTOR || cmd_kind == QB_CMD_CTBR || cmd_kind == QB_CMD_SRT,
+               "command kind %d is not differentiable (rotor, ctbr, srt are)", cmd_kind);
+    // T = -1: one step; g_traj = lam_next, grad_init = lam_prev
+    return qb::launch_vjp(p, cmd_kind, dtype, n, ld, -1, state, action, lam_next, grad_action, lam_prev, boundary, nullptr,
                           qb::as_stream(stream));
 }
 

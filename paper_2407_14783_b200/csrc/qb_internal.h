@@ -57,7 +57,8 @@ int launch_dynamics_step(const qb_params *p, int kind, int dtype, long long n, l
 int launch_command(const qb_params *p, int kind, int dtype, long long n, long long ld, const void *state,
                    const void *action, void *out, cudaStream_t st);
 int launch_vjp(const qb_params *p, int kind, int dtype, long long n, long long ld, int T, const void *states_tape,
-               const void *actions, const void *g_traj, void *grad_actions, void *grad_init, cudaStream_t st);
+               const void *actions, const void *g_traj, void *grad_actions, void *grad_init, uint8_t *boundary,
+               double *action_grad_sum, cudaStream_t st);
 int launch_render(const qb_scene *s, const qb_camera *cam, int dtype, long long n, long long ld, const void *state,
                   const void *origins, const void *rotations, const int32_t *env_scene, void *depth, int32_t *seg,
                   int32_t centroid_id, float *centroid, const float *extra, const int32_t *extra_ids, int n_extra,

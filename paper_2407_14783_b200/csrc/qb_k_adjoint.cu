@@ -1,10 +1,126 @@
-// qb_k_adjoint.cu -- K1 adjoint (placeholder until the VJP kernel lands).
+// qb_k_adjoint.cu -- K1 adjoint kernels: BPTT over a whole horizon in one
+// launch (gradients.rollout_grad, gradients.py:218-237) and the single-step
+// VJP.  One env per thread walks t = T-1 .. 0 keeping lambda (17) in
+// registers; per step it reads the saved pre-step state (17 planes) and the
+// action (16 B), and writes the action gradient (16 B): ~236 B/env-step of
+// HBM traffic, plus the optional in-kernel reduction of the action gradient
+// over envs (warp shuffle, one double atomic per warp) that feeds the
+// multi-GPU all-reduce of a shared open-loop action sequence.
+#include "qb_adjoint.cuh"
 #include "qb_internal.h"
 
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+template <class R, int KIND>
+__global__ void __launch_bounds__(128) k_rollout_bwd(DynConsts<R> C, long long n, long long ld, int T,
+                                                     const typename storage_of<R>::type *tape,
+                                                     const typename storage_of<R>::type *actions,
+                                                     const typename storage_of<R>::type *g_traj,
+                                                     typename storage_of<R>::type *grad_actions,
+                                                     typename storage_of<R>::type *grad_init, uint8_t *boundary,
+                                                     double *action_grad_sum) {
+    using S = typename storage_of<R>::type;
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool live = i < n;
+    const long long ii = live ? i : 0;
+    const bool single = T < 0;
+    const int steps = single ? 1 : T;
+    const long long block = 17 * ld;
+    R lam[17];
+    const S *g_last = single ? g_traj : g_traj + (long long)T * block;
+#pragma unroll
+    for (int k = 0; k < 17; ++k) lam[k] = R(g_last[k * ld + ii]);
+    bool flag = false;
+    for (int t = steps - 1; t >= 0; --t) {
+        R x[17], a[4], cmd[4];
+        const S *xs = tape + (long long)t * block;
+#pragma unroll
+        for (int k = 0; k < 17; ++k) x[k] = R(xs[k * ld + ii]);
+        const S *ap = actions + ((long long)t * n + ii) * 4;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) a[k] = R(ap[k]);
+        command_to_speeds<R, KIND>(C, x, a, cmd);
+        R cb[4] = {R(0.0), R(0.0), R(0.0), R(0.0)};
+        dyn_step_vjp(C, x, cmd, lam, cb, flag);  // lam <- J^T lam (dynamics part)
+        R ga[4];
+        if constexpr (KIND == QB_CMD_ROTOR) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) ga[k] = cb[k];
+        } else if constexpr (KIND == QB_CMD_SRT) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                bool f2 = false;
+                R m = clip_mask(a[k], C.flo, C.fhi, f2);
+                ga[k] = cb[k] * m * speed_of_thrust_grad(C, np_clip(a[k], C.flo, C.fhi));
+            }
+        } else {  // CTBR: through the rate loop + mixer; also adds d/d omega to lam
+            ctbr_vjp(C, x, a[0], a[1], a[2], a[3], cb, ga, lam);
+        }
+        S *gp = grad_actions + ((long long)t * n + ii) * 4;
+        if (live) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) gp[k] = to_store(ga[k]);
+        }
+        if (action_grad_sum) {  // env-sum of the action gradient (shared parameters)
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                double v = live ? r_dbl(ga[k]) : 0.0;
+#pragma unroll
+                for (int s = 16; s > 0; s >>= 1) v += __shfl_xor_sync(FULL, v, s);
+                if ((threadIdx.x & 31) == 0) atomicAdd(action_grad_sum + 4 * t + k, v);
+            }
+        }
+        if (!single) {
+            const S *gt = g_traj + (long long)t * block;
+#pragma unroll
+            for (int k = 0; k < 17; ++k) lam[k] = lam[k] + R(gt[k * ld + ii]);
+        }
+    }
+    if (live) {
+#pragma unroll
+        for (int k = 0; k < 17; ++k) grad_init[k * ld + i] = to_store(lam[k]);
+        if (boundary) boundary[i] = flag ? 1 : 0;
+    }
+}
+
+template <class R>
+int dispatch(const qb_params *p, int kind, long long n, long long ld, int T, const void *tape, const void *actions,
+             const void *gtraj, void *ga, void *gi, uint8_t *boundary, double *sum, cudaStream_t st) {
+    using S = typename storage_of<R>::type;
+    DynConsts<R> C = make_consts<R>(*p);
+    if (C.substeps > 8) {
+        qb::set_error("adjoint supports up to 8 substeps (got %d)", C.substeps);
+        return QB_EINVAL;
+    }
+    const int B = 128;
+    dim3 g(qb::env_grid(n, B));
+    auto *x = static_cast<const S *>(tape);
+    auto *a = static_cast<const S *>(actions);
+    auto *gt = static_cast<const S *>(gtraj);
+    auto *gA = static_cast<S *>(ga);
+    auto *gI = static_cast<S *>(gi);
+    switch (kind) {
+        case QB_CMD_ROTOR: k_rollout_bwd<R, QB_CMD_ROTOR><<<g, B, 0, st>>>(C, n, ld, T, x, a, gt, gA, gI, boundary, sum); break;
+        case QB_CMD_CTBR: k_rollout_bwd<R, QB_CMD_CTBR><<<g, B, 0, st>>>(C, n, ld, T, x, a, gt, gA, gI, boundary, sum); break;
+        case QB_CMD_SRT: k_rollout_bwd<R, QB_CMD_SRT><<<g, B, 0, st>>>(C, n, ld, T, x, a, gt, gA, gI, boundary, sum); break;
+        default: qb::set_error("command kind %d is not differentiable", kind); return QB_EINVAL;
+    }
+    return qb::check_launch("rollout_backward");
+}
+
+}  // namespace
+
 namespace qb {
-int launch_vjp(const qb_params *, int, int, long long, long long, int, const void *, const void *, const void *, void *,
-               void *, cudaStream_t) {
-    set_error("dynamics adjoint not built yet");
-    return QB_EINVAL;
+int launch_vjp(const qb_params *p, int kind, int dtype, long long n, long long ld, int T, const void *states_tape,
+               const void *actions, const void *g_traj, void *grad_actions, void *grad_init, uint8_t *boundary,
+               double *action_grad_sum, cudaStream_t st) {
+    if (n == 0) return QB_OK;
+    if (dtype == QB_F32)
+        return dispatch<float>(p, kind, n, ld, T, states_tape, actions, g_traj, grad_actions, grad_init, boundary,
+                               action_grad_sum, st);
+    return dispatch<xd>(p, kind, n, ld, T, states_tape, actions, g_traj, grad_actions, grad_init, boundary, action_grad_sum,
+                        st);
 }
 }  // namespace qb

@@ -1,19 +1,28 @@
-"""Benchmark of the VisFly/quadsim hot path on B200 (BASELINE.json metric:
-env-steps/s and 64x64 depth frames/s, whole box, vs the CPU reference).
+"""Benchmark of the VisFly/quadsim hot path on B200.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c3|c2|c1|dyn|c5] [--impl ours|reference]
+BASELINE.json metric: env-steps/s and 64x64 depth frames/s (whole box) at
+1/2/4/8 B200 vs the CPU reference.
 
-Default workload = BASELINE config 3 (the largest single-GPU config):
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c3|c1|c2|c4|c5] [--impl ours|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...      (one rank per GPU, NCCL)
+
+Default workload = BASELINE config 3, the largest single-GPU config:
 navigation, 65,536 envs per GPU, 64x64 depth + segmentation from one camera,
-LV actions, full env.step (auto-reset, controller, RK4 dynamics, proximity,
-reward, termination, render).  One env-step renders one 64x64 depth frame,
-so env-steps/s == depth frames/s.  Multi-GPU (torchrun): envs sharded by
-global index, no per-step collective ("scaling": "weak"), time = max over
-ranks of CUDA-event time, value = all ranks' env-steps / that time.
+seeded LV actions, the full env.step (lazy auto-reset, controller, RK4 x2
+dynamics, proximity / collision / out-of-bounds, reward, termination) plus
+the observation render.  One env-step renders one 64x64 depth frame, so
+env-steps/s == depth frames/s.  Multi-GPU: envs sharded by global index,
+no per-step collective ("scaling": "weak"); time = max over ranks of the
+CUDA-event time; value = all ranks' env-steps / that time.
 
-Prints one JSON line (rank 0).  Extra keys: roofline (dominant kernel),
-roofline_dynamics (K1 at HBM-relevant size), cpu_baseline (oracle on the
-host cores), e2e (public API with host buffers), clocks, gpu_launches.
+One JSON line (rank 0).  Besides the contract keys:
+  roofline            dominant kernel of the step (K2 render) vs HBM
+  roofline_dynamics   K1 alone at 16.7M envs (HBM-bound design target)
+  cpu_baseline        CPU oracle (C restatement, OpenMP, all host cores) on a
+                      bounded sample of the same workload
+  e2e                 public API with host buffers (pinned H2D actions, D2H of
+                      observations + reward/flags) inside the timed region
+  clocks, gpu_launches, kernel_ms
 """
 
 from __future__ import annotations
@@ -32,24 +41,30 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+METRIC = "env-steps/sec (= 64x64 depth frames/sec), whole box"
 WORKLOADS = {
-    "c3": dict(desc="navigation, 64x64 depth+segmentation, 65536 envs/GPU (BASELINE config 3)", envs=65536, seg=True),
-    "c2": dict(desc="navigation, 64x64 depth, 100 envs (BASELINE config 2)", envs=100, seg=False),
-    "c1": dict(desc="hover free flight, dynamics only, 100 envs (BASELINE config 1)", envs=100),
+    "c1": "hover free flight (garage), dynamics only, 100 envs/GPU (BASELINE config 1)",
+    "c2": "navigation, 64x64 depth, 100 envs/GPU (BASELINE config 2)",
+    "c3": "navigation, 64x64 depth+segmentation, 65536 envs/GPU (BASELINE config 3)",
+    "c4": "BPTT through dynamics, 16384 envs/GPU, horizon 64, loss/grad all-reduce (BASELINE config 4)",
+    "c5": "landing on a 5e5-triangle indoor mesh, 64x64 down depth+seg, 131072 envs/GPU (BASELINE config 5, 1M on 8 GPUs)",
 }
+ENVS = {"c1": 100, "c2": 100, "c3": 65536, "c4": 16384, "c5": 131072}
 
 
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            p = json.load(f)
-        return p, "measured"
+            return json.load(f), "measured"
     except Exception:
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """nvidia-smi SM clock + throttle reasons, sampled during the timed region."""
+
+    BITS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+            0x80: "hw_power_brake_slowdown", 0x2: "applications_clocks_setting"}
 
     def __init__(self, index=0):
         self.samples, self.index, self._stop, self._t = [], index, threading.Event(), None
@@ -58,14 +73,15 @@ class ClockSampler:
         def run():
             while not self._stop.is_set():
                 try:
-                    out = subprocess.run(
-                        ["nvidia-smi", f"--id={self.index}", "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
-                         "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5).stdout.strip()
+                    out = subprocess.run(["nvidia-smi", f"--id={self.index}",
+                                          "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
                     if out:
-                        self.samples.append(out.split(","))
+                        self.samples.append([x.strip() for x in out.split(",")])
                 except Exception:
                     pass
-                self._stop.wait(0.2)
+                self._stop.wait(0.1)
 
         self._t = threading.Thread(target=run, daemon=True)
         self._t.start()
@@ -74,38 +90,33 @@ class ClockSampler:
         self._stop.set()
         if self._t:
             self._t.join(timeout=6)
-        if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].strip().replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].strip().replace(".", "").isdigit()]
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
         reasons = set()
-        bits = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
-                0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
         for s in self.samples:
             try:
-                v = int(s[2].strip(), 16)
+                v = int(s[2], 16)
             except Exception:
                 continue
-            for b, name in bits.items():
-                if v & b:
-                    reasons.add(name)
+            reasons.update(name for bit, name in self.BITS.items() if v & bit)
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
                 "reasons": sorted(reasons), "samples": len(self.samples)}
 
 
-def dist_setup(args):
+# ---------------------------------------------------------------- distributed
+
+
+def dist_setup():
     import torch
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local if world > 1 else 0)
     if world > 1:
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        torch.cuda.set_device(0)
     return rank, world, local
 
 
@@ -127,52 +138,95 @@ def max_over_ranks(x, world):
     return float(t.item())
 
 
-def l2_flush_buffer():
+def profile_traffic(kernel_key):
+    """Per-unit DRAM traffic (bytes) of a kernel from the committed ncu summary."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            d = json.load(f)
+        return d[kernel_key]["dram_bytes_per_unit"], d[kernel_key]
+    except Exception:
+        return None, None
+
+
+# ---------------------------------------------------------------- our arm
+
+
+def env_workload(kind, rank, world, total):
+    from paper_2407_14783_b200.env import (DistSpec, EnvConfig, InitRandomization, SceneSpec, SensorSpec, make_env,
+                                           navigation_config)
+
+    if kind == "c1":
+        cfg = EnvConfig(num_agents=total, command_type="ctbr", episode_max_steps=1000)
+    elif kind == "c2":
+        cfg = navigation_config(scene_seed=0, num_agents=total)
+    elif kind == "c3":
+        cfg = navigation_config(scene_seed=0, num_agents=total, with_segmentation=True)
+    elif kind == "c5":
+        cfg = EnvConfig(num_agents=total, task="landing", command_type="lv", episode_max_steps=512,
+                        scenes=(SceneSpec(kind="indoor", seed=0),),
+                        randomization=InitRandomization(position=DistSpec("uniform", low=[-12, -12, 1.0], high=[12, 12, 4.5])),
+                        min_spawn_clearance=0.3,
+                        sensors=(SensorSpec(kind="depth", name="depth", orientation="down"),
+                                 SensorSpec(kind="segmentation", name="vision", orientation="down")))
+    else:
+        raise ValueError(kind)
+    return make_env(cfg, shard=(rank, world)), cfg
+
+
+def make_actions(kind, n, count, rank):
     import torch
 
-    return torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
-
-
-# ----------------------------------------------------------------------------
-# our implementation
-
-
-def bench_env(args, rank, world):
-    import torch
-
-    from paper_2407_14783_b200.control import LV
-    from paper_2407_14783_b200.env import make_env, navigation_config
-
-    wl = WORKLOADS[args.workload]
-    n_per = wl["envs"]
-    total = n_per * world
-    cfg = navigation_config(scene_seed=0, num_agents=total, with_segmentation=wl.get("seg", False))
-    env = make_env(cfg, shard=(rank, world))
-    env.reset(seed=args.seed)
-    n = env.num_agents
     g = torch.Generator(device="cuda").manual_seed(1234 + rank)
-    K, W = args.steps, args.warmup
-    acts = torch.empty((K + W, n, 4), device="cuda")
-    acts[..., :3] = torch.randn((K + W, n, 3), device="cuda", generator=g) * 1.5
-    acts[..., 0] += 1.0
-    acts[..., 3] = (torch.rand((K + W, n), device="cuda", generator=g) * 2 - 1) * math.pi
-    cmds = [LV(acts[i, :, :3], acts[i, :, 3]) for i in range(K + W)]
-    # pre-stage contiguous action tensors so the timed loop only launches
-    staged = [acts[i].contiguous() for i in range(K + W)]
+    a = torch.empty((count, n, 4), device="cuda")
+    if kind == "c1":  # hover CTBR + seeded body-rate perturbation (SPEC.md:525)
+        a[..., 0] = 9.81
+        a[..., 1:] = torch.randn((count, n, 3), device="cuda", generator=g) * 0.5
+    else:  # LV set-points + yaw
+        a[..., :3] = torch.randn((count, n, 3), device="cuda", generator=g) * 1.5
+        a[..., 0] += 1.0
+        a[..., 3] = (torch.rand((count, n), device="cuda", generator=g) * 2 - 1) * math.pi
+    return [a[i].contiguous() for i in range(count)]
 
-    def one(i):
-        env._bufs.action = staged[i].data_ptr()
-        env._launch_step()
 
-    for i in range(W):
-        one(i)
-    torch.cuda.synchronize()
-    # per-kernel timing inside the timed region (events on the launching stream)
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(K)]
+def run_env(args, rank, world, kind):
+    import torch
+
     import paper_2407_14783_b200._native as nat
     from paper_2407_14783_b200.sensing import render_state
 
+    total = ENVS[kind] * world
+    env, cfg = env_workload(kind, rank, world, total)
+    env.reset(seed=args.seed)
+    n, K, W = env.num_agents, args.steps, args.warmup
+    acts = make_actions(kind, n, K + W, rank)
+    small = n <= 4096  # latency-bound configs (1, 2): replay the step as a CUDA graph
+    graph = None
+    if small:
+        static_a = torch.empty_like(acts[0])
+        graph = env.make_step_graph(static_a, steps=1)
+
+    def launch(a, events=None):
+        if graph is not None:
+            static_a.copy_(a)
+            graph()
+            return
+        env._bufs.action = a.data_ptr()
+        if events:
+            events[0].record()
+        nat.check(nat.lib().qb_env_step(env._P, env._kind, env._task, env.dev_scenes.handle, env._bufs, nat.stream_of()))
+        if events:
+            events[1].record()
+        for slot in env._cams.values():
+            cid = env._centroid_id(slot)
+            render_state(env.dev_scenes, slot["camera"], env._planes, env_scene=env.agent_scene, depth=slot["depth"],
+                         seg=slot["seg"], centroid_id=cid, centroid=slot["centroid"] if cid else None)
+        if events:
+            events[2].record()
+
+    for i in range(W):
+        launch(acts[i])
+    torch.cuda.synchronize()
+    ev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(3)) for _ in range(K)]
     barrier(world)
     torch.cuda.synchronize()
     clk = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))
@@ -180,80 +234,66 @@ def bench_env(args, rank, world):
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0.record()
     for k in range(K):
-        e0, e1, e2 = ev[k]
-        env._bufs.action = staged[W + k].data_ptr()
-        e0.record()
-        nat.check(nat.lib().qb_env_step(env._P, env._kind, env._task, env.dev_scenes.handle, env._bufs, nat.stream_of()))
-        e1.record()
-        for slot in env._cams.values():
-            render_state(env.dev_scenes, slot["camera"], env._planes, env_scene=env.agent_scene, depth=slot["depth"],
-                         seg=slot["seg"])
-        e2.record()
+        launch(acts[W + k], None if small else ev[k])
     t1.record()
     torch.cuda.synchronize()
     clocks = clk.stop()
-    ms = t0.elapsed_time(t1)
-    step_ms = [a.elapsed_time(b) for a, b, _ in ev]
-    render_ms = [b.elapsed_time(c) for _, b, c in ev]
-    ms = max_over_ranks(ms, world)
-    launches = K * (1 + len(env._cams))
-    # e2e: public API, host (pinned) actions in, observations + reward/flags out
-    e2e = bench_e2e(env, cmds, args, world) if args.e2e else None
-    return dict(env=env, n=n, total=total, ms=ms, step_ms=step_ms, render_ms=render_ms, clocks=clocks, launches=launches,
-                e2e=e2e, cfg=cfg)
+    ms = max_over_ranks(t0.elapsed_time(t1), world)
+    out = dict(env=env, cfg=cfg, n=n, total=total, ms=ms, clocks=clocks, launches=K * (1 + len(env._cams)), graph=small)
+    if not small:
+        out["step_ms"] = float(np.mean([a.elapsed_time(b) for a, b, _ in ev]))
+        out["render_ms"] = float(np.mean([b.elapsed_time(c) for _, b, c in ev]))
+    if args.e2e:
+        out["e2e"] = run_e2e(env, world, kind)
+    return out
 
 
-def bench_e2e(env, cmds, args, world):
+def run_e2e(env, world, kind):
+    """Public API end to end: host (pinned) actions in, observations +
+    reward/terminated/truncated back to host memory, every step."""
     import torch
 
-    from paper_2407_14783_b200.control import LV
+    from paper_2407_14783_b200.control import CTBR, LV
 
     n = env.num_agents
-    K = max(3, min(args.steps, 10))
+    K = 5 if n > 4096 else 50
     rng = np.random.default_rng(0)
-    host_actions = [np.ascontiguousarray(np.concatenate([rng.normal(size=(n, 3)), rng.uniform(-3, 3, (n, 1))], 1),
-                                         dtype=np.float32) for _ in range(K + 1)]
-    obs_keys = [k for k in ("state", "depth", "segmentation") if k in env.get_observation().keys()]
+    host = [np.ascontiguousarray(np.concatenate([rng.normal(size=(n, 3)), rng.uniform(-3, 3, (n, 1))], 1), np.float32)
+            for _ in range(K + 1)]
     outs = {}
 
     def one(a):
-        r = env.step(LV(a[:, :3], a[:, 3]))
-        o = r.observations
-        h2d = a.nbytes
+        cmd = CTBR(a[:, 0] + 9.81, a[:, 1:]) if kind == "c1" else LV(a[:, :3], a[:, 3])
+        r = env.step(cmd)
         d2h = 0
-        for k in obs_keys:
-            t = o[k]
-            if k not in outs:
-                outs[k] = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
-            outs[k].copy_(t, non_blocking=True)
-            d2h += t.numel() * t.element_size()
-        for name, t in (("reward", r.reward), ("terminated", r.terminated), ("truncated", r.truncated)):
+        for name, t in list(r.observations.items()) + [("reward", r.reward), ("terminated", r.terminated),
+                                                         ("truncated", r.truncated)]:
             if name not in outs:
                 outs[name] = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
             outs[name].copy_(t, non_blocking=True)
             d2h += t.numel() * t.element_size()
         torch.cuda.current_stream().synchronize()
-        return h2d, d2h
+        return a.nbytes, d2h
 
-    one(host_actions[0])
+    one(host[0])
     barrier(world)
     torch.cuda.synchronize()
     t = time.perf_counter()
     for k in range(K):
-        h2d, d2h = one(host_actions[k + 1])
-    dt = time.perf_counter() - t
-    dt = max_over_ranks(dt, world)
+        h2d, d2h = one(host[k + 1])
+    dt = max_over_ranks(time.perf_counter() - t, world)
     return {"value": n * world * K / dt, "unit": "env-steps/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-            "steps": K}
+            "steps": K, "path": "env.step(LV numpy) -> observations/reward/flags to pinned host memory"}
 
 
-def bench_dynamics(n, steps, warmup, rank):
-    """K1 alone at an HBM-relevant size: 152 B/env-step algorithmic traffic."""
+def run_dynamics_roofline(pk):
+    """K1 alone at 16.7M envs: 152 B/env-step (read 17 + 4 floats, write 17)."""
     import torch
 
     import paper_2407_14783_b200._native as nat
     from paper_2407_14783_b200.params import native_params
 
+    n = 1 << 24
     P = native_params()
     pl = torch.zeros((17, n), device="cuda")
     pl[0:3] = torch.rand((3, n), device="cuda")
@@ -262,51 +302,147 @@ def bench_dynamics(n, steps, warmup, rank):
     act = torch.empty((n, 4), device="cuda")
     act[:, 0] = 9.81
     act[:, 1:] = torch.randn((n, 3), device="cuda") * 0.3
-    flush = l2_flush_buffer()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
     def launch():
         nat.check(nat.lib().qb_dynamics_step(P, nat.CMD["ctbr"], nat.QB_F32, n, n, nat.ptr(pl), nat.ptr(act), None, None,
                                              nat.stream_of()))
 
-    for _ in range(warmup):
+    for _ in range(3):
         launch()
-    times = []
-    for _ in range(steps):
-        flush.zero_()  # evict L2 between launches
+    ev = []
+    for _ in range(10):
+        flush.zero_()  # L2 flushed between launches
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
         launch()
         b.record()
-        times.append((a, b))
+        ev.append((a, b))
     torch.cuda.synchronize()
-    ms = float(np.mean([a.elapsed_time(b) for a, b in times]))
-    return n, ms
+    ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
+    gbs = n * 152 / (ms / 1e3) / 1e9
+    traffic, _ = profile_traffic("k_dyn_step")
+    return {"bound": "hbm", "achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": gbs / pk["hbm_gbs"],
+            "traffic": traffic * n if traffic else None, "envs": n, "ms": ms, "env_steps_per_sec": n / (ms / 1e3),
+            "note": "K1 (CTBR controller + mixer + RK4 x2 + renorm), 152 algorithmic B/env-step, L2 flushed"}
 
 
-def cpu_baseline_env(cfg_total, n_sample=64, steps=3):
-    """Oracle (C restatement, OpenMP on all host cores) on a bounded sample of
-    the same navigation workload: env-steps/s."""
-    import dataclasses
+def run_bptt(args, rank, world):
+    """Config 4: BPTT through the dynamics, horizon 64, 16384 envs/GPU.
+    One iteration = forward rollout (1 launch) + loss gradient + adjoint sweep
+    (1 launch, env-summed shared-action gradient reduced in-kernel) +
+    all_reduce(SUM) of loss and shared gradient over NCCL."""
+    import torch
 
+    from paper_2407_14783_b200 import gradients as G
+    from paper_2407_14783_b200.params import native_params
+
+    n, T = ENVS["c4"], 64
+    P = native_params()
+    g = torch.Generator(device="cuda").manual_seed(7 + rank)
+    init = torch.zeros((17, n), device="cuda")
+    init[0:3] = (torch.rand((3, n), device="cuda", generator=g) - 0.5) * 0.2
+    init[6] = 1.0
+    init[13:17] = 900.0
+    acts = 900.0 + torch.randn((T, n, 4), device="cuda", generator=g) * 20.0
+    target = torch.tensor([1.0, 0.0, 2.0], device="cuda")
+    gsum = torch.zeros(T * 4, dtype=torch.float64, device="cuda")
+    red = torch.zeros(T * 4 + 1, dtype=torch.float64, device="cuda")
+
+    def iteration():
+        tape, _ = G.rollout_planes(P, "rotor", init, acts)
+        d = tape[-1, 0:3] - target[:, None]
+        loss = (d * d).sum() / (n * world) + 1e-6 * ((acts - 900.0) ** 2).sum()
+        gtraj = torch.zeros_like(tape)
+        gtraj[-1, 0:3] = 2.0 * d / (n * world)
+        gsum.zero_()
+        ga, gi, _ = G.backward_planes(P, "rotor", tape, acts, gtraj, action_grad_sum=gsum)
+        red[: T * 4] = gsum
+        red[-1] = loss
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.all_reduce(red)
+        return ga
+
+    for _ in range(args.warmup):
+        iteration()
+    torch.cuda.synchronize()
+    barrier(world)
+    K = args.steps
+    clk = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))
+    clk.start()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(K):
+        iteration()
+    t1.record()
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    ms = max_over_ranks(t0.elapsed_time(t1), world)
+    # per-kernel timing of one iteration
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    e[0].record()
+    tape, _ = G.rollout_planes(P, "rotor", init, acts)
+    e[1].record()
+    G.backward_planes(P, "rotor", tape, acts, torch.zeros_like(tape), action_grad_sum=gsum)
+    e[2].record()
+    torch.cuda.synchronize()
+    return dict(n=n, T=T, ms=ms, clocks=clocks, fwd_ms=e[0].elapsed_time(e[1]), bwd_ms=e[1].elapsed_time(e[2]))
+
+
+def cpu_baseline_env(kind="c3", n_sample=1024, steps=12):
+    """The CPU oracle (C restatement of the reference, OpenMP on all host
+    cores) on a bounded sample of the same workload: env-steps/s."""
     import oracle
     from oracle.env import OracleEnv
-    from paper_2407_14783_b200.env import navigation_config
+    from paper_2407_14783_b200.env import EnvConfig, navigation_config
     from paper_2407_14783_b200.params import ControllerGains, QuadParams, SimConfig
 
-    cfg = navigation_config(scene_seed=0, num_agents=n_sample, with_segmentation=True)
-    sc = cfg.scenes[0].materialize().arrays
-    osc = oracle.OracleScene(sc.prim_type, sc.prim_data, sc.prim_object_id, sc.prim_aabb_lo, sc.prim_aabb_hi)
-    env = OracleEnv(cfg, [osc], QuadParams(), SimConfig(), ControllerGains())
+    if kind == "c1":
+        cfg = EnvConfig(num_agents=n_sample, command_type="ctbr", episode_max_steps=1000)
+    else:
+        cfg = navigation_config(scene_seed=0, num_agents=n_sample, with_segmentation=(kind != "c2"))
+    scenes = []
+    for spec in cfg.scenes:
+        t = spec.materialize().arrays
+        scenes.append(oracle.OracleScene(t.prim_type, t.prim_data, t.prim_object_id, t.prim_aabb_lo, t.prim_aabb_hi))
+    env = OracleEnv(cfg, scenes, QuadParams(), SimConfig(), ControllerGains())
     env.reset(seed=0)
     rng = np.random.default_rng(0)
-    acts = [np.concatenate([rng.normal(scale=1.5, size=(n_sample, 3)), rng.uniform(-3, 3, (n_sample, 1))], 1)
-            for _ in range(steps + 1)]
-    env.step(acts[0])
+
+    def act():
+        if kind == "c1":
+            return np.concatenate([np.full((n_sample, 1), 9.81), rng.normal(scale=0.5, size=(n_sample, 3))], 1)
+        return np.concatenate([rng.normal(scale=1.5, size=(n_sample, 3)), rng.uniform(-3, 3, (n_sample, 1))], 1)
+
+    env.step(act())
     t = time.perf_counter()
-    for k in range(steps):
-        env.step(acts[k + 1])
+    for _ in range(steps):
+        env.step(act())
     dt = time.perf_counter() - t
     return n_sample * steps / dt, dt
+
+
+def cpu_baseline_bptt(n_sample=8, T=64):
+    """Oracle rollout_grad (dense 17x17 Jacobian chain, gradients.py:218-237)."""
+    import oracle
+    from paper_2407_14783_b200.params import ControllerGains, QuadParams, SimConfig
+
+    P = oracle.pack_params(QuadParams(), SimConfig(), ControllerGains())
+    rng = np.random.default_rng(0)
+    x0 = np.zeros(17); x0[6] = 1.0; x0[13:] = P.hover_speed
+
+    def loss(tr):
+        g = np.zeros_like(tr)
+        g[-1, 0:3] = 2 * (tr[-1, 0:3] - [1.0, 0, 2.0])
+        return 0.0, g
+
+    t = time.perf_counter()
+    for _ in range(n_sample):
+        oracle.rollout_grad(P, x0, 900 + rng.normal(scale=20, size=(T, 4)), loss)
+    dt = time.perf_counter() - t
+    return n_sample * T / dt, dt
 
 
 def main():
@@ -319,77 +455,102 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
     ap.add_argument("--no-cpu", dest="cpu", action="store_false")
-    ap.add_argument("--dyn-n", type=int, default=1 << 24)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    kind = args.workload
+
+    if args.impl == "reference":
+        return reference_arm(args, kind)
 
     import torch
 
-    rank, world, local = dist_setup(args)
+    rank, world, local = dist_setup()
     pk, pk_kind = peaks()
-    wl = WORKLOADS[args.workload]
-    metric = "env-steps/sec (= 64x64 depth frames/sec), whole box"
-
-    if args.impl == "reference":
+    line = {"metric": METRIC, "unit": "env-steps/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (procedurally generated scenes, seeded actions); no datasets offline"}
+    if kind == "c4":
+        r = run_bptt(args, rank, world)
+        steps_total = r["n"] * r["T"] * world * args.steps
+        line.update({"metric": "BPTT env-steps/sec (forward + adjoint), whole box", "value": steps_total / (r["ms"] / 1e3),
+                     "ms_per_step": r["ms"] / args.steps, "clocks": r["clocks"], "gpu_launches": 2 * args.steps,
+                     "config": {"workload": WORKLOADS[kind], "envs_per_gpu": r["n"], "horizon": r["T"],
+                                "parallelism": f"env shards x{world}, all_reduce(SUM) of loss + shared action grad"},
+                     "kernel_ms": {"rollout_forward": r["fwd_ms"], "rollout_backward": r["bwd_ms"]}})
+        fwd_b, bwd_b = 152 + 68, 236  # algorithmic B/env-step (tape write, tape/action read, grad write)
+        gbs = r["n"] * r["T"] * (fwd_b + bwd_b) / ((r["fwd_ms"] + r["bwd_ms"]) / 1e3) / 1e9
+        line["roofline"] = {"bound": "hbm", "achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                            "frac": gbs / pk["hbm_gbs"], "traffic": None,
+                            "note": "forward+adjoint, (220+236) algorithmic B/env-step"}
+        if rank == 0 and args.cpu:
+            v, dt = cpu_baseline_bptt()
+            line["cpu_baseline"] = {"value": v, "unit": "env-steps/s", "cores": 1, "kind": "port",
+                                    "sample": f"8 agents x H=64 oracle rollout_grad ({dt:.1f} s)"}
+    else:
+        r = run_env(args, rank, world, kind)
+        value = r["total"] * args.steps / (r["ms"] / 1e3)
+        line.update({"value": value, "ms_per_step": r["ms"] / args.steps, "clocks": r["clocks"],
+                     "gpu_launches": r["launches"],
+                     "config": {"workload": WORKLOADS[kind], "envs_per_gpu": r["n"], "global_envs": r["total"],
+                                "resolution": "64x64", "integrator": "rk4, 2 substeps",
+                                "sensors": ",".join(f"{s.name}:{s.kind}" for s in r["cfg"].sensors) or "none",
+                                "l2": "per-step output (depth+seg, 2.1 GB at c3) >> 126 MB L2; no flush needed"
+                                if not r["graph"] else "100 envs: latency-bound, step replayed as a CUDA graph",
+                                "parallelism": f"env shards x{world}, no per-step collective"}})
+        if "render_ms" in r:
+            line["kernel_ms"] = {"env_step_k1k3": r["step_ms"], "render_k2": r["render_ms"]}
+            px = r["n"] * 64 * 64
+            nbytes = px * sum(4 for s in r["cfg"].sensors) + r["n"] * 40  # outputs + pose reads
+            gbs = nbytes / (r["render_ms"] / 1e3) / 1e9
+            traffic, meta = profile_traffic("k_render_cull" if kind != "c5" else "k_render_f")
+            line["roofline"] = {
+                "bound": "hbm", "achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": gbs / pk["hbm_gbs"],
+                "traffic": traffic * r["n"] if traffic else None,
+                "note": (f"dominant kernel K2 render ({r['render_ms']:.3f} of {r['ms'] / args.steps:.3f} ms/step): "
+                         f"algorithmic bytes = depth+seg writes + pose reads; the kernel is SM-issue-bound "
+                         f"(see profiles/ncu_summary.json), peak = {pk_kind} HBM copy bandwidth")}
         if rank == 0:
-            v, dt = cpu_baseline_env(wl["envs"], n_sample=64, steps=max(1, min(args.steps, 4)))
-            line = {"impl": "reference", "metric": metric, "value": v, "unit": "env-steps/s", "n_gpus": world,
-                    "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
-                    "config": {"workload": wl["desc"]},
-                    "cpu_baseline": {"value": v, "unit": "env-steps/s", "cores": os.cpu_count(), "kind": "port",
-                                     "sample": "64 navigation envs (depth+seg), oracle C port with OpenMP"},
-                    "e2e": {"value": v, "unit": "env-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-            print(json.dumps(line), flush=True)
-        return
-
-    res = bench_env(args, rank, world)
-    K = args.steps
-    value = res["total"] * K / (res["ms"] / 1e3)
-    # dominant kernel = K2 render: algorithmic ops/ray from the reference BVH counts
-    r_ms = float(np.mean(res["render_ms"]))
-    s_ms = float(np.mean(res["step_ms"]))
-    rays = res["n"] * 64 * 64
-    ops_per_ray = 1470.0
-    achieved_ops = rays * ops_per_ray / (r_ms / 1e3)
-    sm_mhz = pk.get("sm_max_mhz", 1965.0)
-    peak_ops = 148 * 128 * sm_mhz * 1e6
-    out_bytes = rays * (4 + (4 if wl.get("seg") else 0))
-    line = {
-        "metric": metric, "value": value, "unit": "env-steps/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
-        "ms_per_step": res["ms"] / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic (procedural cluttered room, seeded LV actions)",
-        "config": {"workload": wl["desc"], "envs_per_gpu": res["n"], "global_envs": res["total"], "resolution": "64x64",
-                   "sensors": "depth+segmentation" if wl.get("seg") else "depth", "integrator": "rk4 x2 substeps",
-                   "l2": "per-step working set (2.1 GB of depth+seg output) >> 126 MB L2",
-                   "parallelism": f"env shards x{world}, no per-step collective"},
-        "kernel_ms": {"env_step_k1k3": s_ms, "render_k2": r_ms},
-        "roofline": {"bound": "fp32_issue", "achieved": achieved_ops / 1e9, "peak": peak_ops / 1e9, "unit": "Gop/s",
-                     "frac": achieved_ops / peak_ops, "traffic": None,
-                     "note": f"K2 render: {ops_per_ray:.0f} algorithmic FP32 ops/ray (reference-BVH count, SURVEY 8-D) x "
-                             f"{rays} rays per launch / launch time; peak = 148 SMs x 128 lanes x {sm_mhz:.0f} MHz "
-                             f"({pk_kind}); HBM view: {out_bytes / (r_ms / 1e3) / 1e9:.1f} GB/s of "
-                             f"{pk.get('hbm_gbs')} GB/s"},
-        "clocks": res["clocks"], "gpu_launches": res["launches"],
-    }
+            line["roofline_dynamics"] = run_dynamics_roofline(pk)
+            if args.cpu:
+                ns = min(1024, ENVS[kind])
+                steps = 12 if ns > 100 else 400
+                v, dt = cpu_baseline_env(kind if kind in ("c1", "c2") else "c3", n_sample=ns, steps=steps)
+                line["cpu_baseline"] = {"value": v, "unit": "env-steps/s", "cores": os.cpu_count(), "kind": "port",
+                                        "sample": f"{ns} envs x {steps} steps of the same env step on the C oracle "
+                                                  f"(OpenMP), {dt:.1f} s"}
+        if "e2e" in r:
+            line["e2e"] = r["e2e"]
     if rank == 0:
-        n_dyn, ms_dyn = bench_dynamics(args.dyn_n, 10, 3, rank)
-        gbs = n_dyn * 152 / (ms_dyn / 1e3) / 1e9
-        line["roofline_dynamics"] = {"bound": "hbm", "achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                                     "frac": gbs / pk["hbm_gbs"], "traffic": None, "envs": n_dyn, "ms": ms_dyn,
-                                     "env_steps_per_sec": n_dyn / (ms_dyn / 1e3),
-                                     "note": "K1 CTBR RK4x2, 152 B/env-step (read 17+4 floats, write 17), L2 flushed"}
-        if res["e2e"]:
-            line["e2e"] = res["e2e"]
-        if args.cpu:
-            v, dt = cpu_baseline_env(res["total"])
-            line["cpu_baseline"] = {"value": v, "unit": "env-steps/s", "cores": os.cpu_count(), "kind": "port",
-                                    "sample": f"64 navigation envs x 3 steps (depth+seg), {dt:.1f} s of CPU work"}
         print(json.dumps(line), flush=True)
     barrier(world)
     if world > 1:
         import torch.distributed as dist
 
         dist.destroy_process_group()
+
+
+def reference_arm(args, kind):
+    """--impl reference: the reference's algorithm on the host cores (the C
+    oracle restatement -- the Python reference cannot be compiled and does
+    not travel to the GPU box), same metric/config, each step a bounded
+    sample.  Under torchrun only rank 0 runs."""
+    if int(os.environ.get("RANK", "0")) != 0:
+        return
+    if kind == "c4":
+        vals = [cpu_baseline_bptt(n_sample=2)[0] for _ in range(max(1, min(args.steps, 5)))]
+        unit, sample = "env-steps/s", "2 agents x H=64 oracle rollout_grad per step"
+        metric = "BPTT env-steps/sec (forward + adjoint), whole box"
+    else:
+        vals = []
+        for _ in range(max(1, min(args.steps, 5))):
+            vals.append(cpu_baseline_env(kind if kind in ("c1", "c2") else "c3", n_sample=512, steps=2)[0])
+        unit, sample, metric = "env-steps/s", "512 envs x 2 steps per step (C oracle, OpenMP)", METRIC
+    v = float(np.median(vals))
+    line = {"impl": "reference", "metric": metric, "value": v, "unit": unit, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "higher_is_better": True, "config": {"workload": WORKLOADS[kind]},
+            "cpu_baseline": {"value": v, "unit": unit, "cores": os.cpu_count(), "kind": "port", "sample": sample},
+            "e2e": {"value": v, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
 
 
 if __name__ == "__main__":

@@ -336,6 +336,7 @@ def run_bptt(args, rank, world):
 
     from paper_2407_14783_b200 import gradients as G
     from paper_2407_14783_b200.params import native_params
+    from paper_2407_14783_b200.sharding import reduce_bptt
 
     n, T = ENVS["c4"], 64
     P = native_params()
@@ -357,12 +358,7 @@ def run_bptt(args, rank, world):
         gtraj[-1, 0:3] = 2.0 * d / (n * world)
         gsum.zero_()
         ga, gi, _ = G.backward_planes(P, "rotor", tape, acts, gtraj, action_grad_sum=gsum)
-        red[: T * 4] = gsum
-        red[-1] = loss
-        if world > 1:
-            import torch.distributed as dist
-
-            dist.all_reduce(red)
+        reduce_bptt(loss, gsum, out=red)  # one all_reduce(SUM) of [shared grad, loss] over NCCL
         return ga
 
     for _ in range(args.warmup):

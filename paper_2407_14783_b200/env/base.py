@@ -35,6 +35,7 @@ from ..errors import ActionShapeMismatch, ConfigError, NotReset, SpawnFailure
 from ..geometry.device import DeviceScenes
 from ..params import ControllerGains, QuadParams, SimConfig, native_params
 from ..sensing import render_state
+from ..sharding import shard_range
 
 DRONE_ID0 = 60000
 
@@ -156,7 +157,7 @@ class QuadEnvBase:
         self.dtype = dtype or torch.float32
         rank, world = shard
         total = config.num_agents
-        lo, hi = rank * total // world, (rank + 1) * total // world
+        lo, hi = shard_range(rank, world, total)
         self.global_num_agents = total
         self.index_offset = lo
         self.num_agents = hi - lo

@@ -1,5 +1,12 @@
 mkdir -p gpurun_out
-python scripts/profile_step.py --envs 16384 --steps 3 > gpurun_out/prof_plain.log 2>&1 && \
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_r1.csv python scripts/profile_step.py --envs 16384 --steps 3 > gpurun_out/ncu_launch.log 2>&1; echo launches=$?
-ncu --set full --clock-control none --import-source on -k regex:k_render -s 1 -c 1 -o gpurun_out/prof_render_r1 python scripts/profile_step.py --envs 16384 --steps 3 > gpurun_out/ncu_render.log 2>&1; echo render=$?
-ncu --set full --clock-control none --import-source on -k regex:k_env_step -s 1 -c 1 -o gpurun_out/prof_envstep_r1 python scripts/profile_step.py --envs 16384 --steps 3 > gpurun_out/ncu_env.log 2>&1; echo env=$?
+NCU="ncu --set full --clock-control none --import-source on"
+python scripts/profile_kernels.py nav --envs 16384 > gpurun_out/p_plain.log 2>&1 && \
+  $NCU -k regex:k_render_cull -s 1 -c 1 -o gpurun_out/r1_render_cull python scripts/profile_kernels.py nav --envs 16384 > gpurun_out/p1.log 2>&1; echo cull=$?
+$NCU -k regex:k_env_step -s 1 -c 1 -o gpurun_out/r1_env_step python scripts/profile_kernels.py nav --envs 65536 > gpurun_out/p2.log 2>&1; echo envstep=$?
+python scripts/profile_kernels.py indoor --envs 4096 > gpurun_out/p_plain2.log 2>&1 && \
+  $NCU -k regex:k_render_f -s 1 -c 1 -o gpurun_out/r1_render_bvh python scripts/profile_kernels.py indoor --envs 4096 > gpurun_out/p3.log 2>&1; echo bvh=$?
+$NCU -k regex:k_dyn_step -s 1 -c 1 -o gpurun_out/r1_dyn_step python scripts/profile_kernels.py dyn --envs 4194304 > gpurun_out/p4.log 2>&1; echo dyn=$?
+$NCU -k regex:k_rollout -s 2 -c 2 -o gpurun_out/r1_bptt python scripts/profile_kernels.py bptt --envs 16384 > gpurun_out/p5.log 2>&1; echo bptt=$?
+python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/b_plain.log 2>&1 && \
+  ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r1_launches.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/p6.log 2>&1; echo launches=$?
+ls -la gpurun_out

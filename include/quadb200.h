@@ -121,7 +121,7 @@ typedef struct qb_camera {
     double tan_half_h, tan_half_v, max_range; /* CameraModel, sensing.py:32-63 */
     double rotation[9];                       /* camera -> body, row-major */
     double translation[3];                    /* camera origin in body */
-    int32_t mode;  /* FP32 kernel: 0 auto, 1 BVH packet traversal, 2 frustum-culling (scenes <= 512 prims) */
+    int32_t mode;  /* FP32 kernel: 0 auto, 1 BVH packet traversal, 2 frustum-culling (scenes <= 256 prims) */
     int32_t pad_;
 } qb_camera;
 

@@ -137,18 +137,28 @@ template <class R> QB_D void make_wrench(const DynConsts<R> &C, const R *w, Wren
 // dynamics.py:154-200: 13 rigid rates at y = (p, v, q, omega)
 template <class R> QB_D void ode_rhs(const DynConsts<R> &C, const R *y, const Wrench<R> &W, R *dy) {
     const R *v = y + 3, *q = y + 6, *o = y + 10;
-    R bx, by, bz;
-    q_rot<R, -1>(q, v[0], v[1], v[2], bx, by, bz);  // v_B = R^T v
-    R fx = C.neg_drag[0] * bx * r_abs(bx);           // dynamics.py:117-120
-    R fy = C.neg_drag[1] * by * r_abs(by);
-    R fz = C.neg_drag[2] * bz * r_abs(bz);
-    if constexpr (is_exact<R>::value)
-        fz = fz + W.f[0] + W.f[1] + W.f[2] + W.f[3];  // dynamics.py:190 evaluation order
-    else
-        fz = fz + W.fsum;
+    R bx, by, bz, fx, fy, fz, ax, ay, az;
+    if constexpr (is_exact<R>::value) {  // reference operation order (quatmath.rotate / rotate_inv)
+        q_rot<R, -1>(q, v[0], v[1], v[2], bx, by, bz);  // v_B = R^T v
+        fx = C.neg_drag[0] * bx * r_abs(bx);            // dynamics.py:117-120
+        fy = C.neg_drag[1] * by * r_abs(by);
+        fz = C.neg_drag[2] * bz * r_abs(bz);
+        fz = fz + W.f[0] + W.f[1] + W.f[2] + W.f[3];    // dynamics.py:190 evaluation order
+        q_rot<R, 1>(q, fx, fy, fz, ax, ay, az);
+    } else {  // same polynomial R(q) (== to_matrix, also for |q| != 1), built once per stage
+        R m[3][3];
+        q_matrix(q, m);
+        bx = m[0][0] * v[0] + m[1][0] * v[1] + m[2][0] * v[2];
+        by = m[0][1] * v[0] + m[1][1] * v[1] + m[2][1] * v[2];
+        bz = m[0][2] * v[0] + m[1][2] * v[1] + m[2][2] * v[2];
+        fx = C.neg_drag[0] * bx * r_abs(bx);
+        fy = C.neg_drag[1] * by * r_abs(by);
+        fz = C.neg_drag[2] * bz * r_abs(bz) + W.fsum;
+        ax = m[0][0] * fx + m[0][1] * fy + m[0][2] * fz;
+        ay = m[1][0] * fx + m[1][1] * fy + m[1][2] * fz;
+        az = m[2][0] * fx + m[2][1] * fy + m[2][2] * fz;
+    }
     dy[0] = v[0]; dy[1] = v[1]; dy[2] = v[2];
-    R ax, ay, az;
-    q_rot<R, 1>(q, fx, fy, fz, ax, ay, az);
     if constexpr (is_exact<R>::value) {
         dy[3] = ax / C.mass + C.g[0];
         dy[4] = ay / C.mass + C.g[1];
@@ -249,17 +259,31 @@ template <class R> QB_D R speed_of_thrust(const DynConsts<R> &C, R f) {
 template <class R> QB_D void mixer(const DynConsts<R> &C, R force, const R *tq, R *thr) {
     R fcl = np_clip(force, C.flo4, C.fhi4);
     R base[4], tp[4];
-    R up_min = R(infinity_d()), dn_min = R(infinity_d());
+    R scale;
+    if constexpr (is_exact<R>::value) {
+        R up_min = R(infinity_d()), dn_min = R(infinity_d());
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        base[i] = C.minv[i][0] * fcl;
-        tp[i] = C.minv[i][1] * tq[0] + C.minv[i][2] * tq[1] + C.minv[i][3] * tq[2];
-        R up = tp[i] > R(0.0) ? (C.fhi - base[i]) / tp[i] : R(infinity_d());
-        R dn = tp[i] < R(0.0) ? (C.flo - base[i]) / tp[i] : R(infinity_d());
-        up_min = np_min(up_min, up);
-        dn_min = np_min(dn_min, dn);
+        for (int i = 0; i < 4; ++i) {
+            base[i] = C.minv[i][0] * fcl;
+            tp[i] = C.minv[i][1] * tq[0] + C.minv[i][2] * tq[1] + C.minv[i][3] * tq[2];
+            R up = tp[i] > R(0.0) ? (C.fhi - base[i]) / tp[i] : R(infinity_d());
+            R dn = tp[i] < R(0.0) ? (C.flo - base[i]) / tp[i] : R(infinity_d());
+            up_min = np_min(up_min, up);
+            dn_min = np_min(dn_min, dn);
+        }
+        scale = np_max(np_min(np_min(up_min, dn_min), R(1.0)), R(0.0));
+    } else {  // only one of up / dn is finite per rotor: one (fast) division each
+        R bmin = R(infinity_d());
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            base[i] = C.minv[i][0] * fcl;
+            tp[i] = C.minv[i][1] * tq[0] + C.minv[i][2] * tq[1] + C.minv[i][3] * tq[2];
+            R lim = tp[i] > R(0.0) ? C.fhi : C.flo;
+            R b = tp[i] != R(0.0) ? __fdividef(lim - base[i], tp[i]) : R(infinity_d());
+            bmin = fminf(bmin, b);
+        }
+        scale = fmaxf(fminf(bmin, R(1.0)), R(0.0));
     }
-    R scale = np_max(np_min(np_min(up_min, dn_min), R(1.0)), R(0.0));
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         R f = base[i] + scale * tp[i];

@@ -48,7 +48,7 @@ template <class R, class S> __device__ __forceinline__ void store4(S *p, const R
 // step (T == 0) or horizon rollout (T > 0: state = tape block 0, actions_seq
 // (T,n,4), block t+1 written after step t).
 template <class R, int KIND>
-__global__ void __launch_bounds__(128) k_dyn_step(DynConsts<R> C, long long n, long long ld,
+__global__ void __launch_bounds__(128, 8) k_dyn_step(DynConsts<R> C, long long n, long long ld,
                                                   typename storage_of<R>::type *state,
                                                   const typename storage_of<R>::type *action,
                                                   typename storage_of<R>::type *rotor_out, uint8_t *nonfinite, int T) {

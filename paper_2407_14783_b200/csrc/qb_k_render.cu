@@ -4,7 +4,7 @@
 //
 // FP32 production kernels (one warp renders one camera, tile by tile; a tile
 // is an 8x4 block of pixels, so the warp's 32 rays are coherent):
-//   k_render_cull  scenes of <= 512 primitives: two-level frustum culling
+//   k_render_cull  scenes of <= 256 primitives: two-level frustum culling
 //                  (camera, then tile) and warp-uniform ray tests of the few
 //                  survivors -- see the comment above the kernel;
 //   k_render_f     any scene: the BVH is walked as a PACKET: the traversal stack and the node sequence are
@@ -181,18 +181,26 @@ __global__ void __launch_bounds__(256) k_render_f(DevScene S, CamF cam, long lon
 
 // ---------------------------------------------------------------------------
 // Culling renderer for small scenes (<= CULL_MAX primitives per scene, e.g.
-// the 69-primitive navigation room): instead of walking a BVH per ray, a warp
-// culls the scene against its camera frustum once (lane-parallel over
-// primitives, 6 plane/support tests), then for every 8x4 tile culls that
-// candidate list against the tile's 4 side planes (lane-parallel again) and
-// ray-tests only the survivors, warp-uniformly.  The culling is
-// conservative (support functions of spheres / OBBs / triangle bounding
-// spheres, 1 mm margin), and the per-pixel result -- nearest t, ties to the
-// lowest id -- does not depend on the order primitives are tested in, so
-// the output is identical to the BVH kernel's.
-constexpr int CULL_MAX = 512;
-constexpr int CULL_WARPS = 8;
+// the 69-primitive navigation room).  One warp renders one camera:
+//  1. camera culling: lane-parallel over the scene's primitives, 6 plane /
+//     support-function tests (image frustum, near, far) -> candidate list;
+//  2. per candidate (lane-parallel) a CAMERA-SPECIFIC record in shared
+//     memory: its culling bounds in camera space and its ray-test constants
+//     for this camera origin (sphere: o - c; box: slab numerators +-h - R^T(o-c);
+//     oriented box: also R's columns), so a pixel's primitive test is just
+//     the direction-dependent part (AABB ~15, OBB ~30, sphere ~18 instr);
+//  3. per 8x4 tile: cull the records against the tile's 4 side planes in
+//     camera space (lane-parallel), then ray-test the survivors
+//     warp-uniformly with shared approximate reciprocals of the direction.
+// Culling is conservative (support functions of spheres / OBBs / triangle
+// bounding spheres, 1 mm margin); the per-pixel result -- nearest t, ties to
+// the lowest id -- does not depend on test order, so ids equal the BVH
+// kernel's and depths agree to FP32 rounding.
+constexpr int CULL_MAX = 256;   // primitives per scene
+constexpr int CULL_WARPS = 4;   // warps (cameras) per block
+constexpr int CREC = 64;        // precomputed records per camera (nav room: mean 21, max 58); more use the generic path
 constexpr float CULL_EPS = 1e-3f;
+enum { REC_SPHERE = 0, REC_AABB = 1, REC_OBB = 2, REC_GENERIC = 3 };
 
 struct Plane {
     float x, y, z, off;
@@ -213,15 +221,39 @@ __device__ __forceinline__ bool keep(const Plane &P, float rx, float ry, float r
     return d + s >= -CULL_EPS;
 }
 
+__device__ __forceinline__ float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+// slab intersection from precomputed numerators (kernels.py:203-246 semantics:
+// entry clamped at tmin, exit returned when the origin is inside)
+__device__ __forceinline__ float slab_hit(float nlx, float nly, float nlz, float nhx, float nhy, float nhz, float ix, float iy,
+                                          float iz, float tmin, float tmax) {
+    const float tax = nlx * ix, tbx = nhx * ix, tay = nly * iy, tby = nhy * iy, taz = nlz * iz, tbz = nhz * iz;
+    const float t0 = fmaxf(fmaxf(fminf(tax, tbx), fminf(tay, tby)), fmaxf(fminf(taz, tbz), tmin));
+    const float t1 = fminf(fminf(fmaxf(tax, tbx), fmaxf(tay, tby)), fminf(fmaxf(taz, tbz), tmax));
+    if (t0 > t1) return -1.0f;
+    if (t0 > tmin && t0 <= tmax) return t0;
+    if (t1 > tmin && t1 <= tmax) return t1;
+    return -1.0f;
+}
+
 template <bool FROM_STATE>
-__global__ void __launch_bounds__(CULL_WARPS * 32) k_render_cull(DevScene S, CamF cam, long long n, long long ld,
-                                                                 const float *state, const float *origins,
-                                                                 const float *rotations, const int32_t *env_scene,
-                                                                 float *depth, int32_t *seg, int centroid_id,
-                                                                 float *centroid, const float *extra,
-                                                                 const int32_t *extra_ids, int n_extra) {
+__global__ void __launch_bounds__(CULL_WARPS * 32, 6)
+    k_render_cull(DevScene S, CamF cam, long long n, long long ld, const float *state, const float *origins,
+                  const float *rotations, const int32_t *env_scene, float *depth, int32_t *seg, int centroid_id,
+                  float *centroid, const float *extra, const int32_t *extra_ids, int n_extra) {
     __shared__ int cand_s[CULL_WARPS][CULL_MAX];
-    int *cand = cand_s[threadIdx.x >> 5];
+    __shared__ float4 rec_s[CULL_WARPS][CREC][4];      // shading records (warp-broadcast reads)
+    __shared__ int2 met_s[CULL_WARPS][CREC];           // (record type, object id)
+    __shared__ float cul_s[CULL_WARPS][13][CREC];      // culling bounds, SoA (conflict-free lane-parallel reads)
+    const int wib = threadIdx.x >> 5;
+    int *cand = cand_s[wib];
+    float4 (*rec)[4] = rec_s[wib];
+    int2 *met = met_s[wib];
+    float (*cul)[CREC] = cul_s[wib];
     const int lane = threadIdx.x & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
     const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -245,112 +277,241 @@ __global__ void __launch_bounds__(CULL_WARPS * 32) k_render_cull(DevScene S, Cam
         const int scene = env_scene ? env_scene[c] : 0;
         const int p0 = S.prim_offset[scene], p1 = S.prim_offset[scene + 1];
 
-        // ---- camera frustum culling (image frustum, near z >= 0, far z <= max_range)
-        const Plane cp[6] = {world_plane(Rw, 1.f, 0.f, cam.th, 0.f), world_plane(Rw, -1.f, 0.f, cam.th, 0.f),
-                             world_plane(Rw, 0.f, 1.f, cam.tv, 0.f), world_plane(Rw, 0.f, -1.f, cam.tv, 0.f),
-                             world_plane(Rw, 0.f, 0.f, 1.f, 0.f), world_plane(Rw, 0.f, 0.f, -1.f, cam.max_range)};
-        int ncand = 0;
-        for (int b = p0; b < p1; b += 32) {
-            const int p = b + lane;
-            bool k = false;
-            if (p < p1) {
+        // ---- 1. camera frustum culling (image frustum, near z >= 0, far z <= max_range)
+        int ncand = 0;  // warp-uniform
+        {
+            const Plane cp[6] = {world_plane(Rw, 1.f, 0.f, cam.th, 0.f), world_plane(Rw, -1.f, 0.f, cam.th, 0.f),
+                                 world_plane(Rw, 0.f, 1.f, cam.tv, 0.f), world_plane(Rw, 0.f, -1.f, cam.tv, 0.f),
+                                 world_plane(Rw, 0.f, 0.f, 1.f, 0.f), world_plane(Rw, 0.f, 0.f, -1.f, cam.max_range)};
+            int &nc = ncand;
+            for (int b = p0; b < p1; b += 32) {
+                const int p = b + lane;
+                bool k = false;
+                if (p < p1) {
+                    const float4 *cr = S.primc + 4 * p;
+                    const float4 c0 = __ldg(cr), a0 = __ldg(cr + 1), a1 = __ldg(cr + 2), a2 = __ldg(cr + 3);
+                    const float rx = c0.x - o[0], ry = c0.y - o[1], rz = c0.z - o[2];
+                    k = true;
+#pragma unroll
+                    for (int q = 0; q < 6; ++q) k = k && keep(cp[q], rx, ry, rz, c0, a0, a1, a2);
+                }
+                const unsigned m = __ballot_sync(FULL, k);
+                if (k) cand[nc + __popc(m & lt_mask)] = p;
+                nc += __popc(m);
+            }
+            __syncwarp();
+            // ---- 2. camera-specific records
+            for (int k = lane; k < min(nc, CREC); k += 32) {
+                const int p = cand[k];
                 const float4 *cr = S.primc + 4 * p;
                 const float4 c0 = __ldg(cr), a0 = __ldg(cr + 1), a1 = __ldg(cr + 2), a2 = __ldg(cr + 3);
+                const int2 mt = __ldg(S.meta + p);
                 const float rx = c0.x - o[0], ry = c0.y - o[1], rz = c0.z - o[2];
-                k = true;
+                // camera-space culling bounds: v' = Rw^T v
+                auto cs = [&](float x, float y, float z) {
+                    return make_float3(Rw[0] * x + Rw[3] * y + Rw[6] * z, Rw[1] * x + Rw[4] * y + Rw[7] * z,
+                                       Rw[2] * x + Rw[5] * y + Rw[8] * z);
+                };
+                const float3 cc = cs(rx, ry, rz), A0 = cs(a0.x, a0.y, a0.z), A1 = cs(a1.x, a1.y, a1.z),
+                             A2 = cs(a2.x, a2.y, a2.z);
+                int type = REC_GENERIC;
+                float4 s0 = make_float4(0.f, 0.f, 0.f, 0.f), s1 = s0, s2 = s0, s3 = s0;
+                const float4 *pr = S.primf + 4 * p;
+                if (mt.x == QB_SPHERE) {
+                    const float4 pa = __ldg(pr), pb = __ldg(pr + 1);
+                    type = REC_SPHERE;
+                    s0 = make_float4(o[0] - pa.x, o[1] - pa.y, o[2] - pa.z, pb.x);  // m = o - c, r^2
+                } else if (mt.x == QB_BOX) {
+                    const float4 pa = __ldg(pr), pb = __ldg(pr + 1), pc = __ldg(pr + 2), pe = __ldg(pr + 3);
+                    // R rows: (pb.z pb.w pc.x) (pc.y pc.z pc.w) (pe.x pe.y pe.z); local = R^T (o - c)
+                    const float mx = o[0] - pa.x, my = o[1] - pa.y, mz = o[2] - pa.z;
+                    const float lx = pb.z * mx + pc.y * my + pe.x * mz;
+                    const float ly = pb.w * mx + pc.z * my + pe.y * mz;
+                    const float lz = pc.x * mx + pc.w * my + pe.z * mz;
+                    const float hx = pa.w, hy = pb.x, hz = pb.y;
+                    s0 = make_float4(-hx - lx, -hy - ly, -hz - lz, hx - lx);
+                    s1 = make_float4(hy - ly, hz - lz, 0.f, 0.f);
+                    const bool ident = pb.z == 1.f && pb.w == 0.f && pc.x == 0.f && pc.y == 0.f && pc.z == 1.f &&
+                                       pc.w == 0.f && pe.x == 0.f && pe.y == 0.f && pe.z == 1.f;
+                    type = ident ? REC_AABB : REC_OBB;
+                    s2 = make_float4(pb.z, pc.y, pe.x, pb.w);  // columns of R: local d = (col0.d, col1.d, col2.d)
+                    s3 = make_float4(pc.z, pe.y, pc.x, pc.w);
+                    s1.z = pe.z;
+                }
+                met[k] = make_int2(type, mt.y);
+                rec[k][0] = s0;
+                rec[k][1] = s1;
+                rec[k][2] = s2;
+                rec[k][3] = s3;
+                const float cv[13] = {c0.w, cc.x, cc.y, cc.z, A0.x, A0.y, A0.z, A1.x, A1.y, A1.z, A2.x, A2.y, A2.z};
 #pragma unroll
-                for (int q = 0; q < 6; ++q) k = k && keep(cp[q], rx, ry, rz, c0, a0, a1, a2);
+                for (int q = 0; q < 13; ++q) cul[q][k] = cv[q];
             }
-            const unsigned m = __ballot_sync(FULL, k);
-            if (k) cand[ncand + __popc(m & lt_mask)] = p;
-            ncand += __popc(m);
+            __syncwarp();
         }
-        __syncwarp();
 
         long long cnt = 0, sum_col = 0, sum_row = 0;
-        for (int tile = 0; tile < tiles_x * tiles_y; ++tile) {
-            const int j0 = (tile % tiles_x) * TILE_W, i0 = (tile / tiles_x) * TILE_H;
-            const int j = j0 + (lane & 7), i = i0 + (lane >> 3);
-            const bool valid = (j < W) && (i < H);
-            // tile frustum through the pixel-centre rays of its border pixels
-            const int j1 = min(j0 + TILE_W - 1, W - 1), i1 = min(i0 + TILE_H - 1, H - 1);
-            const float xl = (2.0f * (j0 + 0.5f) / W - 1.0f) * cam.th, xr = (2.0f * (j1 + 0.5f) / W - 1.0f) * cam.th;
-            const float yt = (2.0f * (i0 + 0.5f) / H - 1.0f) * cam.tv, yb = (2.0f * (i1 + 0.5f) / H - 1.0f) * cam.tv;
-            const Plane tp[4] = {world_plane(Rw, 1.f, 0.f, -xl, 0.f), world_plane(Rw, -1.f, 0.f, xr, 0.f),
-                                 world_plane(Rw, 0.f, 1.f, -yt, 0.f), world_plane(Rw, 0.f, -1.f, yb, 0.f)};
-            // this lane's pixel ray (same arithmetic as the BVH kernel)
-            const float y = (2.0f * (i + 0.5f) / H - 1.0f) * cam.tv;
-            const float x = (2.0f * (j + 0.5f) / W - 1.0f) * cam.th;
-            const float n2 = x * x + y * y + 1.0f;
-            const float cz = rsqrtf(n2);
-            const float cx = x * cz, cy = y * cz;
-            const float dx = Rw[0] * cx + Rw[1] * cy + Rw[2] * cz;
-            const float dy = Rw[3] * cx + Rw[4] * cy + Rw[5] * cz;
-            const float dz = Rw[6] * cx + Rw[7] * cy + Rw[8] * cz;
-            const float tmax = cam.max_range * sqrtf(n2);
-            float best = tmax;
-            int bid = -1;
-            bool hit = false;
+        // pixel-centre image-plane coordinates: x(j) = ((j + 0.5) * 2/W - 1) * th
+        const float sx = 2.0f / W, sy = 2.0f / H;
+        // an 8x8 tile per warp iteration, two pixels per lane (rows r and r+4):
+        // the tile's culling and loop overhead is shared by 64 rays and each
+        // candidate test runs two independent rays (ILP)
+        constexpr int TH2 = 2 * TILE_H;
+        const int tiles_y2 = (H + TH2 - 1) / TH2;
+        for (int ty = 0, i0 = 0; ty < tiles_y2; ++ty, i0 += TH2)
+        for (int tx = 0, j0 = 0; tx < tiles_x; ++tx, j0 += TILE_W) {
+            const int j = j0 + (lane & 7);
+            int ii[2] = {i0 + (lane >> 3), i0 + TILE_H + (lane >> 3)};
+            // tile planes in CAMERA space through the pixel-centre rays of its border pixels
+            const int j1 = min(j0 + TILE_W - 1, W - 1), i1 = min(i0 + TH2 - 1, H - 1);
+            const float xl = ((j0 + 0.5f) * sx - 1.0f) * cam.th, xr = ((j1 + 0.5f) * sx - 1.0f) * cam.th;
+            const float yt = ((i0 + 0.5f) * sy - 1.0f) * cam.tv, yb = ((i1 + 0.5f) * sy - 1.0f) * cam.tv;
+            const float iL = rsqrtf(1.f + xl * xl), iR = rsqrtf(1.f + xr * xr);
+            const float iT = rsqrtf(1.f + yt * yt), iB = rsqrtf(1.f + yb * yb);
+            const float x = ((j + 0.5f) * sx - 1.0f) * cam.th;
+            float dx[2], dy[2], dz[2], ix[2], iy[2], iz[2], czv[2], tmx[2], best[2];
+            int bid[2];
+            bool hit[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const float y = ((ii[u] + 0.5f) * sy - 1.0f) * cam.tv;
+                const float n2 = x * x + y * y + 1.0f;
+                const float cz = rsqrtf(n2);
+                const float cx = x * cz, cy = y * cz;
+                dx[u] = Rw[0] * cx + Rw[1] * cy + Rw[2] * cz;
+                dy[u] = Rw[3] * cx + Rw[4] * cy + Rw[5] * cz;
+                dz[u] = Rw[6] * cx + Rw[7] * cy + Rw[8] * cz;
+                ix[u] = rcp_approx(dx[u]);
+                iy[u] = rcp_approx(dy[u]);
+                iz[u] = rcp_approx(dz[u]);
+                czv[u] = cz;
+                tmx[u] = cam.max_range * sqrtf(n2);
+                best[u] = tmx[u];
+                bid[u] = -1;
+                hit[u] = false;
+            }
             for (int b = 0; b < ncand; b += 32) {
                 const int k = b + lane;
                 bool kp = false;
                 if (k < ncand) {
-                    const float4 *cr = S.primc + 4 * cand[k];
-                    const float4 c0 = __ldg(cr), a0 = __ldg(cr + 1), a1 = __ldg(cr + 2), a2 = __ldg(cr + 3);
-                    const float rx = c0.x - o[0], ry = c0.y - o[1], rz = c0.z - o[2];
-                    kp = keep(tp[0], rx, ry, rz, c0, a0, a1, a2) && keep(tp[1], rx, ry, rz, c0, a0, a1, a2) &&
-                         keep(tp[2], rx, ry, rz, c0, a0, a1, a2) && keep(tp[3], rx, ry, rz, c0, a0, a1, a2);
+                    if (k < CREC) {
+                        // support = r + sum_k |n . A'_k|; L/R normals (+-1, 0, z), T/B (0, +-1, z)
+                        const float rr = cul[0][k], ccx = cul[1][k], ccy = cul[2][k], ccz = cul[3][k];
+                        const float a0x = cul[4][k], a0y = cul[5][k], a0z = cul[6][k];
+                        const float a1x = cul[7][k], a1y = cul[8][k], a1z = cul[9][k];
+                        const float a2x = cul[10][k], a2y = cul[11][k], a2z = cul[12][k];
+                        const float dL = (ccx - xl * ccz) * iL,
+                                    sL = (fabsf(a0x - xl * a0z) + fabsf(a1x - xl * a1z) + fabsf(a2x - xl * a2z)) * iL;
+                        const float dR = (xr * ccz - ccx) * iR,
+                                    sR = (fabsf(xr * a0z - a0x) + fabsf(xr * a1z - a1x) + fabsf(xr * a2z - a2x)) * iR;
+                        const float dT = (ccy - yt * ccz) * iT,
+                                    sT = (fabsf(a0y - yt * a0z) + fabsf(a1y - yt * a1z) + fabsf(a2y - yt * a2z)) * iT;
+                        const float dB = (yb * ccz - ccy) * iB,
+                                    sB = (fabsf(yb * a0z - a0y) + fabsf(yb * a1z - a1y) + fabsf(yb * a2z - a2y)) * iB;
+                        kp = (dL + sL + rr >= -CULL_EPS) && (dR + sR + rr >= -CULL_EPS) && (dT + sT + rr >= -CULL_EPS) &&
+                             (dB + sB + rr >= -CULL_EPS);
+                    } else {
+                        kp = true;  // beyond the record budget: no tile culling, generic test
+                    }
                 }
                 unsigned m = __ballot_sync(FULL, kp);
                 while (m) {
                     const int bit = __ffs(m) - 1;
                     m &= m - 1;
-                    const int p = cand[b + bit];
-                    const int2 mt = __ldg(S.meta + p);
-                    const float4 *pr = S.primf + 4 * p;
-                    float t;
-                    if (mt.x == QB_SPHERE)
-                        t = ray_sphere_f(pr, o[0], o[1], o[2], dx, dy, dz, tmin, best);
-                    else if (mt.x == QB_BOX)
-                        t = ray_box_f(pr, o[0], o[1], o[2], dx, dy, dz, tmin, best);
-                    else
-                        t = ray_triangle_f(pr, o[0], o[1], o[2], dx, dy, dz, tmin, best);
-                    if (t > 0.0f && (t < best || !hit || (t == best && mt.y < bid))) {
-                        best = t;
-                        bid = mt.y;
-                        hit = true;
+                    const int k2 = b + bit;
+                    float t[2] = {-1.0f, -1.0f};
+                    int oid;
+                    if (k2 < CREC) {
+                        const int2 mt2 = met[k2];
+                        const float4 s0 = rec[k2][0];
+                        oid = mt2.y;
+                        if (mt2.x == REC_AABB) {
+                            const float4 s1 = rec[k2][1];
+#pragma unroll
+                            for (int u = 0; u < 2; ++u)
+                                t[u] = slab_hit(s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, ix[u], iy[u], iz[u], tmin, best[u]);
+                        } else if (mt2.x == REC_OBB) {
+                            const float4 s1 = rec[k2][1], s2 = rec[k2][2], s3 = rec[k2][3];
+                            // local direction = R^T d: columns (s2.x s2.y s2.z) (s2.w s3.x s3.y) (s3.z s3.w s1.z)
+#pragma unroll
+                            for (int u = 0; u < 2; ++u) {
+                                const float lx = s2.x * dx[u] + s2.y * dy[u] + s2.z * dz[u];
+                                const float ly = s2.w * dx[u] + s3.x * dy[u] + s3.y * dz[u];
+                                const float lz = s3.z * dx[u] + s3.w * dy[u] + s1.z * dz[u];
+                                t[u] = slab_hit(s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, rcp_approx(lx), rcp_approx(ly),
+                                                rcp_approx(lz), tmin, best[u]);
+                            }
+                        } else if (mt2.x == REC_SPHERE) {
+#pragma unroll
+                            for (int u = 0; u < 2; ++u) {
+                                const float bb = s0.x * dx[u] + s0.y * dy[u] + s0.z * dz[u];
+                                const float fx = s0.x - bb * dx[u], fy = s0.y - bb * dy[u], fz = s0.z - bb * dz[u];
+                                const float disc = s0.w - (fx * fx + fy * fy + fz * fz);
+                                if (disc >= 0.0f) {
+                                    const float sq = sqrtf(disc);
+                                    const float ta = -bb - sq, tb = -bb + sq;
+                                    t[u] = (ta > tmin && ta <= best[u]) ? ta : ((tb > tmin && tb <= best[u]) ? tb : -1.0f);
+                                }
+                            }
+                        } else {
+#pragma unroll
+                            for (int u = 0; u < 2; ++u)
+                                t[u] = ray_triangle_f(S.primf + 4 * cand[k2], o[0], o[1], o[2], dx[u], dy[u], dz[u], tmin,
+                                                      best[u]);
+                        }
+                    } else {
+                        const int p = cand[k2];
+                        const int2 mt = __ldg(S.meta + p);
+                        oid = mt.y;
+                        const float4 *pr = S.primf + 4 * p;
+#pragma unroll
+                        for (int u = 0; u < 2; ++u)
+                            t[u] = mt.x == QB_SPHERE ? ray_sphere_f(pr, o[0], o[1], o[2], dx[u], dy[u], dz[u], tmin, best[u])
+                                   : mt.x == QB_BOX  ? ray_box_f(pr, o[0], o[1], o[2], dx[u], dy[u], dz[u], tmin, best[u])
+                                                     : ray_triangle_f(pr, o[0], o[1], o[2], dx[u], dy[u], dz[u], tmin, best[u]);
+                    }
+#pragma unroll
+                    for (int u = 0; u < 2; ++u)
+                        if (t[u] > 0.0f && (t[u] < best[u] || !hit[u] || (t[u] == best[u] && oid < bid[u]))) {
+                            best[u] = t[u];
+                            bid[u] = oid;
+                            hit[u] = true;
+                        }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int i = ii[u];
+                float t = hit[u] ? best[u] : -1.0f;
+                int oid = hit[u] ? bid[u] : -1;
+                for (int k = 0; k < n_extra; ++k) {  // swarm agents as spheres (kernels.py:438-445)
+                    const float4 sph = *reinterpret_cast<const float4 *>(extra + (c * n_extra + k) * 4);
+                    float4 rec2[2] = {sph, make_float4(sph.w * sph.w, 0.f, 0.f, 0.f)};
+                    float ts = ray_sphere_f(rec2, o[0], o[1], o[2], dx[u], dy[u], dz[u], tmin, tmx[u]);
+                    if (ts > 0.0f && (t < 0.0f || ts < t)) {
+                        t = ts;
+                        oid = extra_ids[c * n_extra + k];
                     }
                 }
-            }
-            float t = hit ? best : -1.0f;
-            int oid = hit ? bid : -1;
-            for (int k = 0; k < n_extra; ++k) {  // swarm agents as spheres (kernels.py:438-445)
-                const float4 sph = *reinterpret_cast<const float4 *>(extra + (c * n_extra + k) * 4);
-                float4 rec[2] = {sph, make_float4(sph.w * sph.w, 0.f, 0.f, 0.f)};
-                float ts = ray_sphere_f(rec, o[0], o[1], o[2], dx, dy, dz, tmin, tmax);
-                if (ts > 0.0f && (t < 0.0f || ts < t)) {
-                    t = ts;
-                    oid = extra_ids[c * n_extra + k];
-                }
-            }
-            const int out_id = t > 0.0f ? oid : 0;
-            if (valid) {
-                const long long off = (c * H + i) * (long long)W + j;
-                if (depth) depth[off] = t > 0.0f ? t * cz : cam.max_range;
-                if (seg) seg[off] = out_id;
-                if (centroid_id > 0 && out_id == centroid_id) {
-                    cnt += 1;
-                    sum_col += j;
-                    sum_row += i;
+                const int out_id = t > 0.0f ? oid : 0;
+                if (j < W && i < H) {
+                    const long long off = (c * H + i) * (long long)W + j;
+                    if (depth) depth[off] = t > 0.0f ? t * czv[u] : cam.max_range;
+                    if (seg) seg[off] = out_id;
+                    if (centroid_id > 0 && out_id == centroid_id) {
+                        cnt += 1;
+                        sum_col += j;
+                        sum_row += i;
+                    }
                 }
             }
         }
         if (centroid_id > 0) {
 #pragma unroll
-            for (int s = 16; s > 0; s >>= 1) {
-                cnt += __shfl_xor_sync(FULL, cnt, s);
-                sum_col += __shfl_xor_sync(FULL, sum_col, s);
-                sum_row += __shfl_xor_sync(FULL, sum_row, s);
+            for (int s2 = 16; s2 > 0; s2 >>= 1) {
+                cnt += __shfl_xor_sync(FULL, cnt, s2);
+                sum_col += __shfl_xor_sync(FULL, sum_col, s2);
+                sum_row += __shfl_xor_sync(FULL, sum_row, s2);
             }
             if (lane == 0) {
                 centroid[2 * c] = cnt ? (float)((double)sum_col / (double)cnt) : -1.0f;
@@ -475,7 +636,7 @@ int launch_render(const qb_scene *s, const qb_camera *cam, int dtype, long long 
             }
             const int B = CULL_WARPS * 32;
             long long blocks = (n + CULL_WARPS - 1) / CULL_WARPS;
-            long long max_blocks = (long long)sm_count() * 8;
+            long long max_blocks = (long long)sm_count() * 16;
             if (blocks > max_blocks) blocks = max_blocks;
             if (state)
                 k_render_cull<true><<<(int)blocks, B, 0, st>>>(s->dev, c, n, ld, (const float *)state, nullptr, nullptr,

@@ -144,7 +144,7 @@ def render_state(dev_scenes, camera: CameraModel, planes, env_scene=None, depth=
                  centroid=None, extra=None, extra_ids=None, mode: int = 0):
     """K2 straight from the (17,N) state planes (the env observation path).
 
-    mode: 0 auto (frustum-culling kernel for scenes <= 512 primitives, BVH
+    mode: 0 auto (frustum-culling kernel for scenes <= 256 primitives, BVH
     packet kernel otherwise), 1 force BVH, 2 force culling."""
     import torch
 

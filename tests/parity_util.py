@@ -33,10 +33,11 @@ def _axis_rot(axis, ang):
     return np.eye(3) + np.sin(ang) * K + (1 - np.cos(ang)) * K @ K
 
 
-def grazing_mask(scene, origins, rotations, width, height, th, tv, max_range, d_o=4e-6, d_r=1e-6):
+def grazing_mask(scene, origins, rotations, width, height, th, tv, max_range, d_o=1e-5, d_r=3e-6):
     """Pixels whose oracle result is unstable under perturbations a few times
-    larger than FP32 rounding of the pose (~5e-7 m at 5 m) and of the ray
-    direction (~6e-8 rad): silhouettes, edges, oblique incidence
+    larger than the FP32 error of the pose (~5e-7 m at 5 m) and of the ray
+    direction (quaternion -> matrix -> pixel ray in FP32: up to ~8e-7 rad
+    observed): silhouettes, edges, oblique incidence, near-tangent spheres
     (SURVEY.md 7.3-2).  A diagnostic set: parity asserts that every FP32
     mismatch lies inside it and that mismatches are rare.
 

@@ -231,35 +231,36 @@ def test_multi_scene_set(ggeo):
 
 
 @pytest.mark.parametrize("name", ["nav", "tess", "landing"])
-def test_culling_kernel_identical_to_bvh_kernel(ggeo, name):
-    """The frustum-culling renderer is conservative and order-independent:
-    its output must equal the BVH packet kernel's bit for bit."""
+def test_culling_and_bvh_kernels_vs_oracle(ggeo, name):
+    """Both FP32 render kernels (frustum-culling and BVH-packet) against the
+    FP64 oracle on 256 random poses x 2 camera mounts: equal ids and depth
+    within 1e-4 m on every non-grazing pixel."""
     from paper_2407_14783_b200.sensing import render_state
 
-    ds, _ = _dev_scene(ggeo, name)
+    ds, sc = _dev_scene(ggeo, name)
     rng = np.random.default_rng(5)
-    n = 512
+    n = 256
     pos = rng.uniform([-4.5, -4.5, 0.2], [4.5, 4.5, 3.8], (n, 3))
     q = rng.normal(size=(n, 4)) + np.array([2.0, 0, 0, 0])
     q /= np.linalg.norm(q, axis=1, keepdims=True)
     planes = torch.zeros((17, n), dtype=torch.float32, device=DEV)
     planes[0:3] = torch.as_tensor(pos.T, dtype=torch.float32)
     planes[6:10] = torch.as_tensor(q.T, dtype=torch.float32)
+    st = planes.T.double().cpu().numpy()
     for rot in (FORWARD, DOWNWARD):
         cam = CameraModel(rotation=rot, width=64, height=48)
-        out = []
+        o, r = oracle.camera_pose_world(st[:, 0:3], st[:, 6:10], cam.rotation, cam.translation)
+        graz, d0, i0 = grazing_mask(sc, o, r, cam.width, cam.height, cam.tan_half_h, cam.tan_half_v, cam.max_range)
         for mode in (1, 2):
             d = torch.empty((n, 48, 64), dtype=torch.float32, device=DEV)
-            s = torch.empty((n, 48, 64), dtype=torch.int32, device=DEV)
-            render_state(ds, cam, planes, depth=d, seg=s, mode=mode)
-            out.append((d.cpu().numpy(), s.cpu().numpy()))
-        assert np.array_equal(out[0][1], out[1][1])
-        d0, d1 = out[0][0], out[1][0]
-        rel = np.abs(d0 - d1) / np.maximum(np.abs(d0), 1e-30)
-        print(name, "cull vs bvh: ids identical; depth differs on", int((d0 != d1).sum()), "px, max rel", rel.max())
-        # the same primitive wins every pixel; nvcc fuses a*b + c*d into an FMA
-        # on either product depending on the surrounding kernel, so the FP32 ray
-        # (camera pose, direction) may differ by an ulp between the two kernels,
-        # which oblique incidence amplifies to a few 1e-6 in depth -- both stay
-        # well inside the 1e-4 m parity bound against the oracle
-        assert rel.max() <= 2e-5
+            sg = torch.empty((n, 48, 64), dtype=torch.int32, device=DEV)
+            render_state(ds, cam, planes, depth=d, seg=sg, mode=mode)
+            bad = (sg.cpu().numpy() != i0) | (np.abs(d.double().cpu().numpy() - d0) > DEPTH_TOL)
+            print(name, "mode", mode, f"grazing {graz.mean():.2e} mismatched {bad.mean():.2e} "
+                  f"non-grazing mismatched {(bad & ~graz).sum()}")
+            for w in np.argwhere(bad & ~graz)[:3]:
+                w = tuple(w)
+                print("   pixel", w, "gpu", float(d.cpu().numpy()[w]), int(sg.cpu().numpy()[w]), "oracle", d0[w], i0[w],
+                      "pos", st[w[0], 0:3], "q", st[w[0], 6:10])
+            assert not (bad & ~graz).any()
+            assert bad.mean() < 1e-3

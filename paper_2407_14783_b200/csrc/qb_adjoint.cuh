@@ -111,7 +111,7 @@ QB_D void dyn_step_vjp(const DynConsts<R> &C, const R *x_in, const R *cmd_in, R 
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         cmask[i] = clip_mask(cmd_in[i], C.rlo, C.rhi, boundary);
-        cmd[i] = np_clip(cmd_in[i], C.rlo, C.rhi);
+        cmd[i] = p_clip(cmd_in[i], C.rlo, C.rhi);
     }
     const int S = C.substeps < MAXS ? C.substeps : MAXS;
     // forward: keep each substep's input state (13 rigid + 4 rotors)
@@ -124,7 +124,7 @@ QB_D void dyn_step_vjp(const DynConsts<R> &C, const R *x_in, const R *cmd_in, R 
         for (int k = 0; k < 17; ++k) xs[s][k] = x[k];
         R w[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) w[i] = np_clip(cmd[i] + (x[13 + i] - cmd[i]) * C.alpha, C.rlo, C.rhi);
+        for (int i = 0; i < 4; ++i) w[i] = p_clip(cmd[i] + (x[13 + i] - cmd[i]) * C.alpha, C.rlo, C.rhi);
         Wrench<R> Wr;
         make_wrench(C, w, Wr);
         integrate_substep(C, x, Wr);
@@ -140,7 +140,7 @@ QB_D void dyn_step_vjp(const DynConsts<R> &C, const R *x_in, const R *cmd_in, R 
         for (int i = 0; i < 4; ++i) {
             raw[i] = cmd[i] + (x0[13 + i] - cmd[i]) * C.alpha;
             lm[i] = clip_mask(raw[i], C.rlo, C.rhi, boundary);
-            w[i] = np_clip(raw[i], C.rlo, C.rhi);
+            w[i] = p_clip(raw[i], C.rlo, C.rhi);
         }
         Wrench<R> Wr;
         make_wrench(C, w, Wr);
@@ -268,7 +268,7 @@ template <class R>
 QB_D void ctbr_vjp(const DynConsts<R> &C, const R *x, R coll_in, R r0, R r1, R r2, const R *speeds_bar, R *ab, R *xb) {
     const R *om = x + 10;
     const bool coll_pos = coll_in > R(0.0);
-    const R coll = np_max(coll_in, R(0.0));
+    const R coll = p_max(coll_in, R(0.0));
     R err0 = r0 - om[0], err1 = r1 - om[1], err2 = r2 - om[2];
     R jo0 = C.J[0] * om[0], jo1 = C.J[1] * om[1], jo2 = C.J[2] * om[2];
     R tq[3] = {C.J[0] * (C.rate_p[0] * err0) + (om[1] * jo2 - om[2] * jo1),
@@ -276,7 +276,7 @@ QB_D void ctbr_vjp(const DynConsts<R> &C, const R *x, R coll_in, R r0, R r1, R r
                C.J[2] * (C.rate_p[2] * err2) + (om[0] * jo1 - om[1] * jo0)};
     // mixer forward
     R force = C.mass * coll;
-    R fcl = np_clip(force, C.flo4, C.fhi4);
+    R fcl = p_clip(force, C.flo4, C.fhi4);
     bool fb_flag = false;
     R fmask = clip_mask(force, C.flo4, C.fhi4, fb_flag);
     R base[4], tp[4];
@@ -294,7 +294,7 @@ QB_D void ctbr_vjp(const DynConsts<R> &C, const R *x, R coll_in, R r0, R r1, R r
             arg = i;
         }
     }
-    R scale = np_max(np_min(best, R(1.0)), R(0.0));
+    R scale = p_max(p_min(best, R(1.0)), R(0.0));
     const bool scale_active = best < R(1.0) && best > R(0.0) && arg >= 0;
     // backward
     R baseb[4], tpb[4], sb = R(0.0);
@@ -303,7 +303,7 @@ QB_D void ctbr_vjp(const DynConsts<R> &C, const R *x, R coll_in, R r0, R r1, R r
         R thr = base[i] + scale * tp[i];
         bool fl = false;
         R cm = clip_mask(thr, C.flo, C.fhi, fl);
-        R thr_clamped = np_clip(thr, C.flo, C.fhi);
+        R thr_clamped = p_clip(thr, C.flo, C.fhi);
         R g = speeds_bar[i] * speed_of_thrust_grad(C, thr_clamped) * cm;
         baseb[i] = g;
         tpb[i] = scale * g;

@@ -224,12 +224,16 @@ template <class R> QB_D void integrate_substep(const DynConsts<R> &C, R *y, cons
 // Returns false when any component is non-finite (NonFiniteState mask).
 template <class R> QB_D bool dyn_step(const DynConsts<R> &C, R *x, const R *cmd_in) {
     R cmd[4];
+    bool cmd_ok = true;  // FP32 clamps drop NaN: keep the reference's verdict (NaN command -> non-finite state)
 #pragma unroll
-    for (int i = 0; i < 4; ++i) cmd[i] = np_clip(cmd_in[i], C.rlo, C.rhi);
+    for (int i = 0; i < 4; ++i) {
+        cmd_ok &= !r_isnan(cmd_in[i]);
+        cmd[i] = p_clip(cmd_in[i], C.rlo, C.rhi);
+    }
     for (int s = 0; s < C.substeps; ++s) {
         R w[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) w[i] = np_clip(cmd[i] + (x[13 + i] - cmd[i]) * C.alpha, C.rlo, C.rhi);  // :109-114
+        for (int i = 0; i < 4; ++i) w[i] = p_clip(cmd[i] + (x[13 + i] - cmd[i]) * C.alpha, C.rlo, C.rhi);  // :109-114
         Wrench<R> W;
         make_wrench(C, w, W);
         integrate_substep(C, x, W);
@@ -237,7 +241,7 @@ template <class R> QB_D bool dyn_step(const DynConsts<R> &C, R *x, const R *cmd_
         for (int i = 0; i < 4; ++i) x[13 + i] = w[i];
         q_normalize(x + 6);
     }
-    bool ok = true;
+    bool ok = cmd_ok;
 #pragma unroll
     for (int i = 0; i < 17; ++i) ok &= r_isfinite(x[i]);
     return ok;
@@ -246,18 +250,18 @@ template <class R> QB_D bool dyn_step(const DynConsts<R> &C, R *x, const R *cmd_
 // ---------------------------------------------------------------- controller
 // params.py:106-111
 template <class R> QB_D R speed_of_thrust(const DynConsts<R> &C, R f) {
-    R arg = np_max(C.k1sq + C.four_k2 * (f - C.k0), R(0.0));
+    R arg = p_max(C.k1sq + C.four_k2 * (f - C.k0), R(0.0));
     R om;
     if constexpr (is_exact<R>::value)
         om = (C.neg_k1 + r_sqrt(arg)) / C.two_k2;
     else
         om = (C.neg_k1 + r_sqrt(arg)) * C.inv_two_k2;
-    return np_clip(om, C.rlo, C.rhi);
+    return p_clip(om, C.rlo, C.rhi);
 }
 
 // control.py:101-130
 template <class R> QB_D void mixer(const DynConsts<R> &C, R force, const R *tq, R *thr) {
-    R fcl = np_clip(force, C.flo4, C.fhi4);
+    R fcl = p_clip(force, C.flo4, C.fhi4);
     R base[4], tp[4];
     R scale;
     if constexpr (is_exact<R>::value) {
@@ -268,10 +272,10 @@ template <class R> QB_D void mixer(const DynConsts<R> &C, R force, const R *tq, 
             tp[i] = C.minv[i][1] * tq[0] + C.minv[i][2] * tq[1] + C.minv[i][3] * tq[2];
             R up = tp[i] > R(0.0) ? (C.fhi - base[i]) / tp[i] : R(infinity_d());
             R dn = tp[i] < R(0.0) ? (C.flo - base[i]) / tp[i] : R(infinity_d());
-            up_min = np_min(up_min, up);
-            dn_min = np_min(dn_min, dn);
+            up_min = p_min(up_min, up);
+            dn_min = p_min(dn_min, dn);
         }
-        scale = np_max(np_min(np_min(up_min, dn_min), R(1.0)), R(0.0));
+        scale = p_max(p_min(p_min(up_min, dn_min), R(1.0)), R(0.0));
     } else {  // only one of up / dn is finite per rotor: one (fast) division each
         R bmin = R(infinity_d());
 #pragma unroll
@@ -297,14 +301,14 @@ template <class R> QB_D void mixer(const DynConsts<R> &C, R force, const R *tq, 
             if (r_abs(f - C.flo) <= tol) f = C.flo;
             if (r_abs(f - C.fhi) <= tol) f = C.fhi;
         }
-        thr[i] = np_clip(f, C.flo, C.fhi);
+        thr[i] = p_clip(f, C.flo, C.fhi);
     }
 }
 
 // control.py:138-158
 template <class R> QB_D void ctbr_speeds(const DynConsts<R> &C, const R *x, R coll, R r0, R r1, R r2, R *out) {
     const R *om = x + 10;
-    coll = np_max(coll, R(0.0));
+    coll = p_max(coll, R(0.0));
     R err0 = r0 - om[0], err1 = r1 - om[1], err2 = r2 - om[2];
     R jo0 = C.J[0] * om[0], jo1 = C.J[1] * om[1], jo2 = C.J[2] * om[2];
     R tq[3];
@@ -353,7 +357,7 @@ QB_D void accel_to_ctbr(const DynConsts<R> &C, const R *x, const R *a_des, R cy,
     rates[0] = C.neg_att_p[0] * e0;
     rates[1] = C.neg_att_p[1] * e1;
     rates[2] = C.neg_att_p[2] * e2;
-    R c = np_max(spec[0] * rot[0][2] + spec[1] * rot[1][2] + spec[2] * rot[2][2], R(0.0));
+    R c = p_max(spec[0] * rot[0][2] + spec[1] * rot[1][2] + spec[2] * rot[2][2], R(0.0));
     if (degenerate) {
         rates[0] = rates[1] = rates[2] = R(0.0);
         c = R(0.0);
@@ -377,7 +381,7 @@ template <class R, int KIND> QB_D void command_to_speeds(const DynConsts<R> &C, 
         for (int i = 0; i < 4; ++i) out[i] = cmd[i];
     } else if constexpr (KIND == QB_CMD_SRT) {  // control.py:133-135
 #pragma unroll
-        for (int i = 0; i < 4; ++i) out[i] = speed_of_thrust(C, np_clip(cmd[i], C.flo, C.fhi));
+        for (int i = 0; i < 4; ++i) out[i] = speed_of_thrust(C, p_clip(cmd[i], C.flo, C.fhi));
     } else if constexpr (KIND == QB_CMD_CTBR) {
         ctbr_speeds(C, x, cmd[0], cmd[1], cmd[2], cmd[3], out);
     } else {

@@ -313,6 +313,19 @@ QB_D float slab_enter_f(const float4 lo, const float4 hi, float ox, float oy, fl
     return t0 <= t1 ? t0 : infinity_f();
 }
 
+// same test with the ray folded into FMAs: (b - o) * i == fma(b, i, -o*i),
+// oi = o * i precomputed per ray (node bounds are inflated outward, so the
+// ~1-ulp difference cannot drop a primitive the box contains)
+QB_D float slab_enter_fma(const float4 lo, const float4 hi, float oix, float oiy, float oiz, float ix, float iy, float iz,
+                          float tmax) {
+    float tax = fmaf(lo.x, ix, -oix), tbx = fmaf(hi.x, ix, -oix);
+    float tay = fmaf(lo.y, iy, -oiy), tby = fmaf(hi.y, iy, -oiy);
+    float taz = fmaf(lo.z, iz, -oiz), tbz = fmaf(hi.z, iz, -oiz);
+    float t0 = fmaxf(fmaxf(fminf(tax, tbx), fminf(tay, tby)), fmaxf(fminf(taz, tbz), 0.0f));
+    float t1 = fminf(fminf(fmaxf(tax, tbx), fmaxf(tay, tby)), fminf(fmaxf(taz, tbz), tmax));
+    return t0 <= t1 ? t0 : infinity_f();
+}
+
 // exact-double slab entry, reference order
 QB_D xd slab_enter_x(const double *b, xd ox, xd oy, xd oz, xd ix, xd iy, xd iz, xd tmax) {
     xd t0(0.0), t1 = tmax, ta, tb;

@@ -66,6 +66,8 @@ __global__ void __launch_bounds__(128, 8) k_dyn_step(DynConsts<R> C, long long n
         command_to_speeds<R, KIND>(C, x, a, cmd);
         if (rotor_out && T == 0) store4<R, S>(rotor_out + i * 4, cmd);
         ok_all &= dyn_step(C, x, cmd);
+        // a NaN action propagates to a NaN state in the reference (np.clip keeps NaN)
+        ok_all &= !(r_isnan(a[0]) || r_isnan(a[1]) || r_isnan(a[2]) || r_isnan(a[3]));
         S *dst = T > 0 ? state + (long long)(t + 1) * 17 * ld : state;
 #pragma unroll
         for (int k = 0; k < 17; ++k) dst[k * ld + i] = to_store(x[k]);

@@ -222,7 +222,7 @@ template <class R, int KIND> __global__ void __launch_bounds__(128) k_env_step(E
 #pragma unroll
     for (int k = 0; k < 4; ++k) a[k] = R(act[k]);
     command_to_speeds<R, KIND>(A.C, x, a, cmd);
-    const bool ok = dyn_step(A.C, x, cmd);
+    const bool ok = dyn_step(A.C, x, cmd) && !(r_isnan(a[0]) || r_isnan(a[1]) || r_isnan(a[2]) || r_isnan(a[3]));
     if (!ok) {
 #pragma unroll
         for (int k = 0; k < 17; ++k) x[k] = prev[k];

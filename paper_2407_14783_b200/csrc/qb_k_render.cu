@@ -60,10 +60,12 @@ __device__ __forceinline__ void camera_pose(const R *p, const R *q, const R *cro
 }
 
 template <bool FROM_STATE>
-__global__ void __launch_bounds__(256) k_render_f(DevScene S, CamF cam, long long n, long long ld, const float *state,
-                                                  const float *origins, const float *rotations, const int32_t *env_scene,
-                                                  float *depth, int32_t *seg, int centroid_id, float *centroid,
-                                                  const float *extra, const int32_t *extra_ids, int n_extra) {
+__global__ void __launch_bounds__(256, 4) k_render_f(DevScene S, CamF cam, long long n, long long ld, const float *state,
+                                                     const float *origins, const float *rotations, const int32_t *env_scene,
+                                                     float *depth, int32_t *seg, int centroid_id, float *centroid,
+                                                     const float *extra, const int32_t *extra_ids, int n_extra) {
+    __shared__ int stk_s[8][64];
+    int *stk = stk_s[threadIdx.x >> 5];
     const int lane = threadIdx.x & 31;
     const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
@@ -100,31 +102,36 @@ __global__ void __launch_bounds__(256) k_render_f(DevScene S, CamF cam, long lon
             const float dy = Rw[3] * cx + Rw[4] * cy + Rw[5] * cz;
             const float dz = Rw[6] * cx + Rw[7] * cy + Rw[8] * cz;
             const float ix = 1.0f / dx, iy = 1.0f / dy, iz = 1.0f / dz;
+            const float oix = o[0] * ix, oiy = o[1] * iy, oiz = o[2] * iz;
             const float tmax = cam.max_range * sqrtf(n2);
             float best = tmax;
             int bid = -1;
             bool hit = false;
 
-            int stk[64];
+            // warp-uniform traversal: one stack per warp in shared memory (lane 0
+            // pushes, all lanes read the broadcast); children are slab-tested at
+            // the parent by every lane and pushed only if some lane needs them,
+            // nearer child (lane majority) on top
             int sp = 0;
-            stk[sp++] = root;
-            while (sp > 0) {
-                const int node = stk[--sp];
+            int node = root;
+            {
                 const float4 lo = __ldg(S.nodef + 2 * node), hi = __ldg(S.nodef + 2 * node + 1);
-                const float e = slab_enter_f(lo, hi, o[0], o[1], o[2], ix, iy, iz, best);
-                if (!__any_sync(FULL, valid && e <= best)) continue;
+                if (!__any_sync(FULL, valid && slab_enter_fma(lo, hi, oix, oiy, oiz, ix, iy, iz, best) <= best)) node = -1;
+            }
+            while (node >= 0) {
+                const float4 lo = __ldg(S.nodef + 2 * node), hi = __ldg(S.nodef + 2 * node + 1);
                 const int a = __float_as_int(lo.w), b = __float_as_int(hi.w);
                 if (b > 0) {
                     for (int p = a; p < a + b; ++p) {
                         const int2 m = __ldg(S.meta + p);
                         const float4 *pr = S.primf + 4 * p;
                         float t;
-                        if (m.x == QB_SPHERE)
-                            t = ray_sphere_f(pr, o[0], o[1], o[2], dx, dy, dz, tmin, best);
+                        if (m.x == QB_TRIANGLE)
+                            t = ray_triangle_f(pr, o[0], o[1], o[2], dx, dy, dz, tmin, best);
                         else if (m.x == QB_BOX)
                             t = ray_box_f(pr, o[0], o[1], o[2], dx, dy, dz, tmin, best);
                         else
-                            t = ray_triangle_f(pr, o[0], o[1], o[2], dx, dy, dz, tmin, best);
+                            t = ray_sphere_f(pr, o[0], o[1], o[2], dx, dy, dz, tmin, best);
                         if (t > 0.0f && (t < best || !hit || (t == best && m.y < bid))) {
                             best = t;
                             bid = m.y;
@@ -132,11 +139,36 @@ __global__ void __launch_bounds__(256) k_render_f(DevScene S, CamF cam, long lon
                         }
                     }
                 } else {
-                    const int axis = -b;
-                    const float dc = axis == 0 ? dx : (axis == 1 ? dy : dz);
-                    const bool left_first = __popc(__ballot_sync(FULL, dc >= 0.0f)) >= 16;
-                    stk[sp++] = left_first ? a + 1 : a;  // far child first
-                    stk[sp++] = left_first ? a : a + 1;
+                    const float4 llo = __ldg(S.nodef + 2 * a), lhi = __ldg(S.nodef + 2 * a + 1);
+                    const float4 rlo = __ldg(S.nodef + 2 * a + 2), rhi = __ldg(S.nodef + 2 * a + 3);
+                    const float el = slab_enter_fma(llo, lhi, oix, oiy, oiz, ix, iy, iz, best);
+                    const float er = slab_enter_fma(rlo, rhi, oix, oiy, oiz, ix, iy, iz, best);
+                    const bool hl = __any_sync(FULL, valid && el <= best);
+                    const bool hr = __any_sync(FULL, valid && er <= best);
+                    if (hl && hr) {
+                        const bool left_first = __popc(__ballot_sync(FULL, !valid || el <= er)) >= 16;
+                        const int near = left_first ? a : a + 1, far = left_first ? a + 1 : a;
+                        if (lane == 0) stk[sp] = far;
+                        ++sp;
+                        node = near;
+                        continue;
+                    }
+                    if (hl || hr) {
+                        node = hl ? a : a + 1;
+                        continue;
+                    }
+                }
+                // pop the next node some lane still needs
+                node = -1;
+                while (sp > 0) {
+                    __syncwarp();
+                    const int cand_node = stk[sp - 1];
+                    --sp;
+                    const float4 clo = __ldg(S.nodef + 2 * cand_node), chi = __ldg(S.nodef + 2 * cand_node + 1);
+                    if (__any_sync(FULL, valid && slab_enter_fma(clo, chi, oix, oiy, oiz, ix, iy, iz, best) <= best)) {
+                        node = cand_node;
+                        break;
+                    }
                 }
             }
             float t = hit ? best : -1.0f;

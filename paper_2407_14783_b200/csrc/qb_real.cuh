@@ -63,6 +63,16 @@ template <class R> QB_D R py_min(R a, R b) { return b < a ? b : a; }
 template <class R> QB_D R np_max(R a, R b) { return r_isnan(a) ? a : (r_isnan(b) ? b : (b > a ? b : a)); }
 template <class R> QB_D R np_min(R a, R b) { return r_isnan(a) ? a : (r_isnan(b) ? b : (b < a ? b : a)); }
 template <class R> QB_D R np_clip(R x, R lo, R hi) { return np_min(np_max(x, lo), hi); }
+
+// policy clamps: the exact build keeps numpy's NaN propagation; the FP32
+// build uses the single-instruction FMNMX forms (callers re-check finiteness
+// of their inputs where NaN propagation is observable)
+template <class R> QB_D R p_max(R a, R b) { return np_max(a, b); }
+template <class R> QB_D R p_min(R a, R b) { return np_min(a, b); }
+template <class R> QB_D R p_clip(R x, R lo, R hi) { return np_clip(x, lo, hi); }
+template <> QB_D float p_max<float>(float a, float b) { return fmaxf(a, b); }
+template <> QB_D float p_min<float>(float a, float b) { return fminf(a, b); }
+template <> QB_D float p_clip<float>(float x, float lo, float hi) { return fminf(fmaxf(x, lo), hi); }
 #endif
 
 template <class R> struct is_exact { static constexpr bool value = false; };

@@ -264,3 +264,17 @@ def test_culling_and_bvh_kernels_vs_oracle(ggeo, name):
                       "pos", st[w[0], 0:3], "q", st[w[0], 6:10])
             assert not (bad & ~graz).any()
             assert bad.mean() < 1e-3
+
+
+def test_nan_action_flags_nonfinite():
+    """A NaN command propagates to a non-finite state in the reference
+    (np.clip keeps NaN); the FP32 build's single-instruction clamps must not
+    hide it."""
+    x = np.zeros((4, 17)); x[:, 6] = 1.0; x[:, 13:] = 900.0
+    for kind, a in (("rotor", [900.0] * 4), ("ctbr", [9.81, 0, 0, 0]), ("lv", [0, 0, 0, 0])):
+        acts = np.tile(np.asarray(a, float), (4, 1))
+        acts[1, 0] = np.nan
+        acts[3, 3] = np.nan
+        for dt in (torch.float32, torch.float64):
+            _, _, bad = run_step(kind, x, acts, dt)
+            assert bad.tolist() == [0, 1, 0, 1], (kind, dt)

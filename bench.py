@@ -185,7 +185,7 @@ def make_actions(kind, n, count, rank):
         a[..., :3] = torch.randn((count, n, 3), device="cuda", generator=g) * 1.5
         a[..., 0] += 1.0
         a[..., 3] = (torch.rand((count, n), device="cuda", generator=g) * 2 - 1) * math.pi
-    return [a[i].contiguous() for i in range(count)]
+    return a  # (count, n, 4) contiguous; a[i] is step i's (n, 4) action
 
 
 def run_env(args, rank, world, kind):
@@ -199,17 +199,17 @@ def run_env(args, rank, world, kind):
     env.reset(seed=args.seed)
     n, K, W = env.num_agents, args.steps, args.warmup
     acts = make_actions(kind, n, K + W, rank)
-    small = n <= 4096  # latency-bound configs (1, 2): replay the step as a CUDA graph
+    small = n <= 4096  # latency-bound configs (1, 2): replay 10-step CUDA graphs
+    G = 10
     graph = None
     if small:
-        static_a = torch.empty_like(acts[0])
-        graph = env.make_step_graph(static_a, steps=1)
+        K = max(G, (K + G - 1) // G * G)
+        args.steps = K
+        acts = make_actions(kind, n, K + W, rank)
+        static_a = torch.empty((G, n, 4), device="cuda")
+        graph = env.make_step_graph(static_a)
 
     def launch(a, events=None):
-        if graph is not None:
-            static_a.copy_(a)
-            graph()
-            return
         env._bufs.action = a.data_ptr()
         if events:
             events[0].record()
@@ -223,8 +223,14 @@ def run_env(args, rank, world, kind):
         if events:
             events[2].record()
 
+    def launch_graph(first):
+        static_a.copy_(acts[first:first + G])  # stage the next G steps' actions (one device copy)
+        graph()
+
     for i in range(W):
         launch(acts[i])
+    if small:
+        launch_graph(0)
     torch.cuda.synchronize()
     ev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(3)) for _ in range(K)]
     barrier(world)
@@ -233,8 +239,12 @@ def run_env(args, rank, world, kind):
     clk.start()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0.record()
-    for k in range(K):
-        launch(acts[W + k], None if small else ev[k])
+    if small:
+        for k in range(0, K, G):
+            launch_graph(W + k)
+    else:
+        for k in range(K):
+            launch(acts[W + k], ev[k])
     t1.record()
     torch.cuda.synchronize()
     clocks = clk.stop()
@@ -491,7 +501,8 @@ def main():
                                 "resolution": "64x64", "integrator": "rk4, 2 substeps",
                                 "sensors": ",".join(f"{s.name}:{s.kind}" for s in r["cfg"].sensors) or "none",
                                 "l2": "per-step output (depth+seg, 2.1 GB at c3) >> 126 MB L2; no flush needed"
-                                if not r["graph"] else "100 envs: latency-bound, step replayed as a CUDA graph",
+                                if not r["graph"] else "100 envs: latency-bound; 10 env steps per CUDA-graph replay "
+                                                       "(actions staged by device copies inside the timed region)",
                                 "parallelism": f"env shards x{world}, no per-step collective"}})
         if "render_ms" in r:
             line["kernel_ms"] = {"env_step_k1k3": r["step_ms"], "render_k2": r["render_ms"]}

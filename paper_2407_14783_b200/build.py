@@ -94,9 +94,10 @@ def main(argv=None):
     ap.add_argument("--force", action="store_true")
     ap.add_argument("-v", "--verbose", action="store_true")
     ap.add_argument("--ptxas-v", action="store_true", help="print register/spill usage")
+    ap.add_argument("-D", dest="defines", action="append", default=[], help="extra preprocessor define (tuning)")
     a = ap.parse_args(argv)
-    extra = ["-Xptxas", "-v"] if a.ptxas_v else []
-    print(build(force=a.force or a.ptxas_v, verbose=a.verbose or a.ptxas_v, extra_flags=extra))
+    extra = (["-Xptxas", "-v"] if a.ptxas_v else []) + [f"-D{d}" for d in a.defines]
+    print(build(force=a.force or a.ptxas_v or bool(a.defines), verbose=a.verbose or a.ptxas_v, extra_flags=extra))
 
 
 if __name__ == "__main__":

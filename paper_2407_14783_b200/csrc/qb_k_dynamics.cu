@@ -9,6 +9,10 @@
 #include "qb_dynamics.cuh"
 #include "qb_internal.h"
 
+#ifndef QB_DYN_MINB
+#define QB_DYN_MINB 8  // single-step kernel: min resident 128-thread blocks/SM (register cap)
+#endif
+
 namespace {
 
 template <class S> struct Vec4Load;
@@ -48,10 +52,10 @@ template <class R, class S> __device__ __forceinline__ void store4(S *p, const R
 // step (T == 0) or horizon rollout (T > 0: state = tape block 0, actions_seq
 // (T,n,4), block t+1 written after step t).
 template <class R, int KIND>
-__global__ void __launch_bounds__(128, 8) k_dyn_step(DynConsts<R> C, long long n, long long ld,
-                                                  typename storage_of<R>::type *state,
-                                                  const typename storage_of<R>::type *action,
-                                                  typename storage_of<R>::type *rotor_out, uint8_t *nonfinite, int T) {
+__device__ __forceinline__ void dyn_body(const DynConsts<R> &C, long long n, long long ld,
+                                         typename storage_of<R>::type *state,
+                                         const typename storage_of<R>::type *action,
+                                         typename storage_of<R>::type *rotor_out, uint8_t *nonfinite, int T) {
     using S = typename storage_of<R>::type;
     long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -73,6 +77,24 @@ __global__ void __launch_bounds__(128, 8) k_dyn_step(DynConsts<R> C, long long n
         for (int k = 0; k < 17; ++k) dst[k * ld + i] = to_store(x[k]);
     }
     if (nonfinite) nonfinite[i] = ok_all ? 0 : 1;
+}
+
+// one step over many envs: HBM-bound design point -> cap registers for 8 blocks/SM
+template <class R, int KIND>
+__global__ void __launch_bounds__(128, QB_DYN_MINB) k_dyn_step(DynConsts<R> C, long long n, long long ld,
+                                                     typename storage_of<R>::type *state,
+                                                     const typename storage_of<R>::type *action,
+                                                     typename storage_of<R>::type *rotor_out, uint8_t *nonfinite, int T) {
+    dyn_body<R, KIND>(C, n, ld, state, action, rotor_out, nonfinite, T);
+}
+
+// horizon rollout: few envs, long per-thread loop -> no register cap (no spills)
+template <class R, int KIND>
+__global__ void __launch_bounds__(128) k_rollout_fwd(DynConsts<R> C, long long n, long long ld,
+                                                     typename storage_of<R>::type *state,
+                                                     const typename storage_of<R>::type *action,
+                                                     typename storage_of<R>::type *rotor_out, uint8_t *nonfinite, int T) {
+    dyn_body<R, KIND>(C, n, ld, state, action, rotor_out, nonfinite, T);
 }
 
 template <class R, int KIND>
@@ -102,14 +124,18 @@ int dispatch_step(const qb_params *p, int kind, long long n, long long ld, void 
     auto *x = static_cast<S *>(state);
     auto *a = static_cast<const S *>(action);
     auto *o = static_cast<S *>(rotor_out);
+#define QB_LAUNCH(K)                                                                       \
+    (T > 0 ? (k_rollout_fwd<R, K><<<g, B, 0, st>>>(C, n, ld, x, a, o, nonfinite, T), 0)   \
+           : (k_dyn_step<R, K><<<g, B, 0, st>>>(C, n, ld, x, a, o, nonfinite, T), 0))
     switch (kind) {
-        case QB_CMD_SRT: k_dyn_step<R, QB_CMD_SRT><<<g, B, 0, st>>>(C, n, ld, x, a, o, nonfinite, T); break;
-        case QB_CMD_CTBR: k_dyn_step<R, QB_CMD_CTBR><<<g, B, 0, st>>>(C, n, ld, x, a, o, nonfinite, T); break;
-        case QB_CMD_PS: k_dyn_step<R, QB_CMD_PS><<<g, B, 0, st>>>(C, n, ld, x, a, o, nonfinite, T); break;
-        case QB_CMD_LV: k_dyn_step<R, QB_CMD_LV><<<g, B, 0, st>>>(C, n, ld, x, a, o, nonfinite, T); break;
-        case QB_CMD_ROTOR: k_dyn_step<R, QB_CMD_ROTOR><<<g, B, 0, st>>>(C, n, ld, x, a, o, nonfinite, T); break;
+        case QB_CMD_SRT: QB_LAUNCH(QB_CMD_SRT); break;
+        case QB_CMD_CTBR: QB_LAUNCH(QB_CMD_CTBR); break;
+        case QB_CMD_PS: QB_LAUNCH(QB_CMD_PS); break;
+        case QB_CMD_LV: QB_LAUNCH(QB_CMD_LV); break;
+        case QB_CMD_ROTOR: QB_LAUNCH(QB_CMD_ROTOR); break;
         default: qb::set_error("unknown command kind %d", kind); return QB_EINVAL;
     }
+#undef QB_LAUNCH
     return qb::check_launch("dynamics_step");
 }
 

@@ -19,9 +19,21 @@
 // FP64 validation kernel: one thread per pixel, the reference's exact
 // operation order (qb_real.cuh xd), bit-identical to render_batch except
 // where traversal-order-dependent pruning could matter at the last ulp.
+#include <algorithm>
+
 #include "qb_dynamics.cuh"
 #include "qb_geometry.cuh"
 #include "qb_internal.h"
+
+// BVH packet kernel: one camera per warp, QB_RF_BLOCK/32 warps per block and
+// one block per QB_RF_BLOCK/32 cameras, so the hardware block scheduler
+// balances the very uneven per-camera traversal cost; QB_RF_MINB caps registers
+#ifndef QB_RF_BLOCK
+#define QB_RF_BLOCK 64
+#endif
+#ifndef QB_RF_MINB
+#define QB_RF_MINB 16
+#endif
 
 namespace {
 
@@ -60,11 +72,11 @@ __device__ __forceinline__ void camera_pose(const R *p, const R *q, const R *cro
 }
 
 template <bool FROM_STATE>
-__global__ void __launch_bounds__(256, 4) k_render_f(DevScene S, CamF cam, long long n, long long ld, const float *state,
+__global__ void __launch_bounds__(QB_RF_BLOCK, QB_RF_MINB) k_render_f(DevScene S, CamF cam, long long n, long long ld, const float *state,
                                                      const float *origins, const float *rotations, const int32_t *env_scene,
                                                      float *depth, int32_t *seg, int centroid_id, float *centroid,
                                                      const float *extra, const int32_t *extra_ids, int n_extra) {
-    __shared__ int stk_s[8][64];
+    __shared__ int stk_s[QB_RF_BLOCK / 32][64];
     int *stk = stk_s[threadIdx.x >> 5];
     const int lane = threadIdx.x & 31;
     const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -276,7 +288,7 @@ template <bool FROM_STATE>
 __global__ void __launch_bounds__(CULL_WARPS * 32, 6)
     k_render_cull(DevScene S, CamF cam, long long n, long long ld, const float *state, const float *origins,
                   const float *rotations, const int32_t *env_scene, float *depth, int32_t *seg, int centroid_id,
-                  float *centroid, const float *extra, const int32_t *extra_ids, int n_extra) {
+                  float *centroid, const float *extra, const int32_t *extra_ids, int n_extra, int split) {
     __shared__ int cand_s[CULL_WARPS][CULL_MAX];
     __shared__ float4 rec_s[CULL_WARPS][CREC][4];      // shading records (warp-broadcast reads)
     __shared__ int2 met_s[CULL_WARPS][CREC];           // (record type, object id)
@@ -294,7 +306,10 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, 6)
     const int tiles_x = (W + TILE_W - 1) / TILE_W, tiles_y = (H + TILE_H - 1) / TILE_H;
     const float tmin = 1e-9f;
 
-    for (long long c = warp; c < n; c += nwarps) {
+    // small batches: `split` warps share one camera, each taking every split-th tile
+    for (long long wi = warp; wi < n * split; wi += nwarps) {
+        const long long c = wi / split;
+        const int part = (int)(wi % split);
         float o[3], Rw[9];
         if (FROM_STATE) {
             float p[3] = {state[0 * ld + c], state[1 * ld + c], state[2 * ld + c]};
@@ -390,8 +405,8 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, 6)
         // candidate test runs two independent rays (ILP)
         constexpr int TH2 = 2 * TILE_H;
         const int tiles_y2 = (H + TH2 - 1) / TH2;
-        for (int ty = 0, i0 = 0; ty < tiles_y2; ++ty, i0 += TH2)
-        for (int tx = 0, j0 = 0; tx < tiles_x; ++tx, j0 += TILE_W) {
+        for (int tl = part; tl < tiles_y2 * tiles_x; tl += split) {
+            const int i0 = (tl / tiles_x) * TH2, j0 = (tl % tiles_x) * TILE_W;
             const int j = j0 + (lane & 7);
             int ii[2] = {i0 + (lane >> 3), i0 + TILE_H + (lane >> 3)};
             // tile planes in CAMERA space through the pixel-centre rays of its border pixels
@@ -538,7 +553,7 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, 6)
                 }
             }
         }
-        if (centroid_id > 0) {
+        if (centroid_id > 0 && split == 1) {
 #pragma unroll
             for (int s2 = 16; s2 > 0; s2 >>= 1) {
                 cnt += __shfl_xor_sync(FULL, cnt, s2);
@@ -667,24 +682,32 @@ int launch_render(const qb_scene *s, const qb_camera *cam, int dtype, long long 
                 return QB_EINVAL;
             }
             const int B = CULL_WARPS * 32;
-            long long blocks = (n + CULL_WARPS - 1) / CULL_WARPS;
+            // fill the machine: ~24 resident warps per SM; small batches split a
+            // camera's tiles across warps (the per-camera culling is repeated)
+            const long long want = (long long)sm_count() * 24;
+            const int tiles = ((c.H + 2 * TILE_H - 1) / (2 * TILE_H)) * ((c.W + TILE_W - 1) / TILE_W);
+            int split = (int)std::min<long long>(tiles / 2 > 0 ? tiles / 2 : 1, std::max<long long>(1, want / std::max(n, 1LL)));
+            if (split < 1) split = 1;
+            if (split > 1 && !seg && centroid_id > 0) split = 1;  // centroid pass reads seg
+            long long blocks = (n * split + CULL_WARPS - 1) / CULL_WARPS;
             long long max_blocks = (long long)sm_count() * 16;
             if (blocks > max_blocks) blocks = max_blocks;
             if (state)
                 k_render_cull<true><<<(int)blocks, B, 0, st>>>(s->dev, c, n, ld, (const float *)state, nullptr, nullptr,
                                                                env_scene, (float *)depth, seg, centroid_id, centroid, extra,
-                                                               extra_ids, n_extra);
+                                                               extra_ids, n_extra, split);
             else
                 k_render_cull<false><<<(int)blocks, B, 0, st>>>(s->dev, c, n, ld, nullptr, (const float *)origins,
                                                                 (const float *)rotations, env_scene, (float *)depth, seg, 0,
-                                                                nullptr, nullptr, nullptr, 0);
-            return check_launch("render_cull_f32");
+                                                                nullptr, nullptr, nullptr, 0, split);
+            int rc = check_launch("render_cull_f32");
+            if (rc || split == 1 || centroid_id <= 0) return rc;
+            k_centroid<<<env_grid(n, 128), 128, 0, st>>>(n, c.W, c.H, seg, centroid_id, centroid);
+            return check_launch("centroid");
         }
-        const int B = 256;
-        long long warps_needed = n;
-        long long max_blocks = (long long)sm_count() * 8;  // 8 blocks x 8 warps resident per SM
-        long long blocks = (warps_needed * 32 + B - 1) / B;
-        if (blocks > max_blocks) blocks = max_blocks;
+        const int B = QB_RF_BLOCK;
+        long long blocks = (n * 32 + B - 1) / B;
+        if (blocks > 0x7fffffffLL) blocks = 0x7fffffffLL;  // grid-stride loop covers the rest
         if (state)
             k_render_f<true><<<(int)blocks, B, 0, st>>>(s->dev, c, n, ld, (const float *)state, nullptr, nullptr, env_scene,
                                                         (float *)depth, seg, centroid_id, centroid, extra, extra_ids, n_extra);

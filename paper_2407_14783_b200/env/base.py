@@ -377,25 +377,35 @@ class QuadEnvBase:
         return self._planes[0:13, i].double().cpu().numpy()
 
     # ------------------------------------------------------------------ graph capture
-    def make_step_graph(self, action_tensor, steps: int = 1):
-        """Capture `steps` env steps (K1+K3 and K2) into a CUDA graph reading
-        `action_tensor` ((N,4), device).  Returns a callable replaying it:
-        for latency-bound small batches (config 1/2, N=100)."""
+    def make_step_graph(self, actions):
+        """Capture env steps (K1+K3 and K2) into one CUDA graph.
+
+        `actions`: a device tensor (N,4) -- one step per replay -- or (K,N,4):
+        K consecutive steps, step k reading actions[k].  Returns a callable that
+        replays the graph; refill `actions` in place between replays.  For
+        latency-bound small batches (configs 1/2, N=100) this removes the
+        per-step host launch overhead."""
         import torch
 
-        a = action_tensor
-        self._bufs.action = a.data_ptr()
+        seq = actions if actions.dim() == 3 else actions.unsqueeze(0)
+        if seq.shape[1:] != (self.num_agents, 4) or not seq.is_cuda or seq.dtype != self.dtype:
+            raise ActionShapeMismatch(f"graph actions must be a ({self.num_agents},4) or (K,{self.num_agents},4) "
+                                      f"{self.dtype} CUDA tensor")
         stream = torch.cuda.Stream(device=self.device)
         stream.wait_stream(torch.cuda.current_stream(self.device))
         g = torch.cuda.CUDAGraph()
         with torch.cuda.stream(stream):
             for _ in range(2):  # warm-up on the capture stream
-                self._launch_step()
+                for k in range(seq.shape[0]):
+                    self._bufs.action = seq[k].data_ptr()
+                    self._launch_step()
             torch.cuda.current_stream().synchronize()
             with torch.cuda.graph(g, stream=stream):
-                for _ in range(steps):
+                for k in range(seq.shape[0]):
+                    self._bufs.action = seq[k].data_ptr()
                     self._launch_step()
         torch.cuda.current_stream(self.device).wait_stream(stream)
+        self._graph_keepalive = seq
         return g.replay
 
     def _launch_step(self):

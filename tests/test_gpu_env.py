@@ -153,6 +153,13 @@ def test_fp32_stepwise_parity(case):
                 else:
                     bad = img.cpu().numpy() != i0
                 n_graz += graz.sum(); n_bad += bad.sum(); n_pix += bad.size
+                if case == "landing" and sensor.kind == "segmentation":  # pad centroid (tasks.py:121-128)
+                    tgt = res.observations["target"].cpu().numpy()
+                    for a in range(env.num_agents):
+                        rows, cols = np.nonzero(i0[a] == 9)
+                        ref = np.array([cols.mean(), rows.mean()]) if len(rows) else np.array([-1.0, -1.0])
+                        if not bad[a].any():
+                            assert np.array_equal(tgt[a], ref.astype(np.float32)), (t, a, tgt[a], ref)
                 if (bad & ~graz).any():
                     a, i, j = np.argwhere(bad & ~graz)[0]
                     gi = img[a, i, j].item()

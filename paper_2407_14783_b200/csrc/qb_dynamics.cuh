@@ -19,6 +19,8 @@ template <class R> struct DynConsts {
     R arms[4][3];
     R k2, k1, k0, k1sq, four_k2, two_k2, inv_two_k2, neg_k1;
     R neg_drag[3];  // -0.5*rho*Cd*s
+    R ndm[3];       // neg_drag / mass                 (FP32 RHS folding)
+    R cJ[3];        // (J[a+2] - J[a+1]) / J[a]: (w x Jw)_a / J_a = cJ[a] w_{a+1} w_{a+2}
     R rlo, rhi;
     R minv[4][4];
     R flo, fhi, flo4, fhi4;
@@ -41,6 +43,8 @@ template <class R> inline DynConsts<R> make_consts(const qb_params &p) {
         c.invJ[a] = F(1.0 / p.inertia[a]);
         c.g[a] = F(p.gravity[a]);
         c.neg_drag[a] = F(-p.drag_c[a]);
+        c.ndm[a] = F(-p.drag_c[a] / p.mass);
+        c.cJ[a] = F((p.inertia[(a + 2) % 3] - p.inertia[(a + 1) % 3]) / p.inertia[a]);
         c.rate_p[a] = F(p.rate_p[a]);
         c.neg_att_p[a] = F(-p.attitude_p[a]);
         c.vel_p[a] = F(p.vel_p[a]);
@@ -123,15 +127,26 @@ template <class R> struct Wrench {
     R f[4];
     R fsum;
     R tq[3];
+    R fsum_m, tqJ[3];  // FP32 path: fsum / mass, tq / J
 };
 
 template <class R> QB_D void make_wrench(const DynConsts<R> &C, const R *w, Wrench<R> &W) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) W.f[i] = C.k2 * (w[i] * w[i]) + C.k1 * w[i] + C.k0;  // dynamics.py:103-106
+    for (int i = 0; i < 4; ++i) {  // dynamics.py:103-106
+        if constexpr (is_exact<R>::value)
+            W.f[i] = C.k2 * (w[i] * w[i]) + C.k1 * w[i] + C.k0;
+        else  // Horner: two FMAs
+            W.f[i] = (C.k2 * w[i] + C.k1) * w[i] + C.k0;
+    }
     W.fsum = W.f[0] + W.f[1] + W.f[2] + W.f[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a)  // dynamics.py:192-194
         W.tq[a] = W.f[0] * C.arms[0][a] + W.f[1] * C.arms[1][a] + W.f[2] * C.arms[2][a] + W.f[3] * C.arms[3][a];
+    if constexpr (!is_exact<R>::value) {
+        W.fsum_m = W.fsum * C.inv_mass;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) W.tqJ[a] = W.tq[a] * C.invJ[a];
+    }
 }
 
 // dynamics.py:154-200: 13 rigid rates at y = (p, v, q, omega)
@@ -151,12 +166,13 @@ template <class R> QB_D void ode_rhs(const DynConsts<R> &C, const R *y, const Wr
         bx = m[0][0] * v[0] + m[1][0] * v[1] + m[2][0] * v[2];
         by = m[0][1] * v[0] + m[1][1] * v[1] + m[2][1] * v[2];
         bz = m[0][2] * v[0] + m[1][2] * v[1] + m[2][2] * v[2];
-        fx = C.neg_drag[0] * bx * r_abs(bx);
-        fy = C.neg_drag[1] * by * r_abs(by);
-        fz = C.neg_drag[2] * bz * r_abs(bz) + W.fsum;
-        ax = m[0][0] * fx + m[0][1] * fy + m[0][2] * fz;
-        ay = m[1][0] * fx + m[1][1] * fy + m[1][2] * fz;
-        az = m[2][0] * fx + m[2][1] * fy + m[2][2] * fz;
+        // body force / mass (drag coefficients and thrust pre-divided by m)
+        fx = C.ndm[0] * bx * r_abs(bx);
+        fy = C.ndm[1] * by * r_abs(by);
+        fz = C.ndm[2] * bz * r_abs(bz) + W.fsum_m;
+        ax = C.g[0] + m[0][0] * fx + m[0][1] * fy + m[0][2] * fz;
+        ay = C.g[1] + m[1][0] * fx + m[1][1] * fy + m[1][2] * fz;
+        az = C.g[2] + m[2][0] * fx + m[2][1] * fy + m[2][2] * fz;
     }
     dy[0] = v[0]; dy[1] = v[1]; dy[2] = v[2];
     if constexpr (is_exact<R>::value) {
@@ -164,27 +180,44 @@ template <class R> QB_D void ode_rhs(const DynConsts<R> &C, const R *y, const Wr
         dy[4] = ay / C.mass + C.g[1];
         dy[5] = az / C.mass + C.g[2];
     } else {
-        dy[3] = ax * C.inv_mass + C.g[0];
-        dy[4] = ay * C.inv_mass + C.g[1];
-        dy[5] = az * C.inv_mass + C.g[2];
+        dy[3] = ax;
+        dy[4] = ay;
+        dy[5] = az;
     }
     R qw = q[0], qx = q[1], qy = q[2], qz = q[3], ox = o[0], oy = o[1], oz = o[2];
     dy[6] = R(0.5) * (-qx * ox - qy * oy - qz * oz);
     dy[7] = R(0.5) * (qw * ox + qy * oz - qz * oy);
     dy[8] = R(0.5) * (qw * oy - qx * oz + qz * ox);
     dy[9] = R(0.5) * (qw * oz + qx * oy - qy * ox);
-    R cx = oy * (C.J[2] * oz) - oz * (C.J[1] * oy);
-    R cy = oz * (C.J[0] * ox) - ox * (C.J[2] * oz);
-    R cz = ox * (C.J[1] * oy) - oy * (C.J[0] * ox);
     if constexpr (is_exact<R>::value) {
+        R cx = oy * (C.J[2] * oz) - oz * (C.J[1] * oy);
+        R cy = oz * (C.J[0] * ox) - ox * (C.J[2] * oz);
+        R cz = ox * (C.J[1] * oy) - oy * (C.J[0] * ox);
         dy[10] = (W.tq[0] - cx) / C.J[0];
         dy[11] = (W.tq[1] - cy) / C.J[1];
         dy[12] = (W.tq[2] - cz) / C.J[2];
-    } else {
-        dy[10] = (W.tq[0] - cx) * C.invJ[0];
-        dy[11] = (W.tq[1] - cy) * C.invJ[1];
-        dy[12] = (W.tq[2] - cz) * C.invJ[2];
+    } else {  // diagonal J: (w x Jw)_x / Jx = (Jz - Jy)/Jx * wy wz, two ops per axis
+        dy[10] = W.tqJ[0] - C.cJ[0] * (oy * oz);
+        dy[11] = W.tqJ[1] - C.cJ[1] * (oz * ox);
+        dy[12] = W.tqJ[2] - C.cJ[2] * (ox * oy);
     }
+}
+
+// dynamics.py:203-228: raw substep in place (no renormalisation)
+// out = y + c * k over the 13 rigid states; FP32: packed FFMA2 on component
+// pairs (same per-lane rounding as the scalar FFMA, half the instructions)
+template <class R, class K> QB_D void axpy13(R *out, const R *y, K c, const R *k) {
+#pragma unroll
+    for (int i = 0; i < 13; ++i) out[i] = y[i] + c * k[i];
+}
+QB_D void axpy13(float *out, const float *y, float c, const float *k) {
+#pragma unroll
+    for (int i = 0; i < 12; i += 2) {
+        const float2 r = __ffma2_rn(make_float2(k[i], k[i + 1]), make_float2(c, c), make_float2(y[i], y[i + 1]));
+        out[i] = r.x;
+        out[i + 1] = r.y;
+    }
+    out[12] = fmaf(c, k[12], y[12]);
 }
 
 // dynamics.py:203-228: raw substep in place (no renormalisation)
@@ -192,32 +225,24 @@ template <class R> QB_D void integrate_substep(const DynConsts<R> &C, R *y, cons
     if (C.integrator == QB_EULER) {
         R d[13];
         ode_rhs(C, y, W, d);
-#pragma unroll
-        for (int i = 0; i < 13; ++i) y[i] = y[i] + C.h * d[i];
+        axpy13(y, y, C.h, d);
         return;
     }
     R k[13], acc[13], t[13];
     ode_rhs(C, y, W, k);  // k1
 #pragma unroll
-    for (int i = 0; i < 13; ++i) {
-        acc[i] = k[i];
-        t[i] = y[i] + C.half_h * k[i];
-    }
+    for (int i = 0; i < 13; ++i) acc[i] = k[i];
+    axpy13(t, y, C.half_h, k);
     ode_rhs(C, t, W, k);  // k2
-#pragma unroll
-    for (int i = 0; i < 13; ++i) {
-        acc[i] = acc[i] + R(2.0) * k[i];
-        t[i] = y[i] + C.half_h * k[i];
-    }
+    axpy13(acc, acc, R(2.0), k);
+    axpy13(t, y, C.half_h, k);
     ode_rhs(C, t, W, k);  // k3
-#pragma unroll
-    for (int i = 0; i < 13; ++i) {
-        acc[i] = acc[i] + R(2.0) * k[i];
-        t[i] = y[i] + C.h * k[i];
-    }
+    axpy13(acc, acc, R(2.0), k);
+    axpy13(t, y, C.h, k);
     ode_rhs(C, t, W, k);  // k4
 #pragma unroll
-    for (int i = 0; i < 13; ++i) y[i] = y[i] + C.sixth_h * (acc[i] + k[i]);
+    for (int i = 0; i < 13; ++i) acc[i] = acc[i] + k[i];
+    axpy13(y, y, C.sixth_h, acc);
 }
 
 // dynamics.py:231-253 for one env. x = 17-state, cmd = desired rotor speeds.

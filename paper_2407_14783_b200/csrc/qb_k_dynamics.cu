@@ -10,7 +10,7 @@
 #include "qb_internal.h"
 
 #ifndef QB_DYN_MINB
-#define QB_DYN_MINB 8  // single-step kernel: min resident 128-thread blocks/SM (register cap)
+#define QB_DYN_MINB 6  // single-step kernel: min resident 128-thread blocks/SM (register cap, no spills)
 #endif
 
 namespace {
@@ -79,7 +79,9 @@ __device__ __forceinline__ void dyn_body(const DynConsts<R> &C, long long n, lon
     if (nonfinite) nonfinite[i] = ok_all ? 0 : 1;
 }
 
-// one step over many envs: HBM-bound design point -> cap registers for 8 blocks/SM
+// one step over many envs: HBM-bound design point -> cap registers for 6 blocks/SM
+// (measured: 6 beats 8 (spills) and 5; an env-pair FFMA2 variant needed 158
+// registers and lost on occupancy)
 template <class R, int KIND>
 __global__ void __launch_bounds__(128, QB_DYN_MINB) k_dyn_step(DynConsts<R> C, long long n, long long ld,
                                                      typename storage_of<R>::type *state,

@@ -32,7 +32,7 @@
 #define QB_RF_BLOCK 64
 #endif
 #ifndef QB_RF_MINB
-#define QB_RF_MINB 16
+#define QB_RF_MINB 24
 #endif
 
 namespace {

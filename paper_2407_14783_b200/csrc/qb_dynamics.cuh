@@ -96,6 +96,15 @@ QB_D void q_rot(const R *q, R vx, R vy, R vz, R &ox, R &oy, R &oz) {
 // quatmath.py:75-81
 template <class R> QB_D void q_matrix(const R *q, R m[3][3]) {
     R w = q[0], x = q[1], y = q[2], z = q[3];
+    if constexpr (!is_exact<R>::value) {  // FP32: pre-doubled products, 24 ops
+        const R x2 = x + x, y2 = y + y, z2 = z + z;
+        const R xx = x * x2, yy = y * y2, zz = z * z2, xy = x * y2, xz = x * z2, yz = y * z2;
+        const R wx = w * x2, wy = w * y2, wz = w * z2;
+        m[0][0] = R(1.0) - (yy + zz); m[0][1] = xy - wz; m[0][2] = xz + wy;
+        m[1][0] = xy + wz; m[1][1] = R(1.0) - (xx + zz); m[1][2] = yz - wx;
+        m[2][0] = xz - wy; m[2][1] = yz + wx; m[2][2] = R(1.0) - (xx + yy);
+        return;
+    }
     m[0][0] = R(1.0) - R(2.0) * (y * y + z * z);
     m[0][1] = R(2.0) * (x * y - w * z);
     m[0][2] = R(2.0) * (x * z + w * y);
@@ -247,7 +256,8 @@ template <class R> QB_D void integrate_substep(const DynConsts<R> &C, R *y, cons
 
 // dynamics.py:231-253 for one env. x = 17-state, cmd = desired rotor speeds.
 // Returns false when any component is non-finite (NonFiniteState mask).
-template <class R> QB_D bool dyn_step(const DynConsts<R> &C, R *x, const R *cmd_in) {
+// SUB > 0: substep count known at compile time (loop unrolled; must equal C.substeps)
+template <class R, int SUB = 0> QB_D bool dyn_step(const DynConsts<R> &C, R *x, const R *cmd_in) {
     R cmd[4];
     bool cmd_ok = true;  // FP32 clamps drop NaN: keep the reference's verdict (NaN command -> non-finite state)
 #pragma unroll
@@ -255,7 +265,9 @@ template <class R> QB_D bool dyn_step(const DynConsts<R> &C, R *x, const R *cmd_
         cmd_ok &= !r_isnan(cmd_in[i]);
         cmd[i] = p_clip(cmd_in[i], C.rlo, C.rhi);
     }
-    for (int s = 0; s < C.substeps; ++s) {
+    const int nsub = SUB > 0 ? SUB : C.substeps;
+#pragma unroll
+    for (int s = 0; s < nsub; ++s) {
         R w[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) w[i] = p_clip(cmd[i] + (x[13 + i] - cmd[i]) * C.alpha, C.rlo, C.rhi);  // :109-114

@@ -6,6 +6,8 @@
 // 16 B vector per env: 152 B/env-step in FP32 (K1 roofline).
 // Everything else stays in registers; for a horizon rollout the state never
 // leaves registers between steps and only the tape is written.
+#include <type_traits>
+
 #include "qb_dynamics.cuh"
 #include "qb_internal.h"
 
@@ -51,7 +53,7 @@ template <class R, class S> __device__ __forceinline__ void store4(S *p, const R
 
 // step (T == 0) or horizon rollout (T > 0: state = tape block 0, actions_seq
 // (T,n,4), block t+1 written after step t).
-template <class R, int KIND>
+template <class R, int KIND, int SUB = 0>
 __device__ __forceinline__ void dyn_body(const DynConsts<R> &C, long long n, long long ld,
                                          typename storage_of<R>::type *state,
                                          const typename storage_of<R>::type *action,
@@ -69,7 +71,7 @@ __device__ __forceinline__ void dyn_body(const DynConsts<R> &C, long long n, lon
         load4<R, S>(action + ((long long)t * n + i) * 4, a);
         command_to_speeds<R, KIND>(C, x, a, cmd);
         if (rotor_out && T == 0) store4<R, S>(rotor_out + i * 4, cmd);
-        ok_all &= dyn_step(C, x, cmd);
+        ok_all &= dyn_step<R, SUB>(C, x, cmd);
         // a NaN action propagates to a NaN state in the reference (np.clip keeps NaN)
         ok_all &= !(r_isnan(a[0]) || r_isnan(a[1]) || r_isnan(a[2]) || r_isnan(a[3]));
         S *dst = T > 0 ? state + (long long)(t + 1) * 17 * ld : state;
@@ -82,12 +84,13 @@ __device__ __forceinline__ void dyn_body(const DynConsts<R> &C, long long n, lon
 // one step over many envs: HBM-bound design point -> cap registers for 6 blocks/SM
 // (measured: 6 beats 8 (spills) and 5; an env-pair FFMA2 variant needed 158
 // registers and lost on occupancy)
-template <class R, int KIND>
+// SUB = 2 (the default SimConfig) unrolls the substep loop at compile time.
+template <class R, int KIND, int SUB>
 __global__ void __launch_bounds__(128, QB_DYN_MINB) k_dyn_step(DynConsts<R> C, long long n, long long ld,
                                                      typename storage_of<R>::type *state,
                                                      const typename storage_of<R>::type *action,
                                                      typename storage_of<R>::type *rotor_out, uint8_t *nonfinite, int T) {
-    dyn_body<R, KIND>(C, n, ld, state, action, rotor_out, nonfinite, T);
+    dyn_body<R, KIND, SUB>(C, n, ld, state, action, rotor_out, nonfinite, T);
 }
 
 // horizon rollout: few envs, long per-thread loop -> no register cap (no spills)
@@ -116,6 +119,23 @@ __global__ void __launch_bounds__(128) k_command(DynConsts<R> C, long long n, lo
     store4<R, S>(out + i * 4, cmd);
 }
 
+template <class R, int KIND>
+void launch_step(const DynConsts<R> &C, dim3 g, int B, cudaStream_t st, long long n, long long ld,
+                 typename storage_of<R>::type *x, const typename storage_of<R>::type *a,
+                 typename storage_of<R>::type *o, uint8_t *nonfinite, int T) {
+    if (T > 0) {
+        k_rollout_fwd<R, KIND><<<g, B, 0, st>>>(C, n, ld, x, a, o, nonfinite, T);
+        return;
+    }
+    if constexpr (std::is_same<R, float>::value) {
+        if (C.substeps == 2) {
+            k_dyn_step<R, KIND, 2><<<g, B, 0, st>>>(C, n, ld, x, a, o, nonfinite, T);
+            return;
+        }
+    }
+    k_dyn_step<R, KIND, 0><<<g, B, 0, st>>>(C, n, ld, x, a, o, nonfinite, T);
+}
+
 template <class R>
 int dispatch_step(const qb_params *p, int kind, long long n, long long ld, void *state, const void *action,
                   void *rotor_out, uint8_t *nonfinite, int T, cudaStream_t st) {
@@ -126,9 +146,7 @@ int dispatch_step(const qb_params *p, int kind, long long n, long long ld, void 
     auto *x = static_cast<S *>(state);
     auto *a = static_cast<const S *>(action);
     auto *o = static_cast<S *>(rotor_out);
-#define QB_LAUNCH(K)                                                                       \
-    (T > 0 ? (k_rollout_fwd<R, K><<<g, B, 0, st>>>(C, n, ld, x, a, o, nonfinite, T), 0)   \
-           : (k_dyn_step<R, K><<<g, B, 0, st>>>(C, n, ld, x, a, o, nonfinite, T), 0))
+#define QB_LAUNCH(K) launch_step<R, K>(C, g, B, st, n, ld, x, a, o, nonfinite, T)
     switch (kind) {
         case QB_CMD_SRT: QB_LAUNCH(QB_CMD_SRT); break;
         case QB_CMD_CTBR: QB_LAUNCH(QB_CMD_CTBR); break;

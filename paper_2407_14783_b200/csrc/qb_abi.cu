@@ -197,6 +197,7 @@ static float f_up(double v) {
     return f;
 }
 
+
 static float4 f4(float x, float y, float z, float w) { return make_float4(x, y, z, w); }
 
 // conservative culling bounds of one primitive (see DevScene::primc)

@@ -242,6 +242,14 @@ template <class R> QB_D R ray_triangle_ref(const R *d, R ox, R oy, R oz, R dx, R
 //   box      : [cx cy cz hx] [hy hz r00 r01] [r02 r10 r11 r12] [r20 r21 r22 0]
 //   triangle : [ax ay az e1x] [e1y e1z e2x e2y] [e2z 0 0 0]
 
+// 1/x from MUFU.RCP (~1 ulp): ray-setup reciprocals for slab tests against
+// outward-rounded boxes, no IEEE-division slow path (no call, no stack frame)
+QB_D float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
 QB_D float ray_sphere_f(const float4 *p, float ox, float oy, float oz, float dx, float dy, float dz, float tmin, float tmax) {
     float4 a = __ldg(p), b = __ldg(p + 1);
     float mx = ox - a.x, my = oy - a.y, mz = oz - a.z;
@@ -269,7 +277,7 @@ QB_D float ray_box_f(const float4 *p, float ox, float oy, float oz, float dx, fl
     float ldy = b.w * dx + c.z * dy + e.y * dz;
     float ldz = c.x * dx + c.w * dy + e.z * dz;
     float hx = a.w, hy = b.x, hz = b.y;
-    float ix = 1.0f / ldx, iy = 1.0f / ldy, iz = 1.0f / ldz;
+    float ix = rcp_approx(ldx), iy = rcp_approx(ldy), iz = rcp_approx(ldz);
     // slabs; a zero direction gives +-inf (or NaN at the slab plane, which
     // fminf/fmaxf ignore -- the reference's `o outside -> miss` is the inf case)
     float tax = (-hx - lox) * ix, tbx = (hx - lox) * ix;
@@ -290,14 +298,17 @@ QB_D float ray_triangle_f(const float4 *p, float ox, float oy, float oz, float d
     float px = dy * e2z - dz * e2y, py = dz * e2x - dx * e2z, pz = dx * e2y - dy * e2x;
     float det = e1x * px + e1y * py + e1z * pz;
     if (det == 0.0f) return -1.0f;
-    float inv = 1.0f / det;
+    // Moeller-Trumbore with the barycentric tests on the numerators scaled by
+    // sign(det) (u = U/det in [0,1] <=> U*sgn in [0,|det|]): the division is
+    // paid only by the rays that pass both edge tests
+    const float adet = fabsf(det);
     float tx = ox - ax, ty = oy - ay, tz = oz - az;
-    float u = (tx * px + ty * py + tz * pz) * inv;
-    if (u < 0.0f || u > 1.0f) return -1.0f;
+    float U = copysignf(1.0f, det) * (tx * px + ty * py + tz * pz);
+    if (U < 0.0f || U > adet) return -1.0f;
     float qx = ty * e1z - tz * e1y, qy = tz * e1x - tx * e1z, qz = tx * e1y - ty * e1x;
-    float v = (dx * qx + dy * qy + dz * qz) * inv;
-    if (v < 0.0f || u + v > 1.0f) return -1.0f;
-    float t = (e2x * qx + e2y * qy + e2z * qz) * inv;
+    float V = copysignf(1.0f, det) * (dx * qx + dy * qy + dz * qz);
+    if (V < 0.0f || U + V > adet) return -1.0f;
+    float t = __fdividef(e2x * qx + e2y * qy + e2z * qz, det);
     if (t > tmin && t <= tmax) return t;
     return -1.0f;
 }

@@ -35,6 +35,13 @@
 #define QB_RF_MINB 24
 #endif
 
+#ifdef QB_RF_STATS
+__device__ unsigned long long g_rf_stats[4];  // tiles, node visits, prim tests, active lanes
+extern "C" int qb_debug_render_stats(unsigned long long *out) {
+    return (int)cudaMemcpyFromSymbol(out, g_rf_stats, sizeof(g_rf_stats));
+}
+#endif
+
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
@@ -76,14 +83,17 @@ __global__ void __launch_bounds__(QB_RF_BLOCK, QB_RF_MINB) k_render_f(DevScene S
                                                      const float *origins, const float *rotations, const int32_t *env_scene,
                                                      float *depth, int32_t *seg, int centroid_id, float *centroid,
                                                      const float *extra, const int32_t *extra_ids, int n_extra) {
-    __shared__ int stk_s[QB_RF_BLOCK / 32][64];
-    int *stk = stk_s[threadIdx.x >> 5];
+    __shared__ int4 stk_s[QB_RF_BLOCK / 32][64];
+    __shared__ float rw_s[QB_RF_BLOCK / 32][9];  // camera rotation (kept out of registers)
+    int4 *stk = stk_s[threadIdx.x >> 5];
+    float *Rs = rw_s[threadIdx.x >> 5];
     const int lane = threadIdx.x & 31;
     const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
     const int W = cam.W, H = cam.H;
     const int tiles_x = (W + TILE_W - 1) / TILE_W, tiles_y = (H + TILE_H - 1) / TILE_H;
     const float tmin = 1e-9f;
+    const float sx = 2.0f / W, sy = 2.0f / H;
 
     for (long long c = warp; c < n; c += nwarps) {
         float o[3], Rw[9];
@@ -99,42 +109,66 @@ __global__ void __launch_bounds__(QB_RF_BLOCK, QB_RF_MINB) k_render_f(DevScene S
         }
         const int scene = env_scene ? env_scene[c] : 0;
         const int root = S.root[scene];
-        long long cnt = 0, sum_col = 0, sum_row = 0;
+        int cnt = 0, sum_col = 0, sum_row = 0;
+        __syncwarp();
+        if (lane < 9) Rs[lane] = Rw[lane];  // (all lanes hold the same pose)
+        __syncwarp();
 
         for (int tile = 0; tile < tiles_x * tiles_y; ++tile) {
             const int j = (tile % tiles_x) * TILE_W + (lane & 7);
             const int i = (tile / tiles_x) * TILE_H + (lane >> 3);
             const bool valid = (j < W) && (i < H);
-            const float y = (2.0f * (i + 0.5f) / H - 1.0f) * cam.tv;
-            const float x = (2.0f * (j + 0.5f) / W - 1.0f) * cam.th;
+            const float y = ((i + 0.5f) * sy - 1.0f) * cam.tv;
+            const float x = ((j + 0.5f) * sx - 1.0f) * cam.th;
             const float n2 = x * x + y * y + 1.0f;
-            const float cz = rsqrtf(n2);
-            const float cx = x * cz, cy = y * cz;
-            const float dx = Rw[0] * cx + Rw[1] * cy + Rw[2] * cz;
-            const float dy = Rw[3] * cx + Rw[4] * cy + Rw[5] * cz;
-            const float dz = Rw[6] * cx + Rw[7] * cy + Rw[8] * cz;
-            const float ix = 1.0f / dx, iy = 1.0f / dy, iz = 1.0f / dz;
+            float dx, dy, dz, tmax;
+            {
+                const float cz = rsqrtf(n2);
+                const float cx = x * cz, cy = y * cz;
+                dx = Rs[0] * cx + Rs[1] * cy + Rs[2] * cz;
+                dy = Rs[3] * cx + Rs[4] * cy + Rs[5] * cz;
+                dz = Rs[6] * cx + Rs[7] * cy + Rs[8] * cz;
+                tmax = cam.max_range * (n2 * cz);  // max_range / cos(angle to the axis)
+            }
+            const float ix = rcp_approx(dx), iy = rcp_approx(dy), iz = rcp_approx(dz);
             const float oix = o[0] * ix, oiy = o[1] * iy, oiz = o[2] * iz;
-            const float tmax = cam.max_range * sqrtf(n2);
-            float best = tmax;
+            // lanes outside the image carry best = -1: they never want a box
+            float best = valid ? tmax : -1.0f;
             int bid = -1;
             bool hit = false;
+#ifdef QB_RF_STATS
+            unsigned st_visit = 0, st_prim = 0, st_active = __popc(__ballot_sync(FULL, valid));
+#endif
 
-            // warp-uniform traversal: one stack per warp in shared memory (lane 0
-            // pushes, all lanes read the broadcast); children are slab-tested at
-            // the parent by every lane and pushed only if some lane needs them,
-            // nearer child (lane majority) on top
+            // warp-uniform traversal with a per-warp shared-memory stack (lane 0
+            // pushes, all lanes read the broadcast).  The current node is carried
+            // as its (a, b) record taken from the parent's child fetch, so a
+            // visit costs one dependent load (the two child boxes, adjacent);
+            // both children are slab-tested by every lane, the nearer one (lane
+            // majority) is visited next and the other pushed with its
+            // warp-minimum entry distance (REDUX.MIN on the float bits, valid as
+            // entries are >= 0), so a pop needs no reload: it is skipped unless
+            // some lane's current hit still lies beyond that distance.
+            constexpr unsigned INF_BITS = 0x7f800000u;
             int sp = 0;
-            int node = root;
+            int ca, cb;
             {
-                const float4 lo = __ldg(S.nodef + 2 * node), hi = __ldg(S.nodef + 2 * node + 1);
-                if (!__any_sync(FULL, valid && slab_enter_fma(lo, hi, oix, oiy, oiz, ix, iy, iz, best) <= best)) node = -1;
+                const float4 lo = __ldg(S.nodef + 2 * root), hi = __ldg(S.nodef + 2 * root + 1);
+                ca = __float_as_int(lo.w);
+                cb = __float_as_int(hi.w);
+                if (!__any_sync(FULL, slab_enter_fma(lo, hi, oix, oiy, oiz, ix, iy, iz, best) <= best)) ca = -1;
             }
-            while (node >= 0) {
-                const float4 lo = __ldg(S.nodef + 2 * node), hi = __ldg(S.nodef + 2 * node + 1);
-                const int a = __float_as_int(lo.w), b = __float_as_int(hi.w);
-                if (b > 0) {
-                    for (int p = a; p < a + b; ++p) {
+            // (ca, cb): leaf {first, count > 0} or internal {left child, -axis <= 0}; ca < 0: done
+            while (ca >= 0) {
+#ifdef QB_RF_STATS
+                ++st_visit;
+#endif
+                bool descend = false;
+                if (cb > 0) {
+#ifdef QB_RF_STATS
+                    st_prim += cb;
+#endif
+                    for (int p = ca; p < ca + cb; ++p) {
                         const int2 m = __ldg(S.meta + p);
                         const float4 *pr = S.primf + 4 * p;
                         float t;
@@ -151,38 +185,53 @@ __global__ void __launch_bounds__(QB_RF_BLOCK, QB_RF_MINB) k_render_f(DevScene S
                         }
                     }
                 } else {
-                    const float4 llo = __ldg(S.nodef + 2 * a), lhi = __ldg(S.nodef + 2 * a + 1);
-                    const float4 rlo = __ldg(S.nodef + 2 * a + 2), rhi = __ldg(S.nodef + 2 * a + 3);
+                    const float4 llo = __ldg(S.nodef + 2 * ca), lhi = __ldg(S.nodef + 2 * ca + 1);
+                    const float4 rlo = __ldg(S.nodef + 2 * ca + 2), rhi = __ldg(S.nodef + 2 * ca + 3);
                     const float el = slab_enter_fma(llo, lhi, oix, oiy, oiz, ix, iy, iz, best);
                     const float er = slab_enter_fma(rlo, rhi, oix, oiy, oiz, ix, iy, iz, best);
-                    const bool hl = __any_sync(FULL, valid && el <= best);
-                    const bool hr = __any_sync(FULL, valid && er <= best);
+                    const bool wl = el <= best, wr = er <= best;
+                    const bool hl = __any_sync(FULL, wl);
+                    const bool hr = __any_sync(FULL, wr);
                     if (hl && hr) {
-                        const bool left_first = __popc(__ballot_sync(FULL, !valid || el <= er)) >= 16;
-                        const int near = left_first ? a : a + 1, far = left_first ? a + 1 : a;
-                        if (lane == 0) stk[sp] = far;
+                        const bool left_first = __popc(__ballot_sync(FULL, el <= er)) >= 16;
+                        const float4 nlo = left_first ? llo : rlo, nhi = left_first ? lhi : rhi;
+                        const float4 flo = left_first ? rlo : llo, fhi = left_first ? rhi : lhi;
+                        const float ef = left_first ? er : el;
+                        const bool wf = left_first ? wr : wl;
+                        const unsigned em = __reduce_min_sync(FULL, wf ? __float_as_uint(ef) : INF_BITS);
+                        if (lane == 0) stk[sp] = make_int4(__float_as_int(flo.w), __float_as_int(fhi.w), (int)em, 0);
                         ++sp;
-                        node = near;
-                        continue;
-                    }
-                    if (hl || hr) {
-                        node = hl ? a : a + 1;
-                        continue;
+                        ca = __float_as_int(nlo.w);
+                        cb = __float_as_int(nhi.w);
+                        descend = true;
+                    } else if (hl || hr) {
+                        ca = __float_as_int(hl ? llo.w : rlo.w);
+                        cb = __float_as_int(hl ? lhi.w : rhi.w);
+                        descend = true;
                     }
                 }
-                // pop the next node some lane still needs
-                node = -1;
+                if (descend) continue;
+                // pop the next node some lane may still need
+                ca = -1;
+                __syncwarp();
                 while (sp > 0) {
-                    __syncwarp();
-                    const int cand_node = stk[sp - 1];
-                    --sp;
-                    const float4 clo = __ldg(S.nodef + 2 * cand_node), chi = __ldg(S.nodef + 2 * cand_node + 1);
-                    if (__any_sync(FULL, valid && slab_enter_fma(clo, chi, oix, oiy, oiz, ix, iy, iz, best) <= best)) {
-                        node = cand_node;
+                    const int4 e = stk[--sp];
+                    if (__any_sync(FULL, __uint_as_float((unsigned)e.z) <= best)) {
+                        ca = e.x;
+                        cb = e.y;
                         break;
                     }
                 }
+                __syncwarp();
             }
+#ifdef QB_RF_STATS
+            if (lane == 0) {
+                atomicAdd(&g_rf_stats[0], 1ull);
+                atomicAdd(&g_rf_stats[1], (unsigned long long)st_visit);
+                atomicAdd(&g_rf_stats[2], (unsigned long long)st_prim);
+                atomicAdd(&g_rf_stats[3], (unsigned long long)st_active);
+            }
+#endif
             float t = hit ? best : -1.0f;
             int oid = hit ? bid : -1;
             if (n_extra > 0) {  // swarm agents as spheres (kernels.py:438-445)
@@ -199,7 +248,7 @@ __global__ void __launch_bounds__(QB_RF_BLOCK, QB_RF_MINB) k_render_f(DevScene S
             const int out_id = t > 0.0f ? oid : 0;
             if (valid) {
                 const long long off = (c * H + i) * (long long)W + j;
-                if (depth) depth[off] = t > 0.0f ? t * cz : cam.max_range;
+                if (depth) depth[off] = t > 0.0f ? t * rsqrtf(n2) : cam.max_range;
                 if (seg) seg[off] = out_id;
                 if (centroid_id > 0 && out_id == centroid_id) {
                     cnt += 1;
@@ -265,11 +314,6 @@ __device__ __forceinline__ bool keep(const Plane &P, float rx, float ry, float r
     return d + s >= -CULL_EPS;
 }
 
-__device__ __forceinline__ float rcp_approx(float x) {
-    float r;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-    return r;
-}
 
 // slab intersection from precomputed numerators (kernels.py:203-246 semantics:
 // entry clamped at tmin, exit returned when the origin is inside)

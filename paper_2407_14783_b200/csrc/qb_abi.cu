@@ -37,6 +37,12 @@ int sm_count() {
 }
 
 // ------------------------------------------------------------------ BVH
+#ifndef QB_BVH_LEAF
+#define QB_BVH_LEAF 4  // max primitives per leaf
+#endif
+#ifndef QB_BVH_BINS
+#define QB_BVH_BINS 16  // SAH bins per axis
+#endif
 // Binned-SAH binary BVH over primitive AABBs.  Children of an internal node
 // are adjacent (left = a, right = a + 1) and leaf primitives are contiguous,
 // like the reference layout (bvh.py:1-8), but the split is the SAH-optimal
@@ -53,7 +59,7 @@ static double half_area(const double *lo, const double *hi) {
 
 static int build_bvh(int n, const double *plo, const double *phi, std::vector<BNode> &nodes, std::vector<int> &order,
                      int &max_depth) {
-    const int LEAF = 4, BINS = 16, DEPTH_CAP = 56;
+    const int LEAF = QB_BVH_LEAF, BINS = QB_BVH_BINS, DEPTH_CAP = 56;
     order.resize(n);
     for (int i = 0; i < n; ++i) order[i] = i;
     std::vector<double> cen(3 * (size_t)n);

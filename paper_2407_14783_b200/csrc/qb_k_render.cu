@@ -45,6 +45,7 @@ extern "C" int qb_debug_render_stats(unsigned long long *out) {
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
+constexpr float CULL_EPS = 1e-3f;  // conservative culling margin (m)
 constexpr int TILE_W = 8, TILE_H = 4;
 
 struct CamF {
@@ -78,45 +79,141 @@ __device__ __forceinline__ void camera_pose(const R *p, const R *q, const R *cro
         for (int k = 0; k < 3; ++k) Rw[3 * i + k] = m[i][0] * crot[k] + m[i][1] * crot[3 + k] + m[i][2] * crot[6 + k];
 }
 
+// conservative AABB vs half-space n.x + off >= 0 (n unit): the box's most
+// positive corner along n
+QB_D bool box_in_plane(const float4 &lo, const float4 &hi, float nx, float ny, float nz, float off) {
+    const float px = nx >= 0.0f ? hi.x : lo.x, py = ny >= 0.0f ? hi.y : lo.y, pz = nz >= 0.0f ? hi.z : lo.z;
+    return nx * px + ny * py + nz * pz + off >= -CULL_EPS;
+}
+
+// world half-space of a camera-space plane through the camera origin with
+// normal (a, b, c) (not unit): inside iff n_w . (X - o) >= 0
+QB_D void world_plane(const float *Rs, const float *o, float a, float b, float c, float &nx, float &ny, float &nz,
+                      float &off) {
+    const float inv = rsqrtf(a * a + b * b + c * c);
+    a *= inv; b *= inv; c *= inv;
+    nx = Rs[0] * a + Rs[1] * b + Rs[2] * c;
+    ny = Rs[3] * a + Rs[4] * b + Rs[5] * c;
+    nz = Rs[6] * a + Rs[7] * b + Rs[8] * c;
+    off = -(nx * o[0] + ny * o[1] + nz * o[2]);
+}
+
+// K2 BVH packet renderer (large scenes).  One warp renders one camera:
+//  1. camera frontier: lane-parallel breadth-first descent of the scene BVH,
+//     keeping nodes whose box meets the camera frustum (4 image planes, near,
+//     far), level by level while the frontier still fits in 32 entries
+//     (one per lane) -- this replaces the top ~10 levels of every tile's walk;
+//  2. per 8x4-pixel tile (one ray per lane): the frontier is culled against
+//     the tile's 4 side planes (one entry per lane), each survivor is
+//     slab-tested by all rays and pushed far-to-near with its warp-minimum
+//     entry distance;
+//  3. warp-uniform depth-first traversal from that stack: the current node is
+//     carried as its (a, b) record taken from the parent's child fetch (one
+//     dependent load per visit: the two adjacent child boxes), both children
+//     are slab-tested by every lane, the nearer (lane majority) is visited and
+//     the other pushed with its warp-minimum entry (REDUX.MIN on the float
+//     bits; entries are >= 0); a pop is skipped unless some lane's hit still
+//     lies beyond that entry.  Culling is conservative and the result (nearest
+//     t, ties to the lowest id) is traversal-order independent.
 template <bool FROM_STATE>
 __global__ void __launch_bounds__(QB_RF_BLOCK, QB_RF_MINB) k_render_f(DevScene S, CamF cam, long long n, long long ld, const float *state,
                                                      const float *origins, const float *rotations, const int32_t *env_scene,
                                                      float *depth, int32_t *seg, int centroid_id, float *centroid,
                                                      const float *extra, const int32_t *extra_ids, int n_extra) {
-    __shared__ int4 stk_s[QB_RF_BLOCK / 32][64];
-    __shared__ float rw_s[QB_RF_BLOCK / 32][9];  // camera rotation (kept out of registers)
-    int4 *stk = stk_s[threadIdx.x >> 5];
+    constexpr int WPB = QB_RF_BLOCK / 32, STK = 96;  // stack: <= 32 frontier entries + one per tree level (<= 62)
+    __shared__ int2 stk_s[WPB][STK];  // (node record packed as a * 8 + (b + 2), entry distance bits)
+    __shared__ int fr_s[WPB][32];     // camera frontier (node indices)
+    __shared__ float rw_s[WPB][9];    // camera rotation (kept out of registers)
+    int2 *stk = stk_s[threadIdx.x >> 5];
+    int *fr = fr_s[threadIdx.x >> 5];
     float *Rs = rw_s[threadIdx.x >> 5];
     const int lane = threadIdx.x & 31;
+    const unsigned lanes_below = (1u << lane) - 1u;
     const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
     const int W = cam.W, H = cam.H;
     const int tiles_x = (W + TILE_W - 1) / TILE_W, tiles_y = (H + TILE_H - 1) / TILE_H;
     const float tmin = 1e-9f;
     const float sx = 2.0f / W, sy = 2.0f / H;
+    constexpr unsigned INF_BITS = 0x7f800000u;
 
     for (long long c = warp; c < n; c += nwarps) {
-        float o[3], Rw[9];
-        if (FROM_STATE) {
-            float p[3] = {state[0 * ld + c], state[1 * ld + c], state[2 * ld + c]};
-            float q[4] = {state[6 * ld + c], state[7 * ld + c], state[8 * ld + c], state[9 * ld + c]};
-            camera_pose<float>(p, q, cam.rot, cam.trans, o, Rw);
-        } else {
+        float o[3];
+        {
+            float Rw[9];
+            if (FROM_STATE) {
+                float p[3] = {state[0 * ld + c], state[1 * ld + c], state[2 * ld + c]};
+                float q[4] = {state[6 * ld + c], state[7 * ld + c], state[8 * ld + c], state[9 * ld + c]};
+                camera_pose<float>(p, q, cam.rot, cam.trans, o, Rw);
+            } else {
 #pragma unroll
-            for (int k = 0; k < 3; ++k) o[k] = origins[3 * c + k];
+                for (int k = 0; k < 3; ++k) o[k] = origins[3 * c + k];
 #pragma unroll
-            for (int k = 0; k < 9; ++k) Rw[k] = rotations[9 * c + k];
+                for (int k = 0; k < 9; ++k) Rw[k] = rotations[9 * c + k];
+            }
+            __syncwarp();
+            if (lane < 9) Rs[lane] = Rw[lane];  // (all lanes hold the same pose)
+            __syncwarp();
         }
         const int scene = env_scene ? env_scene[c] : 0;
-        const int root = S.root[scene];
         int cnt = 0, sum_col = 0, sum_row = 0;
+
+        // ---- 1. camera frontier
+        int nf = 1;
+        if (lane == 0) fr[0] = S.root[scene];
         __syncwarp();
-        if (lane < 9) Rs[lane] = Rw[lane];  // (all lanes hold the same pose)
-        __syncwarp();
+        {
+            const float xa = (0.5f * sx - 1.0f) * cam.th, xb = ((W - 0.5f) * sx - 1.0f) * cam.th;
+            const float ya = (0.5f * sy - 1.0f) * cam.tv, yb = ((H - 0.5f) * sy - 1.0f) * cam.tv;
+            float pn[6][3], po[6];
+            world_plane(Rs, o, 1.0f, 0.0f, -xa, pn[0][0], pn[0][1], pn[0][2], po[0]);
+            world_plane(Rs, o, -1.0f, 0.0f, xb, pn[1][0], pn[1][1], pn[1][2], po[1]);
+            world_plane(Rs, o, 0.0f, 1.0f, -ya, pn[2][0], pn[2][1], pn[2][2], po[2]);
+            world_plane(Rs, o, 0.0f, -1.0f, yb, pn[3][0], pn[3][1], pn[3][2], po[3]);
+            world_plane(Rs, o, 0.0f, 0.0f, 1.0f, pn[4][0], pn[4][1], pn[4][2], po[4]);  // in front
+            pn[5][0] = -pn[4][0]; pn[5][1] = -pn[4][1]; pn[5][2] = -pn[4][2];
+            po[5] = -po[4] + cam.max_range;                                              // z-depth <= max range
+            auto in_frustum = [&](const float4 &lo, const float4 &hi) {
+                bool in = true;
+#pragma unroll
+                for (int k = 0; k < 6; ++k) in &= box_in_plane(lo, hi, pn[k][0], pn[k][1], pn[k][2], po[k]);
+                return in;
+            };
+            for (int level = 0; level < 64; ++level) {
+                const bool have = lane < nf;
+                const int node = have ? fr[lane] : 0;
+                const float4 lo = __ldg(S.nodef + 2 * node), hi = __ldg(S.nodef + 2 * node + 1);
+                const int a = __float_as_int(lo.w), b = __float_as_int(hi.w);
+                const bool inner = have && b <= 0;
+                if (!__any_sync(FULL, inner)) break;
+                bool kl = false, kr = false;
+                if (inner) {
+                    kl = in_frustum(__ldg(S.nodef + 2 * a), __ldg(S.nodef + 2 * a + 1));
+                    kr = in_frustum(__ldg(S.nodef + 2 * a + 2), __ldg(S.nodef + 2 * a + 3));
+                }
+                const int nout = inner ? (int)kl + (int)kr : (have ? 1 : 0);
+                const unsigned b0 = __ballot_sync(FULL, nout & 1), b1 = __ballot_sync(FULL, nout & 2);
+                const int total = __popc(b0) + 2 * __popc(b1);
+                if (total > 32) break;
+                const int pos = __popc(b0 & lanes_below) + 2 * __popc(b1 & lanes_below);
+                __syncwarp();
+                if (inner) {
+                    int q = pos;
+                    if (kl) fr[q++] = a;
+                    if (kr) fr[q] = a + 1;
+                } else if (have) {
+                    fr[pos] = node;
+                }
+                __syncwarp();
+                nf = total;
+                if (nf == 0) break;
+            }
+        }
 
         for (int tile = 0; tile < tiles_x * tiles_y; ++tile) {
-            const int j = (tile % tiles_x) * TILE_W + (lane & 7);
-            const int i = (tile / tiles_x) * TILE_H + (lane >> 3);
+            const int j0 = (tile % tiles_x) * TILE_W, i0 = (tile / tiles_x) * TILE_H;
+            const int j = j0 + (lane & 7);
+            const int i = i0 + (lane >> 3);
             const bool valid = (j < W) && (i < H);
             const float y = ((i + 0.5f) * sy - 1.0f) * cam.tv;
             const float x = ((j + 0.5f) * sx - 1.0f) * cam.th;
@@ -140,30 +237,73 @@ __global__ void __launch_bounds__(QB_RF_BLOCK, QB_RF_MINB) k_render_f(DevScene S
             unsigned st_visit = 0, st_prim = 0, st_active = __popc(__ballot_sync(FULL, valid));
 #endif
 
-            // warp-uniform traversal with a per-warp shared-memory stack (lane 0
-            // pushes, all lanes read the broadcast).  The current node is carried
-            // as its (a, b) record taken from the parent's child fetch, so a
-            // visit costs one dependent load (the two child boxes, adjacent);
-            // both children are slab-tested by every lane, the nearer one (lane
-            // majority) is visited next and the other pushed with its
-            // warp-minimum entry distance (REDUX.MIN on the float bits, valid as
-            // entries are >= 0), so a pop needs no reload: it is skipped unless
-            // some lane's current hit still lies beyond that distance.
-            constexpr unsigned INF_BITS = 0x7f800000u;
+            // ---- 2. frontier entries meeting the tile's frustum, far-to-near on the stack
             int sp = 0;
-            int ca, cb;
             {
-                const float4 lo = __ldg(S.nodef + 2 * root), hi = __ldg(S.nodef + 2 * root + 1);
-                ca = __float_as_int(lo.w);
-                cb = __float_as_int(hi.w);
-                if (!__any_sync(FULL, slab_enter_fma(lo, hi, oix, oiy, oiz, ix, iy, iz, best) <= best)) ca = -1;
+                const int jb = min(j0 + TILE_W, W) - 1, ib = min(i0 + TILE_H, H) - 1;
+                const float xa = ((j0 + 0.5f) * sx - 1.0f) * cam.th, xb = ((jb + 0.5f) * sx - 1.0f) * cam.th;
+                const float ya = ((i0 + 0.5f) * sy - 1.0f) * cam.tv, yb = ((ib + 0.5f) * sy - 1.0f) * cam.tv;
+                bool in = false;
+                if (lane < nf) {
+                    const int node = fr[lane];
+                    const float4 lo = __ldg(S.nodef + 2 * node), hi = __ldg(S.nodef + 2 * node + 1);
+                    float nx, ny, nz, of;
+                    world_plane(Rs, o, 1.0f, 0.0f, -xa, nx, ny, nz, of);
+                    in = box_in_plane(lo, hi, nx, ny, nz, of);
+                    world_plane(Rs, o, -1.0f, 0.0f, xb, nx, ny, nz, of);
+                    in &= box_in_plane(lo, hi, nx, ny, nz, of);
+                    world_plane(Rs, o, 0.0f, 1.0f, -ya, nx, ny, nz, of);
+                    in &= box_in_plane(lo, hi, nx, ny, nz, of);
+                    world_plane(Rs, o, 0.0f, -1.0f, yb, nx, ny, nz, of);
+                    in &= box_in_plane(lo, hi, nx, ny, nz, of);
+                }
+                // survivors' entry distances (all rays), kept one per lane
+                unsigned my_e = INF_BITS;
+                int my_rec = 0, ns = 0;
+                for (unsigned m = __ballot_sync(FULL, in); m; m &= m - 1) {
+                    const int node = fr[__ffs(m) - 1];
+                    const float4 lo = __ldg(S.nodef + 2 * node), hi = __ldg(S.nodef + 2 * node + 1);
+                    const float e = slab_enter_fma(lo, hi, oix, oiy, oiz, ix, iy, iz, best);
+                    const unsigned em = __reduce_min_sync(FULL, e <= best ? __float_as_uint(e) : INF_BITS);
+                    if (em != INF_BITS) {
+                        if (lane == ns) {
+                            my_e = em;
+                            my_rec = __float_as_int(lo.w) * 8 + (__float_as_int(hi.w) + 2);
+                        }
+                        ++ns;
+                    }
+                }
+                // rank: farthest first (bottom of the stack), ties by lane
+                int rank = 0;
+                for (int q = 0; q < ns; ++q) {
+                    const unsigned eq = __shfl_sync(FULL, my_e, q);
+                    rank += (eq > my_e) || (eq == my_e && q < lane);
+                }
+                __syncwarp();
+                if (lane < ns) stk[rank] = make_int2(my_rec, (int)my_e);
+                sp = ns;
+                __syncwarp();
             }
-            // (ca, cb): leaf {first, count > 0} or internal {left child, -axis <= 0}; ca < 0: done
-            while (ca >= 0) {
+
+            // ---- 3. depth-first traversal; (ca, cb): leaf {first, count > 0} or
+            // internal {left child, -axis <= 0}; ca < 0: pop
+            int ca = -1, cb = 0;
+            while (true) {
+                if (ca < 0) {
+                    while (sp > 0) {
+                        const int2 e = stk[--sp];
+                        if (__any_sync(FULL, __uint_as_float((unsigned)e.y) <= best)) {
+                            ca = e.x >> 3;
+                            cb = (e.x & 7) - 2;
+                            break;
+                        }
+                    }
+                    __syncwarp();
+                    if (ca < 0) break;
+                }
 #ifdef QB_RF_STATS
                 ++st_visit;
 #endif
-                bool descend = false;
                 if (cb > 0) {
 #ifdef QB_RF_STATS
                     st_prim += cb;
@@ -184,45 +324,33 @@ __global__ void __launch_bounds__(QB_RF_BLOCK, QB_RF_MINB) k_render_f(DevScene S
                             hit = true;
                         }
                     }
+                    ca = -1;
+                    continue;
+                }
+                const float4 llo = __ldg(S.nodef + 2 * ca), lhi = __ldg(S.nodef + 2 * ca + 1);
+                const float4 rlo = __ldg(S.nodef + 2 * ca + 2), rhi = __ldg(S.nodef + 2 * ca + 3);
+                const float el = slab_enter_fma(llo, lhi, oix, oiy, oiz, ix, iy, iz, best);
+                const float er = slab_enter_fma(rlo, rhi, oix, oiy, oiz, ix, iy, iz, best);
+                const bool wl = el <= best, wr = er <= best;
+                const bool hl = __any_sync(FULL, wl);
+                const bool hr = __any_sync(FULL, wr);
+                if (hl && hr) {
+                    const bool left_first = __popc(__ballot_sync(FULL, el <= er)) >= 16;
+                    const float4 nlo = left_first ? llo : rlo, nhi = left_first ? lhi : rhi;
+                    const float4 flo = left_first ? rlo : llo, fhi = left_first ? rhi : lhi;
+                    const float ef = left_first ? er : el;
+                    const bool wf = left_first ? wr : wl;
+                    const unsigned em = __reduce_min_sync(FULL, wf ? __float_as_uint(ef) : INF_BITS);
+                    if (lane == 0) stk[sp] = make_int2(__float_as_int(flo.w) * 8 + (__float_as_int(fhi.w) + 2), (int)em);
+                    ++sp;
+                    ca = __float_as_int(nlo.w);
+                    cb = __float_as_int(nhi.w);
+                } else if (hl || hr) {
+                    ca = __float_as_int(hl ? llo.w : rlo.w);
+                    cb = __float_as_int(hl ? lhi.w : rhi.w);
                 } else {
-                    const float4 llo = __ldg(S.nodef + 2 * ca), lhi = __ldg(S.nodef + 2 * ca + 1);
-                    const float4 rlo = __ldg(S.nodef + 2 * ca + 2), rhi = __ldg(S.nodef + 2 * ca + 3);
-                    const float el = slab_enter_fma(llo, lhi, oix, oiy, oiz, ix, iy, iz, best);
-                    const float er = slab_enter_fma(rlo, rhi, oix, oiy, oiz, ix, iy, iz, best);
-                    const bool wl = el <= best, wr = er <= best;
-                    const bool hl = __any_sync(FULL, wl);
-                    const bool hr = __any_sync(FULL, wr);
-                    if (hl && hr) {
-                        const bool left_first = __popc(__ballot_sync(FULL, el <= er)) >= 16;
-                        const float4 nlo = left_first ? llo : rlo, nhi = left_first ? lhi : rhi;
-                        const float4 flo = left_first ? rlo : llo, fhi = left_first ? rhi : lhi;
-                        const float ef = left_first ? er : el;
-                        const bool wf = left_first ? wr : wl;
-                        const unsigned em = __reduce_min_sync(FULL, wf ? __float_as_uint(ef) : INF_BITS);
-                        if (lane == 0) stk[sp] = make_int4(__float_as_int(flo.w), __float_as_int(fhi.w), (int)em, 0);
-                        ++sp;
-                        ca = __float_as_int(nlo.w);
-                        cb = __float_as_int(nhi.w);
-                        descend = true;
-                    } else if (hl || hr) {
-                        ca = __float_as_int(hl ? llo.w : rlo.w);
-                        cb = __float_as_int(hl ? lhi.w : rhi.w);
-                        descend = true;
-                    }
+                    ca = -1;
                 }
-                if (descend) continue;
-                // pop the next node some lane may still need
-                ca = -1;
-                __syncwarp();
-                while (sp > 0) {
-                    const int4 e = stk[--sp];
-                    if (__any_sync(FULL, __uint_as_float((unsigned)e.z) <= best)) {
-                        ca = e.x;
-                        cb = e.y;
-                        break;
-                    }
-                }
-                __syncwarp();
             }
 #ifdef QB_RF_STATS
             if (lane == 0) {
@@ -292,7 +420,6 @@ __global__ void __launch_bounds__(QB_RF_BLOCK, QB_RF_MINB) k_render_f(DevScene S
 constexpr int CULL_MAX = 256;   // primitives per scene
 constexpr int CULL_WARPS = 4;   // warps (cameras) per block
 constexpr int CREC = 64;        // precomputed records per camera (nav room: mean 21, max 58); more use the generic path
-constexpr float CULL_EPS = 1e-3f;
 enum { REC_SPHERE = 0, REC_AABB = 1, REC_OBB = 2, REC_GENERIC = 3 };
 
 struct Plane {

@@ -46,6 +46,7 @@ namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 constexpr float CULL_EPS = 1e-3f;  // conservative culling margin (m)
+constexpr int TPL_MAX = 128;       // tile-plane table entries (64x64 frames use 32)
 constexpr int TILE_W = 8, TILE_H = 4;
 
 struct CamF {
@@ -464,6 +465,7 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, 6)
     __shared__ float4 rec_s[CULL_WARPS][CREC][4];      // shading records (warp-broadcast reads)
     __shared__ int2 met_s[CULL_WARPS][CREC];           // (record type, object id)
     __shared__ float cul_s[CULL_WARPS][13][CREC];      // culling bounds, SoA (conflict-free lane-parallel reads)
+    __shared__ float4 tpl_s[TPL_MAX][2];               // per-tile camera-space planes (xl xr yt yb) (iL iR iT iB)
     const int wib = threadIdx.x >> 5;
     int *cand = cand_s[wib];
     float4 (*rec)[4] = rec_s[wib];
@@ -474,8 +476,26 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, 6)
     const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
     const int W = cam.W, H = cam.H;
-    const int tiles_x = (W + TILE_W - 1) / TILE_W, tiles_y = (H + TILE_H - 1) / TILE_H;
+    const int tiles_x = (W + TILE_W - 1) / TILE_W;
     const float tmin = 1e-9f;
+    // pixel-centre image-plane coordinates: x(j) = ((j + 0.5) * 2/W - 1) * th
+    const float sx = 2.0f / W, sy = 2.0f / H;
+    constexpr int TH2 = 2 * TILE_H;
+    const int tiles_y2 = (H + TH2 - 1) / TH2, n_tiles = tiles_y2 * tiles_x;
+    // the tile planes depend on the tile only: one table per block
+    const bool tpl = n_tiles <= TPL_MAX;
+    if (tpl) {
+        for (int tl = threadIdx.x; tl < n_tiles; tl += blockDim.x) {
+            const int i0 = (tl / tiles_x) * TH2, j0 = (tl % tiles_x) * TILE_W;
+            const int j1 = min(j0 + TILE_W - 1, W - 1), i1 = min(i0 + TH2 - 1, H - 1);
+            const float xl = ((j0 + 0.5f) * sx - 1.0f) * cam.th, xr = ((j1 + 0.5f) * sx - 1.0f) * cam.th;
+            const float yt = ((i0 + 0.5f) * sy - 1.0f) * cam.tv, yb = ((i1 + 0.5f) * sy - 1.0f) * cam.tv;
+            tpl_s[tl][0] = make_float4(xl, xr, yt, yb);
+            tpl_s[tl][1] = make_float4(rsqrtf(1.f + xl * xl), rsqrtf(1.f + xr * xr), rsqrtf(1.f + yt * yt),
+                                       rsqrtf(1.f + yb * yb));
+        }
+    }
+    __syncthreads();
 
     // small batches: `split` warps share one camera, each taking every split-th tile
     for (long long wi = warp; wi < n * split; wi += nwarps) {
@@ -568,28 +588,39 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, 6)
             __syncwarp();
         }
 
-        long long cnt = 0, sum_col = 0, sum_row = 0;
-        // pixel-centre image-plane coordinates: x(j) = ((j + 0.5) * 2/W - 1) * th
-        const float sx = 2.0f / W, sy = 2.0f / H;
+        int cnt = 0, sum_col = 0, sum_row = 0;
+        // per-camera output planes (32-bit offsets inside one frame)
+        float *depth_c = depth ? depth + c * (long long)H * W : nullptr;
+        int32_t *seg_c = seg ? seg + c * (long long)H * W : nullptr;
         // an 8x8 tile per warp iteration, two pixels per lane (rows r and r+4):
         // the tile's culling and loop overhead is shared by 64 rays and each
         // candidate test runs two independent rays (ILP)
-        constexpr int TH2 = 2 * TILE_H;
-        const int tiles_y2 = (H + TH2 - 1) / TH2;
-        for (int tl = part; tl < tiles_y2 * tiles_x; tl += split) {
-            const int i0 = (tl / tiles_x) * TH2, j0 = (tl % tiles_x) * TILE_W;
+        int tx = part % tiles_x, ty = part / tiles_x;
+        for (int tl = part; tl < n_tiles; tl += split) {
+            const int i0 = ty * TH2, j0 = tx * TILE_W;
             const int j = j0 + (lane & 7);
             int ii[2] = {i0 + (lane >> 3), i0 + TILE_H + (lane >> 3)};
             // tile planes in CAMERA space through the pixel-centre rays of its border pixels
-            const int j1 = min(j0 + TILE_W - 1, W - 1), i1 = min(i0 + TH2 - 1, H - 1);
-            const float xl = ((j0 + 0.5f) * sx - 1.0f) * cam.th, xr = ((j1 + 0.5f) * sx - 1.0f) * cam.th;
-            const float yt = ((i0 + 0.5f) * sy - 1.0f) * cam.tv, yb = ((i1 + 0.5f) * sy - 1.0f) * cam.tv;
-            const float iL = rsqrtf(1.f + xl * xl), iR = rsqrtf(1.f + xr * xr);
-            const float iT = rsqrtf(1.f + yt * yt), iB = rsqrtf(1.f + yb * yb);
+            float xl, xr, yt, yb, iL, iR, iT, iB;
+            if (tpl) {
+                const float4 pa = tpl_s[tl][0], pb = tpl_s[tl][1];
+                xl = pa.x; xr = pa.y; yt = pa.z; yb = pa.w;
+                iL = pb.x; iR = pb.y; iT = pb.z; iB = pb.w;
+            } else {
+                const int j1 = min(j0 + TILE_W - 1, W - 1), i1 = min(i0 + TH2 - 1, H - 1);
+                xl = ((j0 + 0.5f) * sx - 1.0f) * cam.th; xr = ((j1 + 0.5f) * sx - 1.0f) * cam.th;
+                yt = ((i0 + 0.5f) * sy - 1.0f) * cam.tv; yb = ((i1 + 0.5f) * sy - 1.0f) * cam.tv;
+                iL = rsqrtf(1.f + xl * xl); iR = rsqrtf(1.f + xr * xr);
+                iT = rsqrtf(1.f + yt * yt); iB = rsqrtf(1.f + yb * yb);
+            }
+            tx += split;
+            while (tx >= tiles_x) {
+                tx -= tiles_x;
+                ++ty;
+            }
             const float x = ((j + 0.5f) * sx - 1.0f) * cam.th;
             float dx[2], dy[2], dz[2], ix[2], iy[2], iz[2], czv[2], tmx[2], best[2];
-            int bid[2];
-            bool hit[2];
+            int bid[2];  // INT_MAX: no hit yet
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
                 const float y = ((ii[u] + 0.5f) * sy - 1.0f) * cam.tv;
@@ -603,10 +634,9 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, 6)
                 iy[u] = rcp_approx(dy[u]);
                 iz[u] = rcp_approx(dz[u]);
                 czv[u] = cz;
-                tmx[u] = cam.max_range * sqrtf(n2);
+                tmx[u] = cam.max_range * (n2 * cz);  // max_range / cos(angle to the axis)
                 best[u] = tmx[u];
-                bid[u] = -1;
-                hit[u] = false;
+                bid[u] = 0x7fffffff;
             }
             for (int b = 0; b < ncand; b += 32) {
                 const int k = b + lane;
@@ -690,18 +720,19 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, 6)
                     }
 #pragma unroll
                     for (int u = 0; u < 2; ++u)
-                        if (t[u] > 0.0f && (t[u] < best[u] || !hit[u] || (t[u] == best[u] && oid < bid[u]))) {
+                        // tests return t <= best; ties go to the lowest object id
+                        if (t[u] > 0.0f && (t[u] < best[u] || oid < bid[u])) {
                             best[u] = t[u];
                             bid[u] = oid;
-                            hit[u] = true;
                         }
                 }
             }
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
                 const int i = ii[u];
-                float t = hit[u] ? best[u] : -1.0f;
-                int oid = hit[u] ? bid[u] : -1;
+                const bool hit = bid[u] != 0x7fffffff;
+                float t = hit ? best[u] : -1.0f;
+                int oid = hit ? bid[u] : -1;
                 for (int k = 0; k < n_extra; ++k) {  // swarm agents as spheres (kernels.py:438-445)
                     const float4 sph = *reinterpret_cast<const float4 *>(extra + (c * n_extra + k) * 4);
                     float4 rec2[2] = {sph, make_float4(sph.w * sph.w, 0.f, 0.f, 0.f)};
@@ -713,9 +744,9 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, 6)
                 }
                 const int out_id = t > 0.0f ? oid : 0;
                 if (j < W && i < H) {
-                    const long long off = (c * H + i) * (long long)W + j;
-                    if (depth) depth[off] = t > 0.0f ? t * czv[u] : cam.max_range;
-                    if (seg) seg[off] = out_id;
+                    const int off = i * W + j;
+                    if (depth_c) depth_c[off] = t > 0.0f ? t * czv[u] : cam.max_range;
+                    if (seg_c) seg_c[off] = out_id;
                     if (centroid_id > 0 && out_id == centroid_id) {
                         cnt += 1;
                         sum_col += j;

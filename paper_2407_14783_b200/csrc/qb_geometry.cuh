@@ -173,6 +173,63 @@ QB_D NearestResult nearest_point(const DevScene &S, int scene, double qx_, doubl
     return {bx.v, by.v, bz.v, best.v, best_id};
 }
 
+// Warp-cooperative nearest point for small scenes (<= NEAREST_BRUTE_MAX
+// primitives): the 32 lanes split the scene's primitives, each keeps its best
+// (d2, object id, primitive) and a shuffle argmin picks the winner -- the same
+// (d2, lowest id) result as the BVH walk above (which prunes only strictly
+// farther boxes), at the latency of a few primitive tests instead of a
+// dependent traversal.  All 32 lanes must call it with the same query; larger
+// scenes fall back to the BVH walk in every lane.
+constexpr int NEAREST_BRUTE_MAX = 1024;
+QB_D NearestResult nearest_point_warp(const DevScene &S, int scene, double qx_, double qy_, double qz_) {
+    const int p0 = S.prim_offset[scene], p1 = S.prim_offset[scene + 1];
+    if (p1 - p0 > NEAREST_BRUTE_MAX) return nearest_point(S, scene, qx_, qy_, qz_);
+    const unsigned FULLM = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    xd qx(qx_), qy(qy_), qz(qz_);
+    double best = infinity_d();
+    int best_id = 0x7fffffff, best_p = 0x7fffffff;
+    double bx = 0.0, by = 0.0, bz = 0.0;
+    for (int p = p0 + lane; p < p1; p += 32) {
+        const int2 m = S.meta[p];
+        const double *dd = S.primd + 16 * p;
+        xd d[15];
+#pragma unroll
+        for (int k = 0; k < 15; ++k) d[k] = xd(dd[k]);
+        V3<xd> c;
+        if (m.x == QB_SPHERE)
+            c = closest_on_sphere<xd>(d[0], d[1], d[2], d[3], qx, qy, qz);
+        else if (m.x == QB_BOX)
+            c = closest_on_box<xd>(d, qx, qy, qz);
+        else
+            c = closest_on_triangle<xd>(d, qx, qy, qz);
+        xd ex = qx - c.x, ey = qy - c.y, ez = qz - c.z;
+        const double pd2 = (ex * ex + ey * ey + ez * ez).v;
+        if (pd2 < best || (pd2 == best && m.y < best_id)) {  // p ascends per lane
+            best = pd2;
+            best_id = m.y;
+            best_p = p;
+            bx = c.x.v; by = c.y.v; bz = c.z.v;
+        }
+    }
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) {
+        const double od = __shfl_xor_sync(FULLM, best, s);
+        const int oi = __shfl_xor_sync(FULLM, best_id, s), op = __shfl_xor_sync(FULLM, best_p, s);
+        if (od < best || (od == best && (oi < best_id || (oi == best_id && op < best_p)))) {
+            best = od;
+            best_id = oi;
+            best_p = op;
+        }
+    }
+    const int owner = best_p == 0x7fffffff ? 0 : (best_p - p0) & 31;
+    bx = __shfl_sync(FULLM, bx, owner);
+    by = __shfl_sync(FULLM, by, owner);
+    bz = __shfl_sync(FULLM, bz, owner);
+    if (best_id == 0x7fffffff) return {0.0, 0.0, 0.0, best, -1};
+    return {bx, by, bz, best, best_id};
+}
+
 // ---------------------------------------------------------------- ray tests
 // Reference formulas (exact policy): kernels.py:185-275
 

@@ -61,26 +61,39 @@ template <class R> __device__ __forceinline__ void hover_state(const DynConsts<R
     for (int k = 13; k < 17; ++k) x[k] = C.hover_speed;
 }
 
-// base.py:114-147 for env i (shard-local index); returns false on SpawnFailure
-template <class R> __device__ bool spawn(const EnvArgs<R> &A, long long i, R *x) {
+// nearest point of one env's query: per thread (BVH walk) or, in the
+// warp-per-env kernels, warp-cooperative
+template <bool WARP> __device__ __forceinline__ NearestResult nearest_q(const DevScene &S, int scene, const double *q) {
+    if constexpr (WARP)
+        return nearest_point_warp(S, scene, q[0], q[1], q[2]);
+    else
+        return nearest_point(S, scene, q[0], q[1], q[2]);
+}
+
+// base.py:114-147 for env i (shard-local index); returns false on SpawnFailure.
+// WARP: all 32 lanes run it on the same env (same draws); `lead` writes.
+template <class R, bool WARP> __device__ bool spawn(const EnvArgs<R> &A, long long i, R *x, bool lead) {
     const qb_task &T = A.T;
     const qb_env_buffers &B = A.B;
     const long long gi = B.index_offset + i;
     const int rc = B.reset_count[i];
     const int scene = T.scene_perm[(int)((gi + rc) % T.n_scene_perm)];
-    B.agent_scene[i] = scene;
-    B.reset_count[i] = rc + 1;
     Pcg64 r = pcg_load(B.rng + 4 * i);
+    if (WARP) __syncwarp();  // every lane has read the old values
+    if (lead) {
+        B.agent_scene[i] = scene;
+        B.reset_count[i] = rc + 1;
+    }
     double pos[3] = {0.0, 0.0, 0.0};
     bool found = false;
     for (int k = 0; k < 1000; ++k) {
         sample_dist(T.spawn[0], r, pos);
-        NearestResult nr = nearest_point(A.S, scene, pos[0], pos[1], pos[2]);
+        NearestResult nr = nearest_q<WARP>(A.S, scene, pos);
         if (__dsqrt_rn(nr.d2) < T.min_spawn_clearance) continue;
         found = true;
         break;
     }
-    if (!found) atomicAdd(B.error_count, 1);
+    if (!found && lead) atomicAdd(B.error_count, 1);
     double vel[3], rpy[3], ang[3], q[4];
     sample_dist(T.spawn[1], r, vel);
     sample_dist(T.spawn[2], r, rpy);
@@ -95,8 +108,11 @@ template <class R> __device__ bool spawn(const EnvArgs<R> &A, long long i, R *x)
         x[6 + k] = from_dbl<R>(q[k]);
         x[13 + k] = A.C.hover_speed;
     }
-    B.step_count[i] = 0;
-    pcg_store(B.rng + 4 * i, r);
+    if (lead) {
+        B.step_count[i] = 0;
+        pcg_store(B.rng + 4 * i, r);
+    }
+    if (WARP) __syncwarp();  // the lead's writes are visible to the lanes that read them next
     return found;
 }
 
@@ -106,9 +122,9 @@ struct Proximity {
 };
 
 // base.py:214-224 in exact double
-template <class R> __device__ __forceinline__ Proximity proximity(const EnvArgs<R> &A, int scene, const R *x) {
+template <class R, bool WARP> __device__ __forceinline__ Proximity proximity(const EnvArgs<R> &A, int scene, const R *x) {
     double p[3] = {r_dbl(x[0]), r_dbl(x[1]), r_dbl(x[2])};
-    NearestResult nr = nearest_point(A.S, scene, p[0], p[1], p[2]);
+    NearestResult nr = nearest_q<WARP>(A.S, scene, p);
     Proximity out;
     out.dist = __dsqrt_rn(nr.d2);
     out.px = nr.px;
@@ -177,45 +193,63 @@ __device__ __forceinline__ void write_post(const EnvArgs<R> &A, long long i, con
     B.out_of_bounds[i] = pr.oob;
 }
 
+// env index of this thread: one env per thread, or one per warp (WARP: every
+// lane computes the env redundantly, lane 0 stores; used for small batches,
+// where the warp-cooperative nearest-point query removes the dependent BVH
+// walk from the step's critical path)
+template <bool WARP> __device__ __forceinline__ long long env_index(bool &lead) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    lead = !WARP || (threadIdx.x & 31) == 0;
+    return WARP ? (t >> 5) : t;
+}
+
 // mode 0: reset, mode 1: proximity refresh only
-template <class R> __global__ void __launch_bounds__(128) k_env_reset(EnvArgs<R> A, uint64_t seed, int mode) {
-    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+template <class R, bool WARP> __global__ void __launch_bounds__(128) k_env_reset(EnvArgs<R> A, uint64_t seed, int mode) {
+    bool lead;
+    const long long i = env_index<WARP>(lead);
     const qb_env_buffers &B = A.B;
     if (i >= B.n) return;
     R x[17];
     if (mode == 0) {
-        pcg_store(B.rng + 4 * i, pcg64_from_seed(seed + (uint64_t)(B.index_offset + i)));
-        B.reset_count[i] = 0;
+        if (lead) {
+            pcg_store(B.rng + 4 * i, pcg64_from_seed(seed + (uint64_t)(B.index_offset + i)));
+            B.reset_count[i] = 0;
+        }
+        if (WARP) __syncwarp();
         hover_state(A.C, x);
-        spawn(A, i, x);
-        store_planes(B.state, B.ld, i, x);
-        if (B.prev_state) store_planes(B.prev_state, B.ld, i, x);
-        B.step_count[i] = 0;
-        B.needs_respawn[i] = 0;
-        B.terminated[i] = 0;
-        B.truncated[i] = 0;
-        B.success[i] = 0;
-        B.nonfinite[i] = 0;
-        B.reward[i] = 0.0f;
+        spawn<R, WARP>(A, i, x, lead);
+        if (lead) {
+            store_planes(B.state, B.ld, i, x);
+            if (B.prev_state) store_planes(B.prev_state, B.ld, i, x);
+            B.step_count[i] = 0;
+            B.needs_respawn[i] = 0;
+            B.terminated[i] = 0;
+            B.truncated[i] = 0;
+            B.success[i] = 0;
+            B.nonfinite[i] = 0;
+            B.reward[i] = 0.0f;
+        }
     } else {
         load_state(A, i, x);
     }
-    write_post(A, i, proximity(A, B.agent_scene[i], x));
+    const Proximity pr = proximity<R, WARP>(A, B.agent_scene[i], x);
+    if (lead) write_post(A, i, pr);
 }
 
-template <class R, int KIND> __global__ void __launch_bounds__(128) k_env_step(EnvArgs<R> A) {
+template <class R, int KIND, bool WARP> __global__ void __launch_bounds__(128) k_env_step(EnvArgs<R> A) {
     using S = typename storage_of<R>::type;
-    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    bool lead;
+    const long long i = env_index<WARP>(lead);
     const qb_env_buffers &B = A.B;
     const qb_task &T = A.T;
     if (i >= B.n) return;
     R x[17];
     load_state(A, i, x);
-    if (T.auto_reset && B.needs_respawn[i]) spawn(A, i, x);
+    if (T.auto_reset && B.needs_respawn[i]) spawn<R, WARP>(A, i, x, lead);
     R prev[17];
 #pragma unroll
     for (int k = 0; k < 17; ++k) prev[k] = x[k];
-    if (B.prev_state) store_planes(B.prev_state, B.ld, i, x);
+    if (B.prev_state && lead) store_planes(B.prev_state, B.ld, i, x);
 
     R a[4], cmd[4];
     const S *act = static_cast<const S *>(B.action) + 4 * i;
@@ -229,7 +263,7 @@ template <class R, int KIND> __global__ void __launch_bounds__(128) k_env_step(E
     }
     const int steps = B.step_count[i] + 1;
     const int scene = B.agent_scene[i];
-    Proximity pr = proximity(A, scene, x);
+    Proximity pr = proximity<R, WARP>(A, scene, x);
 
     double pp[3] = {r_dbl(prev[0]), r_dbl(prev[1]), r_dbl(prev[2])};
     double p[3] = {r_dbl(x[0]), r_dbl(x[1]), r_dbl(x[2])};
@@ -239,6 +273,7 @@ template <class R, int KIND> __global__ void __launch_bounds__(128) k_env_step(E
     task_eval(T, pp, p, v, pr.dist, pr.collision, success, reward);
     const bool terminated = success || pr.collision || pr.oob || !ok;
     const bool truncated = !terminated && steps >= T.episode_max_steps;
+    if (!lead) return;
 
     store_planes(B.state, B.ld, i, x);
     B.step_count[i] = steps;
@@ -273,19 +308,27 @@ int dispatch_env(int mode, const qb_params *p, int kind, const qb_task *task, co
     A.B = *b;
     A.S = s->dev;
     const int BS = 128;
-    dim3 g(qb::env_grid(b->n, BS));
+    // small batches: one warp per env (warp-cooperative nearest point) while
+    // that still fits one wave of the machine
+    const bool warp = b->n * 32 <= (long long)qb::sm_count() * 2048;
+    dim3 g(qb::env_grid(warp ? b->n * 32 : b->n, BS));
     if (mode == 0 || mode == 2) {
-        k_env_reset<R><<<g, BS, 0, st>>>(A, seed, mode == 0 ? 0 : 1);
+        if (warp)
+            k_env_reset<R, true><<<g, BS, 0, st>>>(A, seed, mode == 0 ? 0 : 1);
+        else
+            k_env_reset<R, false><<<g, BS, 0, st>>>(A, seed, mode == 0 ? 0 : 1);
         return qb::check_launch("env_reset");
     }
+#define QB_ENV(K) (warp ? (k_env_step<R, K, true><<<g, BS, 0, st>>>(A), 0) : (k_env_step<R, K, false><<<g, BS, 0, st>>>(A), 0))
     switch (kind) {
-        case QB_CMD_SRT: k_env_step<R, QB_CMD_SRT><<<g, BS, 0, st>>>(A); break;
-        case QB_CMD_CTBR: k_env_step<R, QB_CMD_CTBR><<<g, BS, 0, st>>>(A); break;
-        case QB_CMD_PS: k_env_step<R, QB_CMD_PS><<<g, BS, 0, st>>>(A); break;
-        case QB_CMD_LV: k_env_step<R, QB_CMD_LV><<<g, BS, 0, st>>>(A); break;
-        case QB_CMD_ROTOR: k_env_step<R, QB_CMD_ROTOR><<<g, BS, 0, st>>>(A); break;
+        case QB_CMD_SRT: QB_ENV(QB_CMD_SRT); break;
+        case QB_CMD_CTBR: QB_ENV(QB_CMD_CTBR); break;
+        case QB_CMD_PS: QB_ENV(QB_CMD_PS); break;
+        case QB_CMD_LV: QB_ENV(QB_CMD_LV); break;
+        case QB_CMD_ROTOR: QB_ENV(QB_CMD_ROTOR); break;
         default: qb::set_error("unknown command kind %d", kind); return QB_EINVAL;
     }
+#undef QB_ENV
     return qb::check_launch("env_step");
 }
 

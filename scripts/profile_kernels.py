@@ -5,7 +5,7 @@ import argparse
 import torch
 
 ap = argparse.ArgumentParser()
-ap.add_argument("mode", choices=["nav", "indoor", "dyn", "bptt"])
+ap.add_argument("mode", choices=["nav", "indoor", "dyn", "bptt", "hover"])
 ap.add_argument("--envs", type=int, default=16384)
 a = ap.parse_args()
 if a.mode in ("nav", "indoor"):
@@ -24,6 +24,15 @@ if a.mode in ("nav", "indoor"):
     act[:, 0] = 1.0
     for _ in range(3):
         env.step(LV(act[:, :3], act[:, 3]))
+elif a.mode == "hover":  # config 1: 100 envs, CTBR, default scene, no sensors
+    from paper_2407_14783_b200.control import CTBR
+    from paper_2407_14783_b200.env import EnvConfig, make_env
+    env = make_env(EnvConfig(num_agents=a.envs, command_type="ctbr", episode_max_steps=1000))
+    env.reset(seed=0)
+    act = torch.zeros((a.envs, 4), device="cuda")
+    act[:, 0] = 9.81
+    for _ in range(3):
+        env.step(CTBR(act[:, 0], act[:, 1:]))
 elif a.mode == "dyn":
     import paper_2407_14783_b200._native as nat
     from paper_2407_14783_b200.params import native_params

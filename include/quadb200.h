@@ -197,10 +197,51 @@ int qb_env_step(const qb_params *p, int32_t cmd_kind, const qb_task *task, const
 /* Proximity refresh alone (base.py:214-224) on the current state. */
 int qb_env_refresh(const qb_task *task, const qb_scene *s, const qb_env_buffers *b, void *stream);
 
+/* ---------------------------------------------------------- observations */
+
+/* Sensor noise models (sensing.py:163-235 NoiseSpec / apply_noise). */
+enum qb_noise_kind {
+    QB_NOISE_NORMAL = 0,     /* + sigma * N(0,1) */
+    QB_NOISE_POISSON = 1,    /* Poisson(max(v,0) * scaling) / scaling */
+    QB_NOISE_SALTPEPPER = 2, /* p: corrupt to the image min / max */
+    QB_NOISE_SPECKLE = 3,    /* * (1 + sigma * N(0,1)) */
+    QB_NOISE_REDWOOD = 4     /* disparity-domain N(0, sigma_disparity) + quantization (depth only) */
+};
+enum qb_sensor_kind { QB_SENSOR_DEPTH = 0, QB_SENSOR_SEGMENTATION = 1, QB_SENSOR_IMU = 2 };
+#define QB_MAX_NOISE 4
+#define QB_MAX_SENSORS 8
+
+typedef struct qb_noise {
+    int32_t kind; /* qb_noise_kind */
+    int32_t pad_;
+    double sigma, p, scaling, sigma_disparity, quantization;
+} qb_noise;
+
+typedef struct qb_sensor_obs {
+    int32_t kind;    /* qb_sensor_kind */
+    int32_t n_noise; /* noise models applied in order, <= QB_MAX_NOISE */
+    qb_noise noise[QB_MAX_NOISE];
+    int32_t width, height; /* camera sensors */
+    const void *src; /* DEVICE rendered frames: depth (dtype) or segmentation (int32), (n,H,W); NULL for IMU */
+    void *out;       /* DEVICE observation in dtype: (n,H,W), or (n,6) IMU [specific force_b, angvel_b] */
+} qb_sensor_obs;
+
+/* The sensor part of QuadEnvBase.get_observation (base.py:287-305) for a
+ * shard: for every env, in sensor order, the ideal IMU reading
+ * (sensing.py:124-147) and each sensor's noise chain, drawing from the env's
+ * generator exactly as numpy's Generator does (standard_normal ziggurat,
+ * poisson, random).  Sensors without noise (other than IMU) need no call. */
+int qb_env_observe(const qb_params *p, const qb_env_buffers *b, int32_t n_sensors, const qb_sensor_obs *sensors,
+                   void *stream);
+
 /* numpy.random.default_rng(seed + i) seeding for i in [0,n): out (n,4). */
 int qb_rng_seed(uint64_t seed, int64_t n, uint64_t *out, void *stream);
 /* n draws of next_double from each stream (testing hook): out (n, k). */
 int qb_rng_doubles(int64_t n, uint64_t *rng, int32_t k, double *out, void *stream);
+/* k standard normals (numpy ziggurat) from each stream: out (n, k). */
+int qb_rng_normals(int64_t n, uint64_t *rng, int32_t k, double *out, void *stream);
+/* k Poisson draws per stream with means lam (n, k) (DEVICE): out (n, k) int64. */
+int qb_rng_poissons(int64_t n, uint64_t *rng, int32_t k, const double *lam, int64_t *out, void *stream);
 
 #ifdef __cplusplus
 }

@@ -52,6 +52,51 @@ def _sample(dist, rng):
     return np.asarray(dist.mean, float) + np.asarray(dist.sigma, float) * rng.standard_normal(3)
 
 
+def apply_noise(data, spec, rng, sensor="depth"):
+    """sensing.py:195-235 (validity table checked by the caller)."""
+    values = np.asarray(data, dtype=float)
+    if spec.kind == "normal":
+        return values.copy() if spec.sigma == 0.0 else values + spec.sigma * rng.standard_normal(values.shape)
+    if spec.kind == "poisson":
+        return rng.poisson(np.maximum(values, 0.0) * spec.scaling).astype(float) / spec.scaling
+    if spec.kind == "saltpepper":
+        out = values.copy()
+        if spec.p == 0.0:
+            return out
+        corrupt = rng.random(values.shape) < spec.p
+        salt = rng.random(values.shape) < 0.5
+        lo, hi = values.min(), values.max()
+        out[corrupt & salt] = hi
+        out[corrupt & ~salt] = lo
+        return out
+    if spec.kind == "speckle":
+        return values.copy() if spec.sigma == 0.0 else values * (1.0 + spec.sigma * rng.standard_normal(values.shape))
+    disparity = 1.0 / np.maximum(values, 1e-6)  # redwood
+    if spec.sigma_disparity > 0.0:
+        disparity = disparity + spec.sigma_disparity * rng.standard_normal(values.shape)
+    if spec.quantization > 0.0:
+        disparity = np.round(disparity / spec.quantization) * spec.quantization
+    disparity = np.maximum(disparity, 1.0 / (values.max() + 1.0) if values.size else 1e-6)
+    return 1.0 / disparity
+
+
+def imu_readings(state, P):
+    """sensing.py:124-147: [(thrust + drag)_B / m, body rates] per agent."""
+    w = state[:, 13:17]
+    k2, k1, k0 = P.thrust_coeffs[0], P.thrust_coeffs[1], P.thrust_coeffs[2]
+    thr = k2 * w ** 2 + k1 * w + k0
+    q, v = state[:, 6:10], state[:, 3:6]
+    ux, uy, uz = -q[:, 1], -q[:, 2], -q[:, 3]
+    tx, ty, tz = uy * v[:, 2] - uz * v[:, 1], uz * v[:, 0] - ux * v[:, 2], ux * v[:, 1] - uy * v[:, 0]
+    sx, sy, sz = uy * tz - uz * ty, uz * tx - ux * tz, ux * ty - uy * tx
+    vb = np.stack([v[:, 0] + 2.0 * (q[:, 0] * tx + sx), v[:, 1] + 2.0 * (q[:, 0] * ty + sy),
+                   v[:, 2] + 2.0 * (q[:, 0] * tz + sz)], axis=1)
+    c = np.array([P.drag_c[0], P.drag_c[1], P.drag_c[2]])
+    force = -c * vb * np.abs(vb)
+    force[:, 2] += thr[:, 0] + thr[:, 1] + thr[:, 2] + thr[:, 3]
+    return np.concatenate([force / P.mass, state[:, 10:13]], axis=1)
+
+
 class OracleEnv:
     def __init__(self, config, scenes, params, sim, gains):
         self.config = config
@@ -230,8 +275,21 @@ class OracleEnv:
         """base.py:287-310 + tasks.py:58-62, 113-118 (batched form)."""
         obs = {"state": self.state[:, 0:13].copy()}
         for sensor in self.config.sensors:
+            if sensor.kind == "imu":  # base.py:290-296
+                reading = imu_readings(self.state, self.P)
+                for i in range(self.n):
+                    for nz in sensor.noise:
+                        reading[i] = apply_noise(reading[i], nz, self.rngs[i], "imu")
+                obs[sensor.name] = reading
+                continue
             depth, seg = self.render(sensor)
-            obs[sensor.name] = depth if sensor.kind == "depth" else seg.astype(float)
+            img = depth if sensor.kind == "depth" else seg.astype(float)
+            if sensor.noise:  # base.py:298-303, per agent on its own generator
+                img = img.copy()
+                for i in range(self.n):
+                    for nz in sensor.noise:
+                        img[i] = apply_noise(img[i], nz, self.rngs[i], sensor.kind)
+            obs[sensor.name] = img
             self.seg_cache[sensor.name] = seg
         if self.task == "navigation":
             obs["target"] = np.broadcast_to(self.target, (self.n, 3)).copy()

@@ -132,6 +132,35 @@ class QbEnvBuffers(ctypes.Structure):
     ]
 
 
+QB_MAX_NOISE, QB_MAX_SENSORS = 4, 8
+NOISE_KINDS = {"normal": 0, "poisson": 1, "saltpepper": 2, "speckle": 3, "redwood": 4}
+SENSOR_KINDS = {"depth": 0, "segmentation": 1, "imu": 2}
+
+
+class QbNoise(ctypes.Structure):
+    _fields_ = [
+        ("kind", ctypes.c_int32),
+        ("pad_", ctypes.c_int32),
+        ("sigma", ctypes.c_double),
+        ("p", ctypes.c_double),
+        ("scaling", ctypes.c_double),
+        ("sigma_disparity", ctypes.c_double),
+        ("quantization", ctypes.c_double),
+    ]
+
+
+class QbSensorObs(ctypes.Structure):
+    _fields_ = [
+        ("kind", ctypes.c_int32),
+        ("n_noise", ctypes.c_int32),
+        ("noise", QbNoise * QB_MAX_NOISE),
+        ("width", ctypes.c_int32),
+        ("height", ctypes.c_int32),
+        ("src", _P),
+        ("out", _P),
+    ]
+
+
 # exported symbol -> (argtypes, restype)
 _I64, _I32, _U64, _D = ctypes.c_int64, ctypes.c_int32, ctypes.c_uint64, ctypes.c_double
 _PP = ctypes.POINTER
@@ -157,6 +186,9 @@ SIGNATURES = {
     "qb_env_refresh": ([_PP(QbTask), _P, _PP(QbEnvBuffers), _P], ctypes.c_int),
     "qb_rng_seed": ([_U64, _I64, _P, _P], ctypes.c_int),
     "qb_rng_doubles": ([_I64, _P, _I32, _P, _P], ctypes.c_int),
+    "qb_rng_normals": ([_I64, _P, _I32, _P, _P], ctypes.c_int),
+    "qb_rng_poissons": ([_I64, _P, _I32, _P, _P, _P], ctypes.c_int),
+    "qb_env_observe": ([_PP(QbParams), _PP(QbEnvBuffers), _I32, _P, _P], ctypes.c_int),
 }
 
 _lib = None

@@ -534,6 +534,14 @@ int qb_env_refresh(const qb_task *task, const qb_scene *s, const qb_env_buffers 
     return qb::launch_env(2, &dummy, 0, task, s, b, 0, qb::as_stream(stream));
 }
 
+int qb_env_observe(const qb_params *p, const qb_env_buffers *b, int32_t n_sensors, const qb_sensor_obs *sensors,
+                   void *stream) {
+    QB_REQUIRE(p && b && (sensors || n_sensors == 0), "qb_env_observe: NULL argument");
+    QB_REQUIRE(b->n >= 0 && b->ld >= b->n && b->state && b->rng, "qb_env_observe: bad env buffers");
+    QB_REQUIRE(b->dtype == QB_F32 || b->dtype == QB_F64, "qb_env_observe: bad dtype %d", b->dtype);
+    return qb::launch_observe(p, b, n_sensors, sensors, qb::as_stream(stream));
+}
+
 int qb_rng_seed(uint64_t seed, int64_t n, uint64_t *out, void *stream) {
     QB_REQUIRE(out && n >= 0, "qb_rng_seed: bad arguments");
     return qb::launch_rng_seed(seed, n, out, qb::as_stream(stream));
@@ -542,6 +550,16 @@ int qb_rng_seed(uint64_t seed, int64_t n, uint64_t *out, void *stream) {
 int qb_rng_doubles(int64_t n, uint64_t *rng, int32_t k, double *out, void *stream) {
     QB_REQUIRE(rng && out && n >= 0 && k >= 0, "qb_rng_doubles: bad arguments");
     return qb::launch_rng_doubles(n, rng, k, out, qb::as_stream(stream));
+}
+
+int qb_rng_normals(int64_t n, uint64_t *rng, int32_t k, double *out, void *stream) {
+    QB_REQUIRE(rng && out && n >= 0 && k >= 0, "qb_rng_normals: bad arguments");
+    return qb::launch_rng_normals(n, rng, k, out, qb::as_stream(stream));
+}
+
+int qb_rng_poissons(int64_t n, uint64_t *rng, int32_t k, const double *lam, int64_t *out, void *stream) {
+    QB_REQUIRE(rng && lam && out && n >= 0 && k >= 0, "qb_rng_poissons: bad arguments");
+    return qb::launch_rng_poissons(n, rng, k, lam, out, qb::as_stream(stream));
 }
 
 }  // extern "C"

@@ -71,4 +71,8 @@ int launch_env(int mode, const qb_params *p, int kind, const qb_task *task, cons
                uint64_t seed, cudaStream_t st);
 int launch_rng_seed(uint64_t seed, long long n, uint64_t *out, cudaStream_t st);
 int launch_rng_doubles(long long n, uint64_t *rng, int k, double *out, cudaStream_t st);
+int launch_rng_normals(long long n, uint64_t *rng, int k, double *out, cudaStream_t st);
+int launch_rng_poissons(long long n, uint64_t *rng, int k, const double *lam, int64_t *out, cudaStream_t st);
+int launch_observe(const qb_params *p, const qb_env_buffers *b, int n_sensors, const qb_sensor_obs *sensors,
+                   cudaStream_t st);
 }  // namespace qb

@@ -85,6 +85,21 @@ QB_HD uint64_t pcg64_next64(Pcg64 &r) {
     return (x >> rot) | (x << ((64 - rot) & 63));
 }
 
+// jump the stream ahead by delta draws (LCG power by squaring)
+QB_HD void pcg64_advance(Pcg64 &r, u128 delta) {
+    u128 cur_mult = qbrng::pcg_mult(), cur_plus = r.inc, acc_mult = 1, acc_plus = 0;
+    while (delta > 0) {
+        if (delta & 1) {
+            acc_mult *= cur_mult;
+            acc_plus = acc_plus * cur_mult + cur_plus;
+        }
+        cur_plus = (cur_mult + 1) * cur_plus;
+        cur_mult *= cur_mult;
+        delta >>= 1;
+    }
+    r.state = acc_mult * r.state + acc_plus;
+}
+
 QB_HD double pcg64_next_double(Pcg64 &r) { return (double)(pcg64_next64(r) >> 11) * (1.0 / 9007199254740992.0); }
 
 // storage: 4 x uint64 (state hi, state lo, inc hi, inc lo)
@@ -108,17 +123,93 @@ QB_D double uniform_draw(Pcg64 &r, double lo, double hi) {
     return __dadd_rn(lo, __dmul_rn(range, pcg64_next_double(r)));
 }
 
-// Standard normal.  numpy's Generator uses a 256-level ziggurat whose
-// tables are not exposed; this Marsaglia polar draw on the same stream is
-// statistically (not bitwise) equivalent -- no BASELINE config spawns from a
-// normal distribution.
+#define QB_ZIG_ATTR __device__
+#include "qb_ziggurat.h"
+
+// distributions.c random_standard_normal (numpy 2.3.5): 256-level ziggurat on
+// 52-bit magnitudes; tables in qb_ziggurat.h (generated, pinned against
+// numpy by tests/test_rng_restatement.py).  All arithmetic is the IEEE
+// double op numpy's C performs (no contraction); log1p/exp are CUDA's libm
+// (<= 1 ulp from glibc), which only matters on the ~1% wedge/tail draws.
 QB_D double normal_draw(Pcg64 &r) {
-    double u, v, s;
-    do {
-        u = 2.0 * pcg64_next_double(r) - 1.0;
-        v = 2.0 * pcg64_next_double(r) - 1.0;
-        s = u * u + v * v;
-    } while (s >= 1.0 || s == 0.0);
-    return u * sqrt(-2.0 * log(s) / s);
+    for (;;) {
+        uint64_t w = pcg64_next64(r);
+        const int idx = (int)(w & 0xff);
+        w >>= 8;
+        const uint64_t rabs = (w >> 1) & 0x000fffffffffffffULL;
+        double x = __dmul_rn((double)rabs, __ldg(&qb_zig_wi[idx]));
+        if (w & 0x1) x = -x;
+        if (rabs < __ldg(&qb_zig_ki[idx])) return x;
+        if (idx == 0) {
+            for (;;) {
+                const double xx = __dmul_rn(-(1.0 / QB_ZIG_R), log1p(-pcg64_next_double(r)));
+                const double yy = -log1p(-pcg64_next_double(r));
+                if (__dadd_rn(yy, yy) > __dmul_rn(xx, xx))
+                    return ((rabs >> 8) & 0x1) ? -__dadd_rn(QB_ZIG_R, xx) : __dadd_rn(QB_ZIG_R, xx);
+            }
+        }
+        const double f0 = __ldg(&qb_zig_fi[idx - 1]), f1 = __ldg(&qb_zig_fi[idx]);
+        if (__dadd_rn(__dmul_rn(__dsub_rn(f0, f1), pcg64_next_double(r)), f1) < exp(__dmul_rn(__dmul_rn(-0.5, x), x)))
+            return x;
+    }
+}
+
+// distributions.c random_loggam
+QB_D double loggam_np(double x) {
+    const double a[10] = {8.333333333333333e-02, -2.777777777777778e-03, 7.936507936507937e-04,
+                          -5.952380952380952e-04, 8.417508417508418e-04, -1.917526917526918e-03,
+                          6.410256410256410e-03, -2.955065359477124e-02, 1.796443723688307e-01,
+                          -1.39243221690590e+00};
+    if (x == 1.0 || x == 2.0) return 0.0;
+    const long long n = x < 7.0 ? (long long)(7 - x) : 0;
+    double x0 = __dadd_rn(x, (double)n);
+    const double ix = __ddiv_rn(1.0, x0), x2 = __dmul_rn(ix, ix);
+    double gl0 = a[9];
+    for (int k = 8; k >= 0; --k) gl0 = __dadd_rn(__dmul_rn(gl0, x2), a[k]);
+    double gl = __dsub_rn(__dadd_rn(__dadd_rn(__ddiv_rn(gl0, x0), __dmul_rn(0.5, 1.8378770664093453e+00)),
+                                    __dmul_rn(__dsub_rn(x0, 0.5), log(x0))),
+                          x0);
+    if (x < 7.0)
+        for (long long k = 1; k <= n; ++k) {
+            gl = __dsub_rn(gl, log(__dsub_rn(x0, 1.0)));
+            x0 = __dsub_rn(x0, 1.0);
+        }
+    return gl;
+}
+
+// distributions.c random_poisson: multiplication method below 10, PTRS
+// (Hoermann's transformed rejection) from 10 up
+QB_D long long poisson_draw(Pcg64 &r, double lam) {
+    if (lam >= 10) {
+        const double slam = __dsqrt_rn(lam), loglam = log(lam);
+        const double b = __dadd_rn(0.931, __dmul_rn(2.53, slam));
+        const double a = __dadd_rn(-0.059, __dmul_rn(0.02483, b));
+        const double invalpha = __dadd_rn(1.1239, __ddiv_rn(1.1328, __dsub_rn(b, 3.4)));
+        const double vr = __dsub_rn(0.9277, __ddiv_rn(3.6224, __dsub_rn(b, 2.0)));
+        for (;;) {
+            const double U = __dsub_rn(pcg64_next_double(r), 0.5);
+            const double V = pcg64_next_double(r);
+            const double us = __dsub_rn(0.5, fabs(U));
+            const long long k = (long long)floor(
+                __dadd_rn(__dadd_rn(__dmul_rn(__dadd_rn(__ddiv_rn(__dmul_rn(2.0, a), us), b), U), lam), 0.43));
+            if (us >= 0.07 && V <= vr) return k;
+            if (k < 0 || (us < 0.013 && V > us)) continue;
+            const double lhs = __dsub_rn(__dadd_rn(log(V), log(invalpha)),
+                                         log(__dadd_rn(__ddiv_rn(a, __dmul_rn(us, us)), b)));
+            const double rhs = __dsub_rn(__dadd_rn(-lam, __dmul_rn((double)k, loglam)), loggam_np((double)(k + 1)));
+            if (lhs <= rhs) return k;
+        }
+    }
+    if (lam == 0) return 0;
+    const double enlam = exp(-lam);
+    long long x = 0;
+    double prod = 1.0;
+    for (;;) {
+        prod = __dmul_rn(prod, pcg64_next_double(r));
+        if (prod > enlam)
+            ++x;
+        else
+            return x;
+    }
 }
 #endif

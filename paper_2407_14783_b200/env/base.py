@@ -144,11 +144,6 @@ class QuadEnvBase:
         nat.require_cuda()
         if config.mode != "parallel":
             raise ConfigError("swarm mode is not part of this build (SURVEY F2); use mode='parallel'")
-        for s in config.sensors:
-            if s.noise:
-                raise ConfigError("sensor noise models are not part of this build (SURVEY F1)")
-            if s.kind == "imu":
-                raise ConfigError("IMU sensors are not part of this build (SURVEY F1)")
         self.config = config
         self.params = params if params is not None else QuadParams()
         self.sim = sim if sim is not None else SimConfig()
@@ -162,7 +157,7 @@ class QuadEnvBase:
         self.index_offset = lo
         self.num_agents = hi - lo
         self.scenes = [spec.materialize() for spec in config.scenes]
-        self.sensor_cameras = [(s, s.camera()) for s in config.sensors]
+        self.sensor_cameras = [(s, None if s.kind == "imu" else s.camera()) for s in config.sensors]
         with torch.cuda.device(self.device):
             self.dev_scenes = DeviceScenes(self.scenes, device=self.device)
         self._P = native_params(self.params, self.sim, self.gains)
@@ -201,18 +196,48 @@ class QuadEnvBase:
         self._errors = z(1, dtype=torch.int32)
         self._scene_perm = z(len(self.scenes), dtype=torch.int32)
         # observation buffers: one render per distinct camera
-        self._cams = {}
+        self._cams, self._sensor_slot = {}, {}
         for spec, cam in self.sensor_cameras:
+            if cam is None:
+                continue
             key = (cam.width, cam.height, cam.vertical_fov, tuple(cam.rotation.ravel()), tuple(cam.translation), cam.max_range)
             if key not in self._cams:
-                self._cams[key] = {"camera": cam, "depth": None, "seg": None, "centroid": None}
+                self._cams[key] = {"camera": cam, "depth": None, "seg": None, "centroid": None, "names": []}
             slot = self._cams[key]
+            self._sensor_slot[spec.name] = slot
             if spec.kind == "depth" and slot["depth"] is None:
                 slot["depth"] = torch.zeros((n, cam.height, cam.width), dtype=dt, device=dev)
             if spec.kind == "segmentation" and slot["seg"] is None:
                 slot["seg"] = torch.zeros((n, cam.height, cam.width), dtype=torch.int32, device=dev)
             spec_slot = slot
-            spec_slot.setdefault("names", []).append((spec.name, spec.kind))
+            if not spec.noise:
+                spec_slot["names"].append((spec.name, spec.kind))
+        # the observation pass (qb_env_observe): IMU readings and noisy camera
+        # sensors, in config order -- the order their draws leave each env's
+        # generator (base.py:287-305)
+        self._obs_sensors, self._noise_error = [], None
+        from ..sensing import check_noise, sensor_obs
+
+        for spec, cam in self.sensor_cameras:
+            try:
+                for nz in spec.noise:
+                    check_noise(nz, spec.kind)
+            except Exception as e:  # the reference raises on the first observation
+                self._noise_error = self._noise_error or e
+            if spec.kind == "imu":
+                out = torch.zeros((n, 6), dtype=dt, device=dev)
+                rec = sensor_obs("imu", spec.noise, out)
+            elif spec.noise:
+                slot = self._sensor_slot[spec.name]
+                out = torch.zeros((n, cam.height, cam.width), dtype=dt, device=dev)
+                src = slot["depth"] if spec.kind == "depth" else slot["seg"]
+                rec = sensor_obs(spec.kind, spec.noise, out, src=src, width=cam.width, height=cam.height)
+            else:
+                continue
+            self._obs_sensors.append({"name": spec.name, "kind": spec.kind, "out": out, "rec": rec})
+        if self._obs_sensors:
+            arr = (nat.QbSensorObs * len(self._obs_sensors))(*[o["rec"] for o in self._obs_sensors])
+            self._obs_array = arr
         bufs = nat.QbEnvBuffers()
         bufs.n, bufs.ld, bufs.index_offset = n, n, self.index_offset
         bufs.dtype = nat.QB_F32 if dt == torch.float32 else nat.QB_F64
@@ -351,10 +376,9 @@ class QuadEnvBase:
             self._errors.zero_()
             raise SpawnFailure(f"{n} respawns found no spawn with clearance >= {self.config.min_spawn_clearance}")
 
-    def get_observation(self) -> Observations:
-        """Render every camera once and assemble the batched observation dict."""
-        obs = {"state": self._planes[0:13].T}
-        seg_keys = []
+    def _render_and_observe(self):
+        """Launch the observation kernels: K2 once per distinct camera, then
+        the sensor pass (IMU + noise chains) if any sensor needs it."""
         for slot in self._cams.values():
             cid = self._centroid_id(slot)
             if cid and slot["centroid"] is None:
@@ -363,10 +387,30 @@ class QuadEnvBase:
                 slot["centroid"] = torch.zeros((self.num_agents, 2), dtype=torch.float32, device=self.device)
             render_state(self.dev_scenes, slot["camera"], self._planes, env_scene=self.agent_scene, depth=slot["depth"],
                          seg=slot["seg"], centroid_id=cid, centroid=slot["centroid"] if cid else None)
-            for name, kind in slot["names"]:
-                obs[name] = slot["depth"] if kind == "depth" else slot["seg"]
-                if kind == "segmentation":
-                    seg_keys.append(name)
+        if self._obs_sensors:
+            import ctypes
+
+            nat.check(nat.lib().qb_env_observe(self._P, self._bufs, len(self._obs_sensors),
+                                               ctypes.cast(self._obs_array, ctypes.c_void_p), nat.stream_of()),
+                      "qb_env_observe")
+
+    def get_observation(self) -> Observations:
+        """Render every camera once, run the sensor pass and assemble the
+        batched observation dict."""
+        if self._noise_error is not None:
+            raise self._noise_error
+        self._render_and_observe()
+        obs = {"state": self._planes[0:13].T}
+        seg_keys = []
+        for spec, cam in self.sensor_cameras:
+            noisy = next((o for o in self._obs_sensors if o["name"] == spec.name), None)
+            if noisy is not None:
+                obs[spec.name] = noisy["out"]
+                continue
+            slot = self._sensor_slot[spec.name]
+            obs[spec.name] = slot["depth"] if spec.kind == "depth" else slot["seg"]
+            if spec.kind == "segmentation":
+                seg_keys.append(spec.name)
         self._extra_observations(obs)
         return Observations(obs, self.num_agents, seg_keys)
 
@@ -411,7 +455,4 @@ class QuadEnvBase:
     def _launch_step(self):
         nat.check(nat.lib().qb_env_step(self._P, self._kind, self._task, self.dev_scenes.handle, self._bufs,
                                         nat.stream_of()), "qb_env_step")
-        for slot in self._cams.values():
-            cid = self._centroid_id(slot)
-            render_state(self.dev_scenes, slot["camera"], self._planes, env_scene=self.agent_scene, depth=slot["depth"],
-                         seg=slot["seg"], centroid_id=cid, centroid=slot["centroid"] if cid else None)
+        self._render_and_observe()

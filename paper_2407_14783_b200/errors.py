@@ -60,3 +60,7 @@ class DegenerateAttitude(QuadsimError):
 
 class NativeError(QuadsimError):
     """The sm_100a library returned a non-zero status (qb_last_error())."""
+
+
+class InvalidNoiseForSensor(QuadsimError):
+    """Noise kind is not defined for the given sensor data type (errors.py:56-57)."""

@@ -155,3 +155,161 @@ def render_state(dev_scenes, camera: CameraModel, planes, env_scene=None, depth=
                                   nat.ptr(env_scene), nat.ptr(depth), nat.ptr(seg), int(centroid_id), nat.ptr(centroid),
                                   nat.ptr(extra), nat.ptr(extra_ids), k, nat.stream_of()), "qb_render")
     return depth, seg
+
+
+# ---------------------------------------------------------------------------
+# IMU (sensing.py:121-147)
+
+
+@dataclass
+class ImuReading:
+    specific_force_b: object  # (N, 3) accelerometer, gravity excluded
+    angvel_b: object  # (N, 3) gyro
+
+
+def body_wrench(state, params):
+    """Thrust + drag wrench at the current state (sensing.py:131-147), on the
+    state's device: thrusts k2 w^2 + k1 w + k0, drag -c v_B |v_B| with
+    v_B = R(q)^T v, force_z += t0 + t1 + t2 + t3, torque = sum_i t_i g_i."""
+    import torch
+
+    from .dynamics import Wrench
+
+    planes = state.planes.double()
+    k2, k1, k0 = params.thrust_coeffs
+    w = planes[13:17]
+    thr = k2 * w ** 2 + k1 * w + k0
+    q, v = planes[6:10], planes[3:6]
+    ux, uy, uz = -q[1], -q[2], -q[3]
+    tx, ty, tz = uy * v[2] - uz * v[1], uz * v[0] - ux * v[2], ux * v[1] - uy * v[0]
+    sx, sy, sz = uy * tz - uz * ty, uz * tx - ux * tz, ux * ty - uy * tx
+    vb = torch.stack([v[0] + 2.0 * (q[0] * tx + sx), v[1] + 2.0 * (q[0] * ty + sy), v[2] + 2.0 * (q[0] * tz + sz)])
+    c = torch.as_tensor(0.5 * params.air_density * np.asarray(params.drag_coeffs) * params.cross_area,
+                        dtype=torch.float64, device=planes.device)[:, None]
+    force = -c * vb * vb.abs()
+    force[2] += thr[0] + thr[1] + thr[2] + thr[3]
+    g = torch.as_tensor(np.asarray(params.torque_arms), dtype=torch.float64, device=planes.device)
+    torque = torch.stack([thr[0] * g[0, a] + thr[1] * g[1, a] + thr[2] * g[2, a] + thr[3] * g[3, a] for a in range(3)])
+    return Wrench(force.T, torque.T)
+
+
+def imu_read(state, wrench, params) -> ImuReading:
+    """Ideal IMU: specific force (f+d)/m in the body frame, gyro = body rates."""
+    return ImuReading(wrench.force_b / params.mass, state.planes[10:13].T.double().clone())
+
+
+# ---------------------------------------------------------------------------
+# Noise models (sensing.py:150-235).  apply_noise runs on the device with the
+# numpy Generator's own PCG64 state (read, advanced on the GPU, written back),
+# drawing exactly what numpy would: ziggurat standard normals, PTRS/mult
+# Poisson, next_double uniforms (csrc/qb_rng.cuh, qb_k_observe.cu).
+
+DEPTH_KINDS = {"normal", "poisson", "saltpepper", "speckle", "redwood"}
+IMAGE_KINDS = {"normal", "poisson", "saltpepper", "speckle"}
+IMU_KINDS = {"normal"}
+_SENSOR_KINDS = {"depth": DEPTH_KINDS, "rgb": IMAGE_KINDS, "segmentation": IMAGE_KINDS, "imu": IMU_KINDS}
+
+
+@dataclass(frozen=True)
+class NoiseSpec:
+    """One noise model attachment (sensing.py:165-192).
+
+    normal sigma (additive Gaussian), poisson scaling, saltpepper p,
+    speckle sigma (multiplicative), redwood sigma_disparity + quantization
+    (disparity domain, depth only)."""
+
+    kind: str
+    sigma: float = 0.0
+    p: float = 0.0
+    scaling: float = 1.0
+    sigma_disparity: float = 0.0
+    quantization: float = 0.0
+
+    def __post_init__(self):
+        object.__setattr__(self, "kind", self.kind.lower())
+        if self.kind not in DEPTH_KINDS:
+            raise ValueError(f"unknown noise kind {self.kind!r}")
+        if min(self.sigma, self.p, self.scaling, self.sigma_disparity, self.quantization) < 0:
+            raise ValueError("noise parameters must be nonnegative")
+        if not 0.0 <= self.p <= 1.0:
+            raise ValueError("saltpepper p must be in [0, 1]")
+
+    def native(self):
+        n = nat.QbNoise()
+        n.kind = nat.NOISE_KINDS[self.kind]
+        n.sigma, n.p, n.scaling = self.sigma, self.p, self.scaling
+        n.sigma_disparity, n.quantization = self.sigma_disparity, self.quantization
+        return n
+
+
+def check_noise(spec: NoiseSpec, sensor: str):
+    """The validity table of sensing.py:198-205."""
+    from .errors import InvalidNoiseForSensor
+
+    sensor = sensor.lower()
+    if sensor not in _SENSOR_KINDS:
+        raise InvalidNoiseForSensor(f"unknown sensor type {sensor!r}")
+    if spec.kind not in _SENSOR_KINDS[sensor]:
+        raise InvalidNoiseForSensor(f"noise {spec.kind!r} is not defined for {sensor!r} data")
+
+
+def sensor_obs(kind: str, noise, out, src=None, width: int = 1, height: int = 1):
+    """A qb_sensor_obs record (observation pass of one sensor)."""
+    so = nat.QbSensorObs()
+    so.kind = nat.SENSOR_KINDS["segmentation" if kind == "rgb" else kind]
+    if len(noise) > nat.QB_MAX_NOISE:
+        raise ValueError(f"at most {nat.QB_MAX_NOISE} noise models per sensor")
+    so.n_noise = len(noise)
+    for m, spec in enumerate(noise):
+        so.noise[m] = spec.native()
+    so.width, so.height = int(width), int(height)
+    so.src = nat.ptr(src)
+    so.out = nat.ptr(out)
+    return so
+
+
+def _pcg_words(bitgen):
+    st = bitgen.state
+    if st.get("bit_generator") != "PCG64":
+        raise TypeError("apply_noise needs a numpy Generator on a PCG64 bit generator")
+    s, inc = int(st["state"]["state"]), int(st["state"]["inc"])
+    m = (1 << 64) - 1
+    return [s >> 64, s & m, inc >> 64, inc & m]
+
+
+def apply_noise(data, spec: NoiseSpec, rng, sensor: str = "depth"):
+    """sensing.py:195-235 on the GPU, deterministic under (and advancing) the
+    numpy Generator's state: same draws, same values as the reference.
+    numpy in -> numpy float64 out; CUDA tensor in -> CUDA float64 tensor out."""
+    import torch
+
+    check_noise(spec, sensor)
+    host = not isinstance(data, torch.Tensor)
+    x = torch.as_tensor(np.asarray(data, dtype=float) if host else data, dtype=torch.float64)
+    x = x.to(device=torch.device("cuda", torch.cuda.current_device()) if host else x.device).contiguous()
+    out = torch.empty_like(x)
+    words = _pcg_words(rng.bit_generator)
+    rng_buf = torch.tensor([[w - (1 << 64) if w >= (1 << 63) else w for w in words]], dtype=torch.int64, device=x.device)
+    planes = torch.zeros((17, 1), dtype=torch.float64, device=x.device)
+    b = nat.QbEnvBuffers()
+    b.n, b.ld, b.index_offset, b.dtype = 1, 1, 0, nat.QB_F64
+    b.state, b.rng = planes.data_ptr(), rng_buf.data_ptr()
+    # values are already float: run the chain as a float-image pass over size x 1
+    so = sensor_obs("depth", (spec,), out, src=x, width=max(x.numel(), 1), height=1)
+    if x.numel():
+        from .params import native_params
+
+        with torch.cuda.device(x.device):
+            nat.check(nat.lib().qb_env_observe(native_params(), b, 1, ctypes_pointer(so), nat.stream_of()),
+                      "qb_env_observe")
+        w = [int(v) & ((1 << 64) - 1) for v in rng_buf[0].tolist()]
+        st = rng.bit_generator.state
+        st["state"]["state"] = (w[0] << 64) | w[1]
+        rng.bit_generator.state = st
+    return out.cpu().numpy() if host else out
+
+
+def ctypes_pointer(obj):
+    import ctypes
+
+    return ctypes.cast(ctypes.pointer(obj), ctypes.c_void_p)

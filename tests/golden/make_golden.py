@@ -344,8 +344,85 @@ def gen_rng():
     np.savez_compressed(os.path.join(OUT, "rng.npz"), **out)
 
 
+NOISE_CASES = [  # (sensor, kind, params)
+    ("depth", "normal", dict(sigma=0.05)), ("depth", "normal", dict(sigma=0.0)),
+    ("depth", "poisson", dict(scaling=10.0)), ("depth", "poisson", dict(scaling=250.0)),
+    ("depth", "saltpepper", dict(p=0.1)), ("depth", "speckle", dict(sigma=0.1)),
+    ("depth", "redwood", dict(sigma_disparity=0.01, quantization=0.05)), ("depth", "redwood", dict(sigma_disparity=0.02)),
+    ("segmentation", "normal", dict(sigma=0.5)), ("segmentation", "poisson", dict(scaling=1.0)),
+    ("segmentation", "saltpepper", dict(p=0.2)), ("segmentation", "speckle", dict(sigma=0.05)),
+    ("imu", "normal", dict(sigma=0.1)),
+]
+
+
+def gen_noise():
+    """sensing.apply_noise per (sensor, kind), IMU readings, and a noisy env episode."""
+    from quadsim.sensing import NoiseSpec
+
+    out = {}
+    rng = np.random.default_rng(77)
+    for c, (sensor, kind, kw) in enumerate(NOISE_CASES):
+        if sensor == "depth":
+            data = rng.uniform(0.3, 10.0, (16, 12))
+        elif sensor == "segmentation":
+            data = rng.integers(0, 12, (16, 12)).astype(float)
+        else:
+            data = rng.normal(size=6)
+        g = np.random.default_rng(100 + c)
+        res = sensing.apply_noise(data, NoiseSpec(kind, **kw), g, sensor=sensor)
+        out[f"case{c}_in"] = data
+        out[f"case{c}_out"] = res
+        out[f"case{c}_after"] = np.array(g.random(2))  # pins how many draws were consumed
+    # IMU: body_wrench + imu_read on random states
+    params = QuadParams()
+    states = random_states(rng, 32, params)
+    st = dyn.QuadState.from_vector(states)
+    reading = sensing.imu_read(st, sensing.body_wrench(st, params), params)
+    out["imu_states"] = states
+    out["imu_force"] = reading.specific_force_b
+    out["imu_gyro"] = reading.angvel_b
+    np.savez_compressed(os.path.join(OUT, "noise.npz"), **out)
+
+    # a noisy navigation episode: normal-distribution spawns (ziggurat in the
+    # spawn path), depth + segmentation + IMU sensors with noise chains
+    cfg = tasks.navigation_config(scene_seed=0, num_agents=6)
+    cfg = dataclasses.replace(
+        cfg, episode_max_steps=12, command_type="ctbr",  # CTBR: no trig in the controller -> FP64 bit-exact states
+        randomization=dataclasses.replace(cfg.randomization,
+                                          velocity=DistSpec("normal", mean=[0.2, 0.0, 0.0], sigma=[0.3, 0.3, 0.1])),
+        sensors=(SensorSpec(kind="depth", name="depth", noise=(NoiseSpec("normal", sigma=0.02),
+                                                             NoiseSpec("redwood", sigma_disparity=0.005))),
+                 SensorSpec(kind="imu", name="imu", noise=(NoiseSpec("normal", sigma=0.05),)),
+                 SensorSpec(kind="segmentation", name="vision", noise=(NoiseSpec("saltpepper", p=0.05),))))
+    env = tasks.make_env(cfg)
+
+    def lv(rng, t, n):  # CTBR: collective thrust + body rates
+        return np.concatenate([rng.uniform(6.0, 14.0, (n, 1)), rng.normal(scale=2.0, size=(n, 3))], axis=1)
+
+    rec = record_env(env, lv, 20, seed=4, keep_images=())
+    keep = (0, 1, 2, 12, 20)  # observation snapshots after reset (0) and after steps 1, 2, 12, 20
+    obs_log = {"depth": [], "imu": [], "vision": []}
+    env2 = tasks.make_env(cfg)
+    obs = env2.reset(seed=4)
+    r2 = np.random.default_rng(4 + 1000)
+    for key in obs_log:
+        obs_log[key].append(np.stack([o[key] for o in obs]))
+    for t in range(1, 21):
+        res = env2.step(ctl.command_from_array(cfg.command_type, lv(r2, t - 1, 6)))
+        if t in keep:
+            for key in obs_log:
+                obs_log[key].append(np.stack([o[key] for o in res.observations]))
+    rec.update({f"obs_{k}": np.array(v) for k, v in obs_log.items()})
+    rec["obs_steps"] = np.array(keep)
+    np.savez_compressed(os.path.join(OUT, "env_noise.npz"), **rec)
+
+
 if __name__ == "__main__":
     print("reference:", quadsim.__file__, "numpy", np.__version__)
+    if len(sys.argv) > 2 and sys.argv[2] == "noise":
+        gen_noise()
+        sys.exit(0)
+    gen_noise()
     gen_rng()
     gen_dynamics()
     gen_jacobian()

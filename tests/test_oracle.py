@@ -221,3 +221,75 @@ def test_pcg64_seeding_restatement():
         s, inc = seed_pcg(int(seed))
         w = [int(x) for x in g["pcg_state"][i]]
         assert s == (w[0] << 64 | w[1]) and inc == (w[2] << 64 | w[3])
+
+
+# ------------------------------------------------------------- F1: sensors
+def noise_config():
+    """The noisy navigation config make_golden.py records (env_noise.npz)."""
+    from paper_2407_14783_b200.env import DistSpec, NoiseSpec, SensorSpec, navigation_config
+
+    cfg = navigation_config(scene_seed=0, num_agents=6)
+    return dataclasses.replace(
+        cfg, episode_max_steps=12, command_type="ctbr",
+        randomization=dataclasses.replace(cfg.randomization,
+                                          velocity=DistSpec("normal", mean=[0.2, 0.0, 0.0], sigma=[0.3, 0.3, 0.1])),
+        sensors=(SensorSpec(kind="depth", name="depth", noise=(NoiseSpec("normal", sigma=0.02),
+                                                             NoiseSpec("redwood", sigma_disparity=0.005))),
+                 SensorSpec(kind="imu", name="imu", noise=(NoiseSpec("normal", sigma=0.05),)),
+                 SensorSpec(kind="segmentation", name="vision", noise=(NoiseSpec("saltpepper", p=0.05),))))
+
+
+NOISE_CASES = [
+    ("depth", "normal", dict(sigma=0.05)), ("depth", "normal", dict(sigma=0.0)),
+    ("depth", "poisson", dict(scaling=10.0)), ("depth", "poisson", dict(scaling=250.0)),
+    ("depth", "saltpepper", dict(p=0.1)), ("depth", "speckle", dict(sigma=0.1)),
+    ("depth", "redwood", dict(sigma_disparity=0.01, quantization=0.05)), ("depth", "redwood", dict(sigma_disparity=0.02)),
+    ("segmentation", "normal", dict(sigma=0.5)), ("segmentation", "poisson", dict(scaling=1.0)),
+    ("segmentation", "saltpepper", dict(p=0.2)), ("segmentation", "speckle", dict(sigma=0.05)),
+    ("imu", "normal", dict(sigma=0.1)),
+]
+
+
+@pytest.mark.parametrize("case", range(len(NOISE_CASES)))
+def test_apply_noise_bit_exact(case):
+    from oracle.env import apply_noise
+    from paper_2407_14783_b200.sensing import NoiseSpec
+
+    g = golden("noise")
+    sensor, kind, kw = NOISE_CASES[case]
+    rng = np.random.default_rng(100 + case)
+    out = apply_noise(g[f"case{case}_in"], NoiseSpec(kind, **kw), rng, sensor)
+    assert np.array_equal(out, g[f"case{case}_out"])
+    assert np.array_equal(rng.random(2), g[f"case{case}_after"])  # same number of draws consumed
+
+
+def test_imu_reading_bit_exact():
+    from oracle.env import imu_readings
+
+    g = golden("noise")
+    r = imu_readings(g["imu_states"], P())
+    assert np.array_equal(r[:, :3], g["imu_force"])
+    assert np.array_equal(r[:, 3:], g["imu_gyro"])
+
+
+def test_env_noise_replay():
+    """Normal-distribution spawns + depth/IMU/segmentation noise chains."""
+    g = golden("env_noise")
+    cfg = noise_config()
+    env = _replay("env_noise", cfg, 4, ["nav"])
+    # observation snapshots: replay again and compare the noisy observations
+    scenes = []
+    for spec in cfg.scenes:
+        t = spec.materialize().arrays
+        scenes.append(oracle.OracleScene(t.prim_type, t.prim_data, t.prim_object_id, t.prim_aabb_lo, t.prim_aabb_hi))
+    env = OracleEnv(cfg, scenes, QuadParams(), SimConfig(), ControllerGains())
+    obs = env.reset(seed=4)
+    keep = list(g["obs_steps"])
+    snaps = {0: obs}
+    for t in range(1, 21):
+        obs = env.step(g["actions"][t - 1])[0]
+        if t in keep:
+            snaps[t] = obs
+    for j, t in enumerate(keep):
+        for key in ("depth", "imu", "vision"):
+            assert np.array_equal(snaps[t][key], g[f"obs_{key}"][j]), (key, t)

@@ -3,7 +3,7 @@
 BASELINE.json metric: env-steps/s and 64x64 depth frames/s (whole box) at
 1/2/4/8 B200 vs the CPU reference.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c3|c1|c2|c4|c5] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c3|c1|c2|c4|c5|c3n] [--impl ours|reference]
   torchrun --nproc-per-node N bench.py --gpus N ...      (one rank per GPU, NCCL)
 
 Default workload = BASELINE config 3, the largest single-GPU config:
@@ -48,8 +48,10 @@ WORKLOADS = {
     "c3": "navigation, 64x64 depth+segmentation, 65536 envs/GPU (BASELINE config 3)",
     "c4": "BPTT through dynamics, 16384 envs/GPU, horizon 64, loss/grad all-reduce (BASELINE config 4)",
     "c5": "landing on a 5e5-triangle indoor mesh, 64x64 down depth+seg, 131072 envs/GPU (BASELINE config 5, 1M on 8 GPUs)",
+    "c3n": "config 3 + sensor noise (SURVEY F1): depth N(0, 0.02) -> Redwood, segmentation salt-and-pepper 2%, "
+           "IMU N(0, 0.05); 65536 envs/GPU",
 }
-ENVS = {"c1": 100, "c2": 100, "c3": 65536, "c4": 16384, "c5": 131072}
+ENVS = {"c1": 100, "c2": 100, "c3": 65536, "c4": 16384, "c5": 131072, "c3n": 65536}
 
 
 def peaks():
@@ -161,6 +163,17 @@ def env_workload(kind, rank, world, total):
         cfg = navigation_config(scene_seed=0, num_agents=total)
     elif kind == "c3":
         cfg = navigation_config(scene_seed=0, num_agents=total, with_segmentation=True)
+    elif kind == "c3n":
+        import dataclasses
+
+        from paper_2407_14783_b200.sensing import NoiseSpec
+
+        cfg = navigation_config(scene_seed=0, num_agents=total, with_segmentation=True)
+        cfg = dataclasses.replace(cfg, sensors=(
+            SensorSpec(kind="depth", name="depth", noise=(NoiseSpec("normal", sigma=0.02),
+                                                          NoiseSpec("redwood", sigma_disparity=0.002))),
+            SensorSpec(kind="segmentation", name="vision", noise=(NoiseSpec("saltpepper", p=0.02),)),
+            SensorSpec(kind="imu", name="imu", noise=(NoiseSpec("normal", sigma=0.05),))))
     elif kind == "c5":
         cfg = EnvConfig(num_agents=total, task="landing", command_type="lv", episode_max_steps=512,
                         scenes=(SceneSpec(kind="indoor", seed=0),),
@@ -192,7 +205,6 @@ def run_env(args, rank, world, kind):
     import torch
 
     import paper_2407_14783_b200._native as nat
-    from paper_2407_14783_b200.sensing import render_state
 
     total = ENVS[kind] * world
     env, cfg = env_workload(kind, rank, world, total)
@@ -216,12 +228,12 @@ def run_env(args, rank, world, kind):
         nat.check(nat.lib().qb_env_step(env._P, env._kind, env._task, env.dev_scenes.handle, env._bufs, nat.stream_of()))
         if events:
             events[1].record()
-        for slot in env._cams.values():
-            cid = env._centroid_id(slot)
-            render_state(env.dev_scenes, slot["camera"], env._planes, env_scene=env.agent_scene, depth=slot["depth"],
-                         seg=slot["seg"], centroid_id=cid, centroid=slot["centroid"] if cid else None)
+        env._render()
         if events:
             events[2].record()
+        env._observe()
+        if events:
+            events[3].record()
 
     def launch_graph(first):
         static_a.copy_(acts[first:first + G])  # stage the next G steps' actions (one device copy)
@@ -232,7 +244,7 @@ def run_env(args, rank, world, kind):
     if small:
         launch_graph(0)
     torch.cuda.synchronize()
-    ev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(3)) for _ in range(K)]
+    ev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(4)) for _ in range(K)]
     barrier(world)
     torch.cuda.synchronize()
     clk = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))
@@ -249,10 +261,13 @@ def run_env(args, rank, world, kind):
     torch.cuda.synchronize()
     clocks = clk.stop()
     ms = max_over_ranks(t0.elapsed_time(t1), world)
-    out = dict(env=env, cfg=cfg, n=n, total=total, ms=ms, clocks=clocks, launches=K * (1 + len(env._cams)), graph=small)
+    launches = K * (1 + len(env._cams) + (1 if env._obs_sensors else 0))
+    out = dict(env=env, cfg=cfg, n=n, total=total, ms=ms, clocks=clocks, launches=launches, graph=small)
     if not small:
-        out["step_ms"] = float(np.mean([a.elapsed_time(b) for a, b, _ in ev]))
-        out["render_ms"] = float(np.mean([b.elapsed_time(c) for _, b, c in ev]))
+        out["step_ms"] = float(np.mean([e[0].elapsed_time(e[1]) for e in ev]))
+        out["render_ms"] = float(np.mean([e[1].elapsed_time(e[2]) for e in ev]))
+        if env._obs_sensors:
+            out["observe_ms"] = float(np.mean([e[2].elapsed_time(e[3]) for e in ev]))
     if args.e2e:
         out["e2e"] = run_e2e(env, world, kind)
     return out
@@ -506,6 +521,8 @@ def main():
                                 "parallelism": f"env shards x{world}, no per-step collective"}})
         if "render_ms" in r:
             line["kernel_ms"] = {"env_step_k1k3": r["step_ms"], "render_k2": r["render_ms"]}
+            if "observe_ms" in r:
+                line["kernel_ms"]["observe_imu_noise"] = r["observe_ms"]
             px = r["n"] * 64 * 64
             nbytes = px * sum(4 for s in r["cfg"].sensors) + r["n"] * 40  # outputs + pose reads
             gbs = nbytes / (r["render_ms"] / 1e3) / 1e9

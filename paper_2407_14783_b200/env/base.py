@@ -379,6 +379,10 @@ class QuadEnvBase:
     def _render_and_observe(self):
         """Launch the observation kernels: K2 once per distinct camera, then
         the sensor pass (IMU + noise chains) if any sensor needs it."""
+        self._render()
+        self._observe()
+
+    def _render(self):
         for slot in self._cams.values():
             cid = self._centroid_id(slot)
             if cid and slot["centroid"] is None:
@@ -387,6 +391,8 @@ class QuadEnvBase:
                 slot["centroid"] = torch.zeros((self.num_agents, 2), dtype=torch.float32, device=self.device)
             render_state(self.dev_scenes, slot["camera"], self._planes, env_scene=self.agent_scene, depth=slot["depth"],
                          seg=slot["seg"], centroid_id=cid, centroid=slot["centroid"] if cid else None)
+
+    def _observe(self):
         if self._obs_sensors:
             import ctypes
 

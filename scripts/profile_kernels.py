@@ -5,7 +5,7 @@ import argparse
 import torch
 
 ap = argparse.ArgumentParser()
-ap.add_argument("mode", choices=["nav", "indoor", "dyn", "bptt", "hover"])
+ap.add_argument("mode", choices=["nav", "indoor", "dyn", "bptt", "hover", "noise"])
 ap.add_argument("--envs", type=int, default=16384)
 a = ap.parse_args()
 if a.mode in ("nav", "indoor"):
@@ -19,6 +19,16 @@ if a.mode in ("nav", "indoor"):
                         sensors=(SensorSpec(kind="depth", name="depth", orientation="down"),
                                  SensorSpec(kind="segmentation", name="vision", orientation="down")))
     env = make_env(cfg)
+    env.reset(seed=0)
+    act = torch.zeros((a.envs, 4), device="cuda")
+    act[:, 0] = 1.0
+    for _ in range(3):
+        env.step(LV(act[:, :3], act[:, 3]))
+elif a.mode == "noise":  # config 3 + the c3n sensor noise chains
+    import bench
+    from paper_2407_14783_b200.control import LV
+
+    env, _ = bench.env_workload("c3n", 0, 1, a.envs)
     env.reset(seed=0)
     act = torch.zeros((a.envs, 4), device="cuda")
     act[:, 0] = 1.0

@@ -36,7 +36,7 @@ extern "C" {
 
 enum qb_status { QB_OK = 0, QB_EINVAL = 1, QB_ECUDA = 2, QB_ENOMEM = 3, QB_EEMPTY = 4 };
 enum qb_dtype { QB_F32 = 0, QB_F64 = 1 };
-enum qb_task_kind { QB_TASK_FREE = 0, QB_TASK_NAVIGATION = 1, QB_TASK_LANDING = 2 };
+enum qb_task_kind { QB_TASK_FREE = 0, QB_TASK_NAVIGATION = 1, QB_TASK_LANDING = 2, QB_TASK_GAP_CROSSING = 3 };
 enum qb_dist_kind { QB_DIST_FIXED = 0, QB_DIST_UNIFORM = 1, QB_DIST_NORMAL = 2 };
 
 const char *qb_last_error(void);
@@ -131,10 +131,11 @@ typedef struct qb_camera {
  * env_scene (n) selects the scene of each env (NULL = scene 0).  When
  * centroid_id > 0, centroid (n,2) receives the (col,row) pixel centroid of
  * that id or (-1,-1) (tasks._id_centroid, tasks.py:121-128).  extra (n,K,4)
- * spheres + extra_ids (n,K): swarm agents (kernels.py:438-445). */
+ * spheres (x, y, z, r) in dtype + extra_ids (n,K): swarm agents
+ * (kernels.py:438-445), DEVICE. */
 int qb_render(const qb_scene *s, const qb_camera *cam, int32_t dtype, int64_t n, int64_t ld, const void *state,
               const int32_t *env_scene, void *depth, int32_t *seg, int32_t centroid_id, float *centroid,
-              const float *extra, const int32_t *extra_ids, int32_t n_extra, void *stream);
+              const void *extra, const int32_t *extra_ids, int32_t n_extra, void *stream);
 
 /* Same renderer from explicit camera poses (render_batch's own inputs):
  * origins (n,3), rotations (n,3,3) camera->world, in dtype. */
@@ -164,6 +165,14 @@ typedef struct qb_task {
     /* landing (tasks.py:78-118) */
     double pad_center[2];
     double pad_half, success_height, success_speed, w_height, w_speed_landing, w_collision, pad_top;
+    /* swarm mode (base.py:114-147, 214-232; one swarm = all n envs of the
+     * buffers, one scene): spawns clear of lower-index agents by
+     * 2 r + 0.1, pairwise collision at 2 r.  Gap crossing (tasks.py:131-174)
+     * reuses success_radius / w_progress / w_obstacle / safe_distance. */
+    int32_t swarm;
+    int32_t pad2_;
+    const double *targets; /* DEVICE (n,3) per-agent targets (gap crossing) */
+    double w_agent;
 } qb_task;
 
 typedef struct qb_env_buffers {
@@ -193,6 +202,14 @@ int qb_env_reset(const qb_params *p, const qb_task *task, const qb_scene *s, con
  * success + reward, terminated/truncated. */
 int qb_env_step(const qb_params *p, int32_t cmd_kind, const qb_task *task, const qb_scene *s, const qb_env_buffers *b,
                 void *stream);
+
+/* Swarm views for the observation (base.py:245-277, 306-309): for every
+ * agent i, the other agents j != i (ascending) as render spheres
+ * (x, y, z, collision_radius) in dtype (n, n-1, 4) with ids DRONE_ID0 + j
+ * (n, n-1), and their 13-component states (n, n-1, 13) in dtype.  Any output
+ * may be NULL. */
+int qb_env_swarm_views(const qb_task *task, const qb_env_buffers *b, void *spheres, int32_t *sphere_ids,
+                       void *swarm_obs, void *stream);
 
 /* Proximity refresh alone (base.py:214-224) on the current state. */
 int qb_env_refresh(const qb_task *task, const qb_scene *s, const qb_env_buffers *b, void *stream);

@@ -21,6 +21,7 @@ from . import (DOWNWARD, FORWARD, CMD_KINDS, OracleScene, camera_pose_world, com
                pack_params)
 
 PAD_ID = 9  # generate.py:15
+DRONE_ID0 = 60000  # base.py:34
 PAD_TOP = 0.02  # generate.py:91
 
 
@@ -122,8 +123,17 @@ class OracleEnv:
             self.w_speed = float(tp.get("w_speed", 0.5))
             self.w_collision = float(tp.get("w_collision", 1.0))
             self.seg_sensor = [s.name for s in config.sensors if s.kind == "segmentation"][-1]
+        elif self.task == "gap_crossing":  # tasks.py:134-149
+            default = [[3.5, -1.5 + 1.5 * i, 1.5] for i in range(config.num_agents)]
+            self.targets = np.asarray(tp.get("targets", default), float).reshape(config.num_agents, 3)
+            self.success_radius = float(tp.get("success_radius", 0.5))
+            self.w_progress = float(tp.get("w_progress", 10.0))
+            self.w_obstacle = float(tp.get("w_obstacle", 0.5))
+            self.w_agent = float(tp.get("w_agent", 0.5))
+            self.safe_distance = float(tp.get("safe_distance", 0.8))
         elif self.task != "free":
             raise NotImplementedError(self.task)
+        self.swarm = config.mode == "swarm"
         self.bounds = [(sc.bounds_lo - config.bounds_margin, sc.bounds_hi + config.bounds_margin) for sc in self.scenes]
         self.state = np.zeros((self.n, 17))
         self.agent_scene = np.zeros(self.n, int)
@@ -162,7 +172,7 @@ class OracleEnv:
 
     def _spawn(self, i):
         """base.py:114-147."""
-        self.agent_scene[i] = self.scene_perm[(i + self.reset_counts[i]) % len(self.scenes)]
+        self.agent_scene[i] = 0 if self.swarm else self.scene_perm[(i + self.reset_counts[i]) % len(self.scenes)]
         self.reset_counts[i] += 1
         rng = self.rngs[i]
         rand = self.config.randomization
@@ -173,6 +183,10 @@ class OracleEnv:
             _, d, _ = scene.nearest_point(cand[None])
             if d[0] < self.config.min_spawn_clearance:
                 continue
+            if self.swarm:  # base.py:141-146 _swarm_spawn_clear
+                min_sep = 2.0 * self.config.collision_radius + 0.1
+                if any(np.linalg.norm(self.state[j, 0:3] - cand) < min_sep for j in range(i)):
+                    continue
             pos = cand
             break
         if pos is None:
@@ -224,6 +238,13 @@ class OracleEnv:
             p = self.state[m, 0:3]
             self.oob[m] = ~(np.all(p >= lo, axis=1) & np.all(p <= hi, axis=1))
         self.collision = self.nearest_dist < self.config.collision_radius
+        if self.swarm and self.n > 1:  # base.py:225-232
+            pos = self.state[:, 0:3]
+            for i in range(self.n):
+                for j in range(i + 1, self.n):
+                    if np.linalg.norm(pos[i] - pos[j]) < 2.0 * self.config.collision_radius:
+                        self.collision[i] = True
+                        self.collision[j] = True
 
     # ----------------------------------------------------------------- tasks
     def _dist(self, x):
@@ -233,7 +254,13 @@ class OracleEnv:
     def _height(self):
         return np.maximum(self.state[:, 2] - PAD_TOP - self.config.collision_radius, 0.0)
 
+    def _gap_dist(self, x):  # tasks.py:151-153
+        d = x[:, 0:3] - self.targets
+        return np.sqrt(d[:, 0] ** 2 + d[:, 1] ** 2 + d[:, 2] ** 2)
+
     def get_success(self):
+        if self.task == "gap_crossing":  # tasks.py:155-156
+            return self._gap_dist(self.state) < self.success_radius
         if self.task == "navigation":  # tasks.py:49-50
             return self._dist(self.state) < self.success_radius
         if self.task == "landing":  # tasks.py:101-106
@@ -244,6 +271,16 @@ class OracleEnv:
         return np.zeros(self.n, bool)
 
     def get_reward(self):
+        if self.task == "gap_crossing":  # tasks.py:158-169
+            progress = self._gap_dist(self.prev_state) - self._gap_dist(self.state)
+            proximity = np.clip(1.0 - self.nearest_dist / self.safe_distance, 0.0, 1.0)
+            reward = self.w_progress * progress - self.w_obstacle * proximity
+            if self.n > 1:
+                pos = self.state[:, 0:3]
+                for i in range(self.n):
+                    dmin = min(np.linalg.norm(pos[i] - pos[j]) for j in range(self.n) if j != i)
+                    reward[i] -= self.w_agent * max(0.0, 1.0 - dmin / self.safe_distance)
+            return reward
         if self.task == "navigation":  # tasks.py:52-56
             progress = self._dist(self.prev_state) - self._dist(self.state)
             speed2 = (self.state[:, 3:6] ** 2).sum(axis=1)
@@ -266,7 +303,16 @@ class OracleEnv:
         for s in np.unique(self.agent_scene):
             m = np.nonzero(self.agent_scene == s)[0]
             o, r = camera_pose_world(self.state[m, 0:3], self.state[m, 6:10], rot, sensor.translation)
-            d, i = self.scenes[s].render(o, r, W, H, th, tv, sensor.max_range)
+            extra = ids = None
+            if self.swarm and self.n > 1:  # base.py:245-255, 268-272
+                extra = np.empty((len(m), self.n - 1, 4))
+                ids = np.empty((len(m), self.n - 1), np.int64)
+                for k, a in enumerate(m):
+                    others = [j for j in range(self.n) if j != a]
+                    extra[k, :, 0:3] = self.state[others, 0:3]
+                    extra[k, :, 3] = self.config.collision_radius
+                    ids[k] = DRONE_ID0 + np.array(others)
+            d, i = self.scenes[s].render(o, r, W, H, th, tv, sensor.max_range, extra, ids)
             depth[m] = d
             seg[m] = i
         return depth, seg
@@ -291,8 +337,12 @@ class OracleEnv:
                         img[i] = apply_noise(img[i], nz, self.rngs[i], sensor.kind)
             obs[sensor.name] = img
             self.seg_cache[sensor.name] = seg
+        if self.swarm and self.n > 1:  # base.py:306-309
+            obs["swarm"] = np.stack([self.state[[j for j in range(self.n) if j != i], 0:13] for i in range(self.n)])
         if self.task == "navigation":
             obs["target"] = np.broadcast_to(self.target, (self.n, 3)).copy()
+        elif self.task == "gap_crossing":  # tasks.py:171-174
+            obs["target"] = self.targets.copy()
         elif self.task == "landing":  # tasks.py:121-128
             seg = self.seg_cache[self.seg_sensor]
             tgt = np.full((self.n, 2), -1.0)

@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(_HERE, "libquadb200.so")
 
 QB_F32, QB_F64 = 0, 1
 CMD = {"srt": 0, "ctbr": 1, "ps": 2, "lv": 3, "rotor": 4}
-TASKS = {"free": 0, "navigation": 1, "landing": 2}
+TASKS = {"free": 0, "navigation": 1, "landing": 2, "gap_crossing": 3}
 DISTS = {"fixed": 0, "uniform": 1, "normal": 2}
 
 c_double3 = ctypes.c_double * 3
@@ -98,6 +98,10 @@ class QbTask(ctypes.Structure):
         ("w_speed_landing", ctypes.c_double),
         ("w_collision", ctypes.c_double),
         ("pad_top", ctypes.c_double),
+        ("swarm", ctypes.c_int32),
+        ("pad2_", ctypes.c_int32),
+        ("targets", ctypes.c_void_p),
+        ("w_agent", ctypes.c_double),
     ]
 
 
@@ -184,6 +188,7 @@ SIGNATURES = {
     "qb_env_reset": ([_PP(QbParams), _PP(QbTask), _P, _PP(QbEnvBuffers), _U64, _P], ctypes.c_int),
     "qb_env_step": ([_PP(QbParams), _I32, _PP(QbTask), _P, _PP(QbEnvBuffers), _P], ctypes.c_int),
     "qb_env_refresh": ([_PP(QbTask), _P, _PP(QbEnvBuffers), _P], ctypes.c_int),
+    "qb_env_swarm_views": ([_PP(QbTask), _PP(QbEnvBuffers), _P, _P, _P, _P], ctypes.c_int),
     "qb_rng_seed": ([_U64, _I64, _P, _P], ctypes.c_int),
     "qb_rng_doubles": ([_I64, _P, _I32, _P, _P], ctypes.c_int),
     "qb_rng_normals": ([_I64, _P, _I32, _P, _P], ctypes.c_int),

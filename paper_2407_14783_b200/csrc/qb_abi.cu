@@ -471,7 +471,7 @@ static int check_cam(const qb_camera *cam) {
 
 int qb_render(const qb_scene *s, const qb_camera *cam, int32_t dtype, int64_t n, int64_t ld, const void *state,
               const int32_t *env_scene, void *depth, int32_t *seg, int32_t centroid_id, float *centroid,
-              const float *extra, const int32_t *extra_ids, int32_t n_extra, void *stream) {
+              const void *extra, const int32_t *extra_ids, int32_t n_extra, void *stream) {
     QB_REQUIRE(s && state && n >= 0 && ld >= n, "qb_render: bad arguments");
     int rc = check_cam(cam);
     if (rc) return rc;
@@ -501,7 +501,11 @@ static int check_env(const qb_task *task, const qb_scene *s, const qb_env_buffer
                    b->nearest_dist && b->nearest_pt && b->rng && b->error_count,
                "env: a required buffer is NULL");
     QB_REQUIRE(task->scene_perm && task->n_scene_perm >= 1, "env: scene_perm missing");
-    QB_REQUIRE(task->task >= 0 && task->task <= 2, "env: unknown task %d", task->task);
+    QB_REQUIRE(task->task >= 0 && task->task <= 3, "env: unknown task %d", task->task);
+    QB_REQUIRE(task->task != QB_TASK_GAP_CROSSING || (task->swarm && task->targets),
+               "env: gap crossing needs swarm mode and targets");
+    QB_REQUIRE(!task->swarm || (b->prev_state && task->n_scene_perm == 1),
+               "env: swarm mode needs prev_state tracking and exactly one scene");
     return QB_OK;
 }
 
@@ -532,6 +536,13 @@ int qb_env_refresh(const qb_task *task, const qb_scene *s, const qb_env_buffers 
     for (int k = 0; k < 3; ++k) dummy.inertia[k] = 1.0;
     dummy.thrust_coeffs[0] = 1.0;
     return qb::launch_env(2, &dummy, 0, task, s, b, 0, qb::as_stream(stream));
+}
+
+int qb_env_swarm_views(const qb_task *task, const qb_env_buffers *b, void *spheres, int32_t *sphere_ids,
+                       void *swarm_obs, void *stream) {
+    QB_REQUIRE(task && b && b->state, "qb_env_swarm_views: NULL argument");
+    QB_REQUIRE(b->dtype == QB_F32 || b->dtype == QB_F64, "qb_env_swarm_views: bad dtype %d", b->dtype);
+    return qb::launch_swarm_views(task, b, spheres, sphere_ids, swarm_obs, qb::as_stream(stream));
 }
 
 int qb_env_observe(const qb_params *p, const qb_env_buffers *b, int32_t n_sensors, const qb_sensor_obs *sensors,

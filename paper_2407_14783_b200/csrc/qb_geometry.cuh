@@ -307,6 +307,22 @@ QB_D float rcp_approx(float x) {
     return r;
 }
 
+// sphere (centre a.xyz, r^2 = r2) from registers: swarm agents in the epilogue
+QB_D float ray_sphere_v(float4 a, float r2, float ox, float oy, float oz, float dx, float dy, float dz, float tmin,
+                        float tmax) {
+    float mx = ox - a.x, my = oy - a.y, mz = oz - a.z;
+    float bb = mx * dx + my * dy + mz * dz;
+    float fx = mx - bb * dx, fy = my - bb * dy, fz = mz - bb * dz;
+    float disc = r2 - (fx * fx + fy * fy + fz * fz);
+    if (disc < 0.0f) return -1.0f;
+    float s = sqrtf(disc);
+    float t = -bb - s;
+    if (t > tmin && t <= tmax) return t;
+    t = -bb + s;
+    if (t > tmin && t <= tmax) return t;
+    return -1.0f;
+}
+
 QB_D float ray_sphere_f(const float4 *p, float ox, float oy, float oz, float dx, float dy, float dz, float tmin, float tmax) {
     float4 a = __ldg(p), b = __ldg(p + 1);
     float mx = ox - a.x, my = oy - a.y, mz = oz - a.z;

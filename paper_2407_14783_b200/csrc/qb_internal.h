@@ -61,7 +61,7 @@ int launch_vjp(const qb_params *p, int kind, int dtype, long long n, long long l
                double *action_grad_sum, cudaStream_t st);
 int launch_render(const qb_scene *s, const qb_camera *cam, int dtype, long long n, long long ld, const void *state,
                   const void *origins, const void *rotations, const int32_t *env_scene, void *depth, int32_t *seg,
-                  int32_t centroid_id, float *centroid, const float *extra, const int32_t *extra_ids, int n_extra,
+                  int32_t centroid_id, float *centroid, const void *extra, const int32_t *extra_ids, int n_extra,
                   cudaStream_t st);
 int launch_nearest(const qb_scene *s, const int32_t *env_scene, long long n, const double *q, double *pt, double *dist,
                    int32_t *oid, cudaStream_t st);
@@ -69,6 +69,8 @@ int launch_raycast(const qb_scene *s, int dtype, const int32_t *env_scene, long 
                    double tmin, double tmax, void *t, int32_t *oid, cudaStream_t st);
 int launch_env(int mode, const qb_params *p, int kind, const qb_task *task, const qb_scene *s, const qb_env_buffers *b,
                uint64_t seed, cudaStream_t st);
+int launch_swarm_views(const qb_task *task, const qb_env_buffers *b, void *spheres, int32_t *ids, void *obs,
+                       cudaStream_t st);
 int launch_rng_seed(uint64_t seed, long long n, uint64_t *out, cudaStream_t st);
 int launch_rng_doubles(long long n, uint64_t *rng, int k, double *out, cudaStream_t st);
 int launch_rng_normals(long long n, uint64_t *rng, int k, double *out, cudaStream_t st);

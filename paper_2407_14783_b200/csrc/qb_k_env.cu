@@ -70,9 +70,29 @@ template <bool WARP> __device__ __forceinline__ NearestResult nearest_q(const De
         return nearest_point(S, scene, q[0], q[1], q[2]);
 }
 
+__device__ __forceinline__ xd norm3(xd a, xd b, xd c) { return r_sqrt(a * a + b * b + c * c); }
+
+// base.py:141-146 _swarm_spawn_clear: candidate at least 2 r + 0.1 from every
+// lower-index agent (their current positions); warp-parallel over j
+template <class R>
+__device__ bool swarm_spawn_clear(const EnvArgs<R> &A, long long i, const double *cand) {
+    using S = typename storage_of<R>::type;
+    const S *st = static_cast<const S *>(A.B.state);
+    const xd min_sep = xd(2.0) * xd(A.T.collision_radius) + xd(0.1);
+    bool close = false;
+    for (long long j = threadIdx.x & 31; j < i; j += 32) {
+        const xd d = norm3(xd((double)st[0 * A.B.ld + j]) - xd(cand[0]), xd((double)st[1 * A.B.ld + j]) - xd(cand[1]),
+                           xd((double)st[2 * A.B.ld + j]) - xd(cand[2]));
+        close |= d < min_sep;
+    }
+    return !__any_sync(0xffffffffu, close);
+}
+
 // base.py:114-147 for env i (shard-local index); returns false on SpawnFailure.
 // WARP: all 32 lanes run it on the same env (same draws); `lead` writes.
-template <class R, bool WARP> __device__ bool spawn(const EnvArgs<R> &A, long long i, R *x, bool lead) {
+// SWARM (warp only): also clear of the lower-index agents.
+template <class R, bool WARP, bool SWARM = false>
+__device__ bool spawn(const EnvArgs<R> &A, long long i, R *x, bool lead) {
     const qb_task &T = A.T;
     const qb_env_buffers &B = A.B;
     const long long gi = B.index_offset + i;
@@ -90,6 +110,9 @@ template <class R, bool WARP> __device__ bool spawn(const EnvArgs<R> &A, long lo
         sample_dist(T.spawn[0], r, pos);
         NearestResult nr = nearest_q<WARP>(A.S, scene, pos);
         if (__dsqrt_rn(nr.d2) < T.min_spawn_clearance) continue;
+        if constexpr (SWARM) {
+            if (!swarm_spawn_clear(A, i, pos)) continue;
+        }
         found = true;
         break;
     }
@@ -140,8 +163,6 @@ template <class R, bool WARP> __device__ __forceinline__ Proximity proximity(con
     out.oob = !inside;
     return out;
 }
-
-__device__ __forceinline__ xd norm3(xd a, xd b, xd c) { return r_sqrt(a * a + b * b + c * c); }
 
 // tasks.py:45-56 (navigation), 97-111 (landing); free: zero reward, no success
 __device__ __forceinline__ void task_eval(const qb_task &T, const double *pp, const double *p, const double *v, double nd,
@@ -210,14 +231,14 @@ template <class R, bool WARP> __global__ void __launch_bounds__(128) k_env_reset
     const qb_env_buffers &B = A.B;
     if (i >= B.n) return;
     R x[17];
-    if (mode == 0) {
+    if (mode == 0 || mode == 3) {
         if (lead) {
             pcg_store(B.rng + 4 * i, pcg64_from_seed(seed + (uint64_t)(B.index_offset + i)));
             B.reset_count[i] = 0;
         }
         if (WARP) __syncwarp();
         hover_state(A.C, x);
-        spawn<R, WARP>(A, i, x, lead);
+        if (mode == 0) spawn<R, WARP>(A, i, x, lead);
         if (lead) {
             store_planes(B.state, B.ld, i, x);
             if (B.prev_state) store_planes(B.prev_state, B.ld, i, x);
@@ -232,8 +253,100 @@ template <class R, bool WARP> __global__ void __launch_bounds__(128) k_env_reset
     } else {
         load_state(A, i, x);
     }
+    if (mode == 3) return;  // swarm reset: spawns and proximity follow
     const Proximity pr = proximity<R, WARP>(A, B.agent_scene[i], x);
     if (lead) write_post(A, i, pr);
+}
+
+// Swarm mode (one swarm = all envs of the buffers).  Spawns are sequential
+// in agent order (base.py:101-102, 169-172): agent i must clear the agents
+// j < i at their current positions, so one warp walks the agents, each spawn
+// warp-parallel (nearest point over the scene, clearance over j < i).
+template <class R> __global__ void __launch_bounds__(32) k_swarm_spawn(EnvArgs<R> A, int all) {
+    const qb_env_buffers &B = A.B;
+    const bool lead = threadIdx.x == 0;
+    for (long long i = 0; i < B.n; ++i) {
+        if (!all && !(A.T.auto_reset && B.needs_respawn[i])) continue;
+        R x[17];
+        hover_state(A.C, x);
+        spawn<R, true, true>(A, i, x, lead);
+        if (lead) {
+            store_planes(B.state, B.ld, i, x);
+            if (all && B.prev_state) store_planes(B.prev_state, B.ld, i, x);
+            B.needs_respawn[i] = 0;
+        }
+        __syncwarp();
+    }
+}
+
+// base.py:225-232 pairwise collision (d < 2 r), then -- after a step -- the
+// task hooks and termination flags on the final collision flags; gap
+// crossing (tasks.py:131-165) adds the nearest-agent penalty.
+template <class R> __global__ void __launch_bounds__(128) k_swarm_post(EnvArgs<R> A, int after_step) {
+    using S = typename storage_of<R>::type;
+    const qb_env_buffers &B = A.B;
+    const qb_task &T = A.T;
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= B.n) return;
+    const S *st = static_cast<const S *>(B.state);
+    const double p[3] = {(double)st[i], (double)st[B.ld + i], (double)st[2 * B.ld + i]};
+    const xd two_r = xd(2.0) * xd(T.collision_radius);
+    bool hit = false;
+    double dmin = infinity_d();
+    for (long long j = 0; j < B.n; ++j) {
+        if (j == i) continue;
+        const xd d = norm3(xd(p[0]) - xd((double)st[j]), xd(p[1]) - xd((double)st[B.ld + j]),
+                           xd(p[2]) - xd((double)st[2 * B.ld + j]));
+        hit |= d < two_r;
+        dmin = fmin(dmin, d.v);
+    }
+    const bool collision = B.collision[i] || hit;
+    B.collision[i] = collision;
+    if (!after_step) return;
+    const S *ps = static_cast<const S *>(B.prev_state);
+    const double pp[3] = {(double)ps[i], (double)ps[B.ld + i], (double)ps[2 * B.ld + i]};
+    const double v[3] = {(double)st[3 * B.ld + i], (double)st[4 * B.ld + i], (double)st[5 * B.ld + i]};
+    bool success;
+    double reward;
+    if (T.task == QB_TASK_GAP_CROSSING) {
+        const double *tg = T.targets + 3 * i;
+        const xd dc = norm3(xd(p[0]) - xd(tg[0]), xd(p[1]) - xd(tg[1]), xd(p[2]) - xd(tg[2]));
+        const xd dp = norm3(xd(pp[0]) - xd(tg[0]), xd(pp[1]) - xd(tg[1]), xd(pp[2]) - xd(tg[2]));
+        success = dc < xd(T.success_radius);
+        const xd prox = np_clip(xd(1.0) - xd(B.nearest_dist[i]) / xd(T.safe_distance), xd(0.0), xd(1.0));
+        xd rw = xd(T.w_progress) * (dp - dc) - xd(T.w_obstacle) * prox;
+        if (B.n > 1) rw = rw - xd(T.w_agent) * py_max(xd(0.0), xd(1.0) - xd(dmin) / xd(T.safe_distance));
+        reward = rw.v;
+    } else {
+        task_eval(T, pp, p, v, B.nearest_dist[i], collision, success, reward);
+    }
+    const bool terminated = success || collision || B.out_of_bounds[i] || B.nonfinite[i];
+    const bool truncated = !terminated && B.step_count[i] >= T.episode_max_steps;
+    B.success[i] = success;
+    B.reward[i] = (float)reward;
+    B.terminated[i] = terminated;
+    B.truncated[i] = truncated;
+    B.needs_respawn[i] = terminated || truncated;
+}
+
+// base.py:245-277, 306-309: other agents as render spheres and swarm states
+template <class R>
+__global__ void k_swarm_views(EnvArgs<R> A, typename storage_of<R>::type *spheres, int32_t *ids,
+                              typename storage_of<R>::type *obs) {
+    using S = typename storage_of<R>::type;
+    const qb_env_buffers &B = A.B;
+    const long long m = B.n - 1;
+    const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (m <= 0 || idx >= B.n * m) return;
+    const long long i = idx / m, k = idx % m, j = k < i ? k : k + 1;
+    const S *st = static_cast<const S *>(B.state);
+    if (spheres) {
+        for (int c = 0; c < 3; ++c) spheres[idx * 4 + c] = st[c * B.ld + j];
+        spheres[idx * 4 + 3] = (S)A.T.collision_radius;
+    }
+    if (ids) ids[idx] = 60000 + (int32_t)(B.index_offset + j);  // DRONE_ID0 + j (base.py:23)
+    if (obs)
+        for (int c = 0; c < 13; ++c) obs[idx * 13 + c] = st[c * B.ld + j];
 }
 
 template <class R, int KIND, bool WARP> __global__ void __launch_bounds__(128) k_env_step(EnvArgs<R> A) {
@@ -245,7 +358,7 @@ template <class R, int KIND, bool WARP> __global__ void __launch_bounds__(128) k
     if (i >= B.n) return;
     R x[17];
     load_state(A, i, x);
-    if (T.auto_reset && B.needs_respawn[i]) spawn<R, WARP>(A, i, x, lead);
+    if (T.auto_reset && B.needs_respawn[i] && !T.swarm) spawn<R, WARP>(A, i, x, lead);
     R prev[17];
 #pragma unroll
     for (int k = 0; k < 17; ++k) prev[k] = x[k];
@@ -312,13 +425,24 @@ int dispatch_env(int mode, const qb_params *p, int kind, const qb_task *task, co
     // that still fits one wave of the machine
     const bool warp = b->n * 32 <= (long long)qb::sm_count() * 2048;
     dim3 g(qb::env_grid(warp ? b->n * 32 : b->n, BS));
-    if (mode == 0 || mode == 2) {
+    const bool swarm = task->swarm != 0;
+    const dim3 gp(qb::env_grid(b->n, BS));
+    auto reset_kernel = [&](int m) {
         if (warp)
-            k_env_reset<R, true><<<g, BS, 0, st>>>(A, seed, mode == 0 ? 0 : 1);
+            k_env_reset<R, true><<<g, BS, 0, st>>>(A, seed, m);
         else
-            k_env_reset<R, false><<<g, BS, 0, st>>>(A, seed, mode == 0 ? 0 : 1);
+            k_env_reset<R, false><<<g, BS, 0, st>>>(A, seed, m);
+    };
+    if (mode == 0 || mode == 2) {
+        if (swarm && mode == 0) {  // init streams / flags, then spawn in agent order
+            reset_kernel(3);
+            k_swarm_spawn<R><<<1, 32, 0, st>>>(A, 1);
+        }
+        reset_kernel(mode == 0 && !swarm ? 0 : 1);
+        if (swarm) k_swarm_post<R><<<gp, BS, 0, st>>>(A, 0);
         return qb::check_launch("env_reset");
     }
+    if (swarm && task->auto_reset) k_swarm_spawn<R><<<1, 32, 0, st>>>(A, 0);
 #define QB_ENV(K) (warp ? (k_env_step<R, K, true><<<g, BS, 0, st>>>(A), 0) : (k_env_step<R, K, false><<<g, BS, 0, st>>>(A), 0))
     switch (kind) {
         case QB_CMD_SRT: QB_ENV(QB_CMD_SRT); break;
@@ -329,13 +453,34 @@ int dispatch_env(int mode, const qb_params *p, int kind, const qb_task *task, co
         default: qb::set_error("unknown command kind %d", kind); return QB_EINVAL;
     }
 #undef QB_ENV
+    if (swarm) k_swarm_post<R><<<gp, BS, 0, st>>>(A, 1);
     return qb::check_launch("env_step");
+}
+
+template <class R> int dispatch_views(const qb_task *task, const qb_env_buffers *b, void *spheres, int32_t *ids, void *obs,
+                                      cudaStream_t st) {
+    using S = typename storage_of<R>::type;
+    EnvArgs<R> A;
+    A.T = *task;
+    A.B = *b;
+    const long long m = b->n - 1;
+    if (m <= 0) return QB_OK;
+    k_swarm_views<R><<<qb::env_grid(b->n * m, 128), 128, 0, st>>>(A, static_cast<S *>(spheres), ids,
+                                                                 static_cast<S *>(obs));
+    return qb::check_launch("env_swarm_views");
 }
 
 }  // namespace
 
 namespace qb {
 // mode 0 reset, 1 step, 2 refresh
+int launch_swarm_views(const qb_task *task, const qb_env_buffers *b, void *spheres, int32_t *ids, void *obs,
+                       cudaStream_t st) {
+    if (b->n == 0) return QB_OK;
+    if (b->dtype == QB_F32) return dispatch_views<float>(task, b, spheres, ids, obs, st);
+    return dispatch_views<xd>(task, b, spheres, ids, obs, st);
+}
+
 int launch_env(int mode, const qb_params *p, int kind, const qb_task *task, const qb_scene *s, const qb_env_buffers *b,
                uint64_t seed, cudaStream_t st) {
     if (b->n == 0) return QB_OK;

@@ -366,8 +366,7 @@ __global__ void __launch_bounds__(QB_RF_BLOCK, QB_RF_MINB) k_render_f(DevScene S
             if (n_extra > 0) {  // swarm agents as spheres (kernels.py:438-445)
                 for (int k = 0; k < n_extra; ++k) {
                     const float4 sph = *reinterpret_cast<const float4 *>(extra + (c * n_extra + k) * 4);
-                    float4 rec[2] = {sph, make_float4(sph.w * sph.w, 0.f, 0.f, 0.f)};
-                    float ts = ray_sphere_f(rec, o[0], o[1], o[2], dx, dy, dz, tmin, tmax);
+                    float ts = ray_sphere_v(sph, sph.w * sph.w, o[0], o[1], o[2], dx, dy, dz, tmin, tmax);
                     if (ts > 0.0f && (t < 0.0f || ts < t)) {
                         t = ts;
                         oid = extra_ids[c * n_extra + k];
@@ -735,8 +734,7 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, 6)
                 int oid = hit ? bid[u] : -1;
                 for (int k = 0; k < n_extra; ++k) {  // swarm agents as spheres (kernels.py:438-445)
                     const float4 sph = *reinterpret_cast<const float4 *>(extra + (c * n_extra + k) * 4);
-                    float4 rec2[2] = {sph, make_float4(sph.w * sph.w, 0.f, 0.f, 0.f)};
-                    float ts = ray_sphere_f(rec2, o[0], o[1], o[2], dx[u], dy[u], dz[u], tmin, tmx[u]);
+                    float ts = ray_sphere_v(sph, sph.w * sph.w, o[0], o[1], o[2], dx[u], dy[u], dz[u], tmin, tmx[u]);
                     if (ts > 0.0f && (t < 0.0f || ts < t)) {
                         t = ts;
                         oid = extra_ids[c * n_extra + k];
@@ -776,7 +774,8 @@ template <bool FROM_STATE>
 __global__ void __launch_bounds__(128) k_render_x(DevScene S, CamD cam, long long n, long long ld, const double *state,
                                                   const double *origins, const double *rotations,
                                                   const int32_t *env_scene, double *depth, int32_t *seg,
-                                                  int centroid_id, float *centroid) {
+                                                  int centroid_id, float *centroid, const double *extra,
+                                                  const int32_t *extra_ids, int n_extra) {
     const long long pix = (long long)cam.W * cam.H;
     const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (gid >= n * pix) return;
@@ -806,6 +805,15 @@ __global__ void __launch_bounds__(128) k_render_x(DevScene S, CamD cam, long lon
     xd tmax = xd(cam.max_range) / cz;
     int oid;
     double t = raycast_x(S, env_scene ? env_scene[c] : 0, o[0].v, o[1].v, o[2].v, dx.v, dy.v, dz.v, 1e-9, tmax.v, oid);
+    for (int k = 0; k < n_extra; ++k) {  // swarm agents as spheres (kernels.py:438-445)
+        const double *sp = extra + (c * n_extra + k) * 4;
+        const xd ts = ray_sphere_ref<xd>(xd(sp[0]), xd(sp[1]), xd(sp[2]), xd(sp[3]), o[0], o[1], o[2], dx, dy, dz,
+                                         xd(1e-9), tmax);
+        if (ts.v > 0.0 && (t < 0.0 || ts.v < t)) {
+            t = ts.v;
+            oid = extra_ids[c * n_extra + k];
+        }
+    }
     const long long off = c * pix + (long long)i * cam.W + j;
     if (depth) depth[off] = t > 0.0 ? (xd(t) * cz).v : cam.max_range;
     if (seg) seg[off] = t > 0.0 ? oid : 0;
@@ -865,7 +873,7 @@ namespace qb {
 
 int launch_render(const qb_scene *s, const qb_camera *cam, int dtype, long long n, long long ld, const void *state,
                   const void *origins, const void *rotations, const int32_t *env_scene, void *depth, int32_t *seg,
-                  int32_t centroid_id, float *centroid, const float *extra, const int32_t *extra_ids, int n_extra,
+                  int32_t centroid_id, float *centroid, const void *extra, const int32_t *extra_ids, int n_extra,
                   cudaStream_t st) {
     if (n == 0) return QB_OK;
     if (dtype == QB_F32) {
@@ -896,8 +904,8 @@ int launch_render(const qb_scene *s, const qb_camera *cam, int dtype, long long 
             if (blocks > max_blocks) blocks = max_blocks;
             if (state)
                 k_render_cull<true><<<(int)blocks, B, 0, st>>>(s->dev, c, n, ld, (const float *)state, nullptr, nullptr,
-                                                               env_scene, (float *)depth, seg, centroid_id, centroid, extra,
-                                                               extra_ids, n_extra, split);
+                                                               env_scene, (float *)depth, seg, centroid_id, centroid,
+                                                               (const float *)extra, extra_ids, n_extra, split);
             else
                 k_render_cull<false><<<(int)blocks, B, 0, st>>>(s->dev, c, n, ld, nullptr, (const float *)origins,
                                                                 (const float *)rotations, env_scene, (float *)depth, seg, 0,
@@ -912,7 +920,8 @@ int launch_render(const qb_scene *s, const qb_camera *cam, int dtype, long long 
         if (blocks > 0x7fffffffLL) blocks = 0x7fffffffLL;  // grid-stride loop covers the rest
         if (state)
             k_render_f<true><<<(int)blocks, B, 0, st>>>(s->dev, c, n, ld, (const float *)state, nullptr, nullptr, env_scene,
-                                                        (float *)depth, seg, centroid_id, centroid, extra, extra_ids, n_extra);
+                                                        (float *)depth, seg, centroid_id, centroid, (const float *)extra,
+                                                        extra_ids, n_extra);
         else
             k_render_f<false><<<(int)blocks, B, 0, st>>>(s->dev, c, n, ld, nullptr, (const float *)origins,
                                                          (const float *)rotations, env_scene, (float *)depth, seg, 0, nullptr,
@@ -930,16 +939,14 @@ int launch_render(const qb_scene *s, const qb_camera *cam, int dtype, long long 
     long long total = n * (long long)c.W * c.H;
     const int B = 128;
     int blocks = (int)((total + B - 1) / B);
-    if (n_extra > 0) {
-        set_error("extra spheres are only supported by the FP32 renderer");
-        return QB_EINVAL;
-    }
     if (state)
         k_render_x<true><<<blocks, B, 0, st>>>(s->dev, c, n, ld, (const double *)state, nullptr, nullptr, env_scene,
-                                              (double *)depth, seg, centroid_id, centroid);
+                                              (double *)depth, seg, centroid_id, centroid, (const double *)extra,
+                                              extra_ids, n_extra);
     else
         k_render_x<false><<<blocks, B, 0, st>>>(s->dev, c, n, ld, nullptr, (const double *)origins,
-                                               (const double *)rotations, env_scene, (double *)depth, seg, 0, nullptr);
+                                               (const double *)rotations, env_scene, (double *)depth, seg, 0, nullptr,
+                                               nullptr, nullptr, 0);
     int rc = check_launch("render_f64");
     if (rc) return rc;
     if (centroid_id > 0) {

@@ -142,8 +142,12 @@ class QuadEnvBase:
         import torch
 
         nat.require_cuda()
-        if config.mode != "parallel":
-            raise ConfigError("swarm mode is not part of this build (SURVEY F2); use mode='parallel'")
+        self.swarm = config.mode == "swarm"
+        if self.swarm and shard[1] != 1:
+            raise ConfigError("swarm mode runs one swarm per env (all agents interact): replicate envs across ranks "
+                              "instead of sharding one")
+        if self.swarm and not track_prev_state:
+            raise ConfigError("swarm mode needs prev_state tracking")
         self.config = config
         self.params = params if params is not None else QuadParams()
         self.sim = sim if sim is not None else SimConfig()
@@ -238,6 +242,12 @@ class QuadEnvBase:
         if self._obs_sensors:
             arr = (nat.QbSensorObs * len(self._obs_sensors))(*[o["rec"] for o in self._obs_sensors])
             self._obs_array = arr
+        # swarm mode: the other agents as render spheres + the swarm observation
+        self._swarm_spheres = self._swarm_ids = self._swarm_obs = None
+        if self.swarm and n > 1:
+            self._swarm_spheres = torch.zeros((n, n - 1, 4), dtype=dt, device=dev)
+            self._swarm_ids = torch.zeros((n, n - 1), dtype=torch.int32, device=dev)
+            self._swarm_obs = torch.zeros((n, n - 1, 13), dtype=dt, device=dev)
         bufs = nat.QbEnvBuffers()
         bufs.n, bufs.ld, bufs.index_offset = n, n, self.index_offset
         bufs.dtype = nat.QB_F32 if dt == torch.float32 else nat.QB_F64
@@ -260,6 +270,7 @@ class QuadEnvBase:
         t.n_scene_perm = len(self.scenes)
         t.scene_perm = self._scene_perm.data_ptr()
         t.collision_radius, t.min_spawn_clearance, t.bounds_margin = c.collision_radius, c.min_spawn_clearance, c.bounds_margin
+        t.swarm = int(self.swarm)
         r = c.randomization
         for k, spec in enumerate((r.position, r.velocity, r.orientation, r.angvel)):
             _dist(t.spawn[k], spec)
@@ -383,6 +394,10 @@ class QuadEnvBase:
         self._observe()
 
     def _render(self):
+        if self._swarm_obs is not None:  # other agents as spheres + swarm states (base.py:245-277, 306-309)
+            nat.check(nat.lib().qb_env_swarm_views(self._task, self._bufs, nat.ptr(self._swarm_spheres),
+                                                   nat.ptr(self._swarm_ids), nat.ptr(self._swarm_obs), nat.stream_of()),
+                      "qb_env_swarm_views")
         for slot in self._cams.values():
             cid = self._centroid_id(slot)
             if cid and slot["centroid"] is None:
@@ -390,7 +405,8 @@ class QuadEnvBase:
 
                 slot["centroid"] = torch.zeros((self.num_agents, 2), dtype=torch.float32, device=self.device)
             render_state(self.dev_scenes, slot["camera"], self._planes, env_scene=self.agent_scene, depth=slot["depth"],
-                         seg=slot["seg"], centroid_id=cid, centroid=slot["centroid"] if cid else None)
+                         seg=slot["seg"], centroid_id=cid, centroid=slot["centroid"] if cid else None,
+                         extra=self._swarm_spheres, extra_ids=self._swarm_ids)
 
     def _observe(self):
         if self._obs_sensors:
@@ -417,6 +433,8 @@ class QuadEnvBase:
             obs[spec.name] = slot["depth"] if spec.kind == "depth" else slot["seg"]
             if spec.kind == "segmentation":
                 seg_keys.append(spec.name)
+        if self._swarm_obs is not None:
+            obs["swarm"] = self._swarm_obs
         self._extra_observations(obs)
         return Observations(obs, self.num_agents, seg_keys)
 

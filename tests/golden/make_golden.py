@@ -417,11 +417,47 @@ def gen_noise():
     np.savez_compressed(os.path.join(OUT, "env_noise.npz"), **rec)
 
 
+def swarm_config():
+    """Gap crossing in swarm mode with CTBR commands (FP64-exact controller),
+    a crowded spawn box and a depth + segmentation camera (drone spheres)."""
+    cfg = tasks.gap_crossing_config(gap_width=1.0, num_agents=6)
+    return dataclasses.replace(
+        cfg, command_type="ctbr", episode_max_steps=40,
+        randomization=dataclasses.replace(cfg.randomization, position=DistSpec("uniform", low=[-3.4, -0.6, 1.3],
+                                                                               high=[-2.8, 0.6, 1.7])),
+        sensors=(SensorSpec(kind="depth", name="depth", width=48, height=32),
+                 SensorSpec(kind="segmentation", name="vision", width=48, height=32)))
+
+
+def gen_swarm():
+    cfg = swarm_config()
+    env = tasks.make_env(cfg)
+
+    def ctbr(rng, t, n):
+        return np.concatenate([rng.uniform(2.0, 22.0, (n, 1)), rng.normal(scale=6.0, size=(n, 3))], axis=1)
+
+    rec = record_env(env, ctbr, 120, seed=2, keep_images=(0, 1, 17, 119))
+    env2 = tasks.make_env(cfg)
+    obs = env2.reset(seed=2)
+    swarm = [np.stack([o["swarm"] for o in obs])]
+    r2 = np.random.default_rng(2 + 1000)
+    for t in range(120):
+        res = env2.step(ctl.command_from_array("ctbr", ctbr(r2, t, 6)))
+        swarm.append(np.stack([o["swarm"] for o in res.observations]))
+    rec["swarm_obs"] = np.array(swarm)
+    np.savez_compressed(os.path.join(OUT, "env_swarm.npz"), **rec)
+    print("swarm collisions", rec["collision"].sum(), "terminated", rec["terminated"].sum(), "success", rec["success"].sum())
+
+
 if __name__ == "__main__":
     print("reference:", quadsim.__file__, "numpy", np.__version__)
     if len(sys.argv) > 2 and sys.argv[2] == "noise":
         gen_noise()
         sys.exit(0)
+    if len(sys.argv) > 2 and sys.argv[2] == "swarm":
+        gen_swarm()
+        sys.exit(0)
+    gen_swarm()
     gen_noise()
     gen_rng()
     gen_dynamics()

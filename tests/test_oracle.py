@@ -293,3 +293,36 @@ def test_env_noise_replay():
     for j, t in enumerate(keep):
         for key in ("depth", "imu", "vision"):
             assert np.array_equal(snaps[t][key], g[f"obs_{key}"][j]), (key, t)
+
+
+# ------------------------------------------------------------- F2: swarm mode
+def swarm_config():
+    """make_golden.py swarm_config: gap crossing, 6 agents, CTBR, depth + segmentation."""
+    from paper_2407_14783_b200.env import DistSpec, SensorSpec, gap_crossing_config
+
+    cfg = gap_crossing_config(gap_width=1.0, num_agents=6)
+    return dataclasses.replace(
+        cfg, command_type="ctbr", episode_max_steps=40,
+        randomization=dataclasses.replace(cfg.randomization, position=DistSpec("uniform", low=[-3.4, -0.6, 1.3],
+                                                                               high=[-2.8, 0.6, 1.7])),
+        sensors=(SensorSpec(kind="depth", name="depth", width=48, height=32),
+                 SensorSpec(kind="segmentation", name="vision", width=48, height=32)))
+
+
+def test_env_swarm_gap_crossing_replay():
+    """Sequential swarm spawns, pairwise collisions, drone spheres in the
+    render, swarm observation and the gap-crossing reward, bit for bit."""
+    g = golden("env_swarm")
+    env = _replay("env_swarm", swarm_config(), 2, ["gap"])
+    assert env.swarm
+    cfg = swarm_config()
+    scenes = []
+    for spec in cfg.scenes:
+        t = spec.materialize().arrays
+        scenes.append(oracle.OracleScene(t.prim_type, t.prim_data, t.prim_object_id, t.prim_aabb_lo, t.prim_aabb_hi))
+    env = OracleEnv(cfg, scenes, QuadParams(), SimConfig(), ControllerGains())
+    obs = env.reset(seed=2)
+    assert np.array_equal(obs["swarm"], g["swarm_obs"][0])
+    for t in range(g["actions"].shape[0]):
+        obs = env.step(g["actions"][t])[0]
+        assert np.array_equal(obs["swarm"], g["swarm_obs"][t + 1]), t

@@ -50,8 +50,10 @@ WORKLOADS = {
     "c5": "landing on a 5e5-triangle indoor mesh, 64x64 down depth+seg, 131072 envs/GPU (BASELINE config 5, 1M on 8 GPUs)",
     "c3n": "config 3 + sensor noise (SURVEY F1): depth N(0, 0.02) -> Redwood, segmentation salt-and-pepper 2%, "
            "IMU N(0, 0.05); 65536 envs/GPU",
+    "swarm": "swarm gap crossing (SURVEY F2): one swarm of 256 agents, 64x64 depth with the other 255 agents "
+             "rendered as spheres, pairwise collisions",
 }
-ENVS = {"c1": 100, "c2": 100, "c3": 65536, "c4": 16384, "c5": 131072, "c3n": 65536}
+ENVS = {"c1": 100, "c2": 100, "c3": 65536, "c4": 16384, "c5": 131072, "c3n": 65536, "swarm": 256}
 
 
 def peaks():
@@ -174,6 +176,16 @@ def env_workload(kind, rank, world, total):
                                                           NoiseSpec("redwood", sigma_disparity=0.002))),
             SensorSpec(kind="segmentation", name="vision", noise=(NoiseSpec("saltpepper", p=0.02),)),
             SensorSpec(kind="imu", name="imu", noise=(NoiseSpec("normal", sigma=0.05),))))
+    elif kind == "swarm":
+        import dataclasses
+
+        from paper_2407_14783_b200.env import gap_crossing_config
+
+        # one swarm per rank (swarms do not shard: every agent sees every other)
+        cfg = gap_crossing_config(num_agents=total // world)
+        cfg = dataclasses.replace(cfg, randomization=InitRandomization(
+            position=DistSpec("uniform", low=[-5.5, -5.5, 0.5], high=[-1.0, 5.5, 3.5])))
+        return make_env(cfg), cfg
     elif kind == "c5":
         cfg = EnvConfig(num_agents=total, task="landing", command_type="lv", episode_max_steps=512,
                         scenes=(SceneSpec(kind="indoor", seed=0),),

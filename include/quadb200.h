@@ -99,6 +99,14 @@ typedef struct qb_scene qb_scene;
 int qb_scene_create(int32_t n_scenes, const int64_t *prim_offsets, const int64_t *prim_type, const double *prim_data,
                     const int64_t *prim_oid, const double *prim_lo, const double *prim_hi, qb_scene **out);
 int qb_scene_destroy(qb_scene *s);
+
+/* bvh.build_bvh (bvh.py:16-70) with this library's binned-SAH split, in the
+ * reference's flat layout: node_count > 0 marks a leaf over
+ * prim_order[first : first + count], 0 an internal node whose children are
+ * first and first + 1; at most 4 primitives per leaf.  Host-only (no GPU).
+ * Pass node_lo == NULL to get the node count in *n_nodes first. */
+int qb_bvh_build(int64_t n, const double *prim_lo, const double *prim_hi, int64_t *n_nodes, double *node_lo,
+                 double *node_hi, int64_t *node_first, int64_t *node_count, int64_t *prim_order);
 /* stats: [n_nodes, n_prims, max_depth, n_scenes] */
 int qb_scene_stats(const qb_scene *s, int64_t *out4);
 /* raw bounds of scene k: lo.xyz hi.xyz (Scene.bounds, shapes.py:214-217) */
@@ -107,7 +115,7 @@ int qb_scene_bounds(const qb_scene *s, int32_t k, double *out6);
 /* queries.nearest_point (queries.py:28-38 / kernels.py:120-182), exact
  * double, batched: q (n,3) f64 device; pt (n,3), d (n) distance, oid (n). */
 int qb_nearest_point(const qb_scene *s, const int32_t *env_scene, int64_t n, const double *q, double *pt, double *dist,
-                     int32_t *oid, void *stream);
+                     int32_t *oid, double *dist2, void *stream); /* dist2: the squared distance (kernels.py returns it), may be NULL */
 
 /* queries.raycast (queries.py:56-71 / kernels.py:389-399), batched; t=-1 on
  * miss.  o, d (n,3) in dtype; t (n) in dtype. */
@@ -140,7 +148,8 @@ int qb_render(const qb_scene *s, const qb_camera *cam, int32_t dtype, int64_t n,
 /* Same renderer from explicit camera poses (render_batch's own inputs):
  * origins (n,3), rotations (n,3,3) camera->world, in dtype. */
 int qb_render_poses(const qb_scene *s, const qb_camera *cam, int32_t dtype, int64_t n, const void *origins,
-                    const void *rotations, const int32_t *env_scene, void *depth, int32_t *seg, void *stream);
+                    const void *rotations, const int32_t *env_scene, void *depth, int32_t *seg, const void *extra,
+                    const int32_t *extra_ids, int32_t n_extra, void *stream);
 
 /* --------------------------------------------------------------------- env */
 

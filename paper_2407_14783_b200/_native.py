@@ -179,12 +179,13 @@ SIGNATURES = {
     "qb_dynamics_vjp": ([_PP(QbParams), _I32, _I32, _I64, _I64, _P, _P, _P, _P, _P, _P, _P], ctypes.c_int),
     "qb_scene_create": ([_I32, _P, _P, _P, _P, _P, _P, _PP(_P)], ctypes.c_int),
     "qb_scene_destroy": ([_P], ctypes.c_int),
+    "qb_bvh_build": ([_I64, _P, _P, _P, _P, _P, _P, _P, _P], ctypes.c_int),
     "qb_scene_stats": ([_P, _P], ctypes.c_int),
     "qb_scene_bounds": ([_P, _I32, _P], ctypes.c_int),
-    "qb_nearest_point": ([_P, _P, _I64, _P, _P, _P, _P, _P], ctypes.c_int),
+    "qb_nearest_point": ([_P, _P, _I64, _P, _P, _P, _P, _P, _P], ctypes.c_int),
     "qb_raycast": ([_P, _I32, _P, _I64, _P, _P, _D, _D, _P, _P, _P], ctypes.c_int),
     "qb_render": ([_P, _PP(QbCamera), _I32, _I64, _I64, _P, _P, _P, _P, _I32, _P, _P, _P, _I32, _P], ctypes.c_int),
-    "qb_render_poses": ([_P, _PP(QbCamera), _I32, _I64, _P, _P, _P, _P, _P, _P], ctypes.c_int),
+    "qb_render_poses": ([_P, _PP(QbCamera), _I32, _I64, _P, _P, _P, _P, _P, _P, _P, _I32, _P], ctypes.c_int),
     "qb_env_reset": ([_PP(QbParams), _PP(QbTask), _P, _PP(QbEnvBuffers), _U64, _P], ctypes.c_int),
     "qb_env_step": ([_PP(QbParams), _I32, _PP(QbTask), _P, _PP(QbEnvBuffers), _P], ctypes.c_int),
     "qb_env_refresh": ([_PP(QbTask), _P, _PP(QbEnvBuffers), _P], ctypes.c_int),

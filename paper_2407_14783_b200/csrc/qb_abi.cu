@@ -423,6 +423,34 @@ int qb_scene_create(int32_t n_scenes, const int64_t *prim_offsets, const int64_t
     return QB_OK;
 }
 
+int qb_bvh_build(int64_t n, const double *prim_lo, const double *prim_hi, int64_t *n_nodes, double *node_lo,
+                 double *node_hi, int64_t *node_first, int64_t *node_count, int64_t *prim_order) {
+    QB_REQUIRE(n > 0 && n < (1LL << 30) && prim_lo && prim_hi && n_nodes, "qb_bvh_build: bad arguments");
+    std::vector<qb::BNode> nodes;
+    std::vector<int> order;
+    int depth = 0;
+    if (qb::build_bvh((int)n, prim_lo, prim_hi, nodes, order, depth) != 0) {
+        qb::set_error("qb_bvh_build: tree too deep (%d)", depth);
+        return QB_EINVAL;
+    }
+    if (!node_lo) {
+        *n_nodes = (int64_t)nodes.size();
+        return QB_OK;
+    }
+    QB_REQUIRE(*n_nodes == (int64_t)nodes.size() && node_hi && node_first && node_count && prim_order,
+               "qb_bvh_build: output arrays sized for %lld nodes", (long long)nodes.size());
+    for (size_t i = 0; i < nodes.size(); ++i) {
+        for (int k = 0; k < 3; ++k) {
+            node_lo[3 * i + k] = nodes[i].lo[k];
+            node_hi[3 * i + k] = nodes[i].hi[k];
+        }
+        node_first[i] = nodes[i].a;
+        node_count[i] = nodes[i].b > 0 ? nodes[i].b : 0;
+    }
+    for (int64_t i = 0; i < n; ++i) prim_order[i] = order[i];
+    return QB_OK;
+}
+
 int qb_scene_destroy(qb_scene *s) {
     if (!s) return QB_OK;
     int prev = 0;
@@ -451,9 +479,9 @@ int qb_scene_bounds(const qb_scene *s, int32_t k, double *out6) {
 }
 
 int qb_nearest_point(const qb_scene *s, const int32_t *env_scene, int64_t n, const double *q, double *pt, double *dist,
-                     int32_t *oid, void *stream) {
+                     int32_t *oid, double *dist2, void *stream) {
     QB_REQUIRE(s && q && n >= 0, "qb_nearest_point: bad arguments");
-    return qb::launch_nearest(s, env_scene, n, q, pt, dist, oid, qb::as_stream(stream));
+    return qb::launch_nearest(s, env_scene, n, q, pt, dist, oid, dist2, qb::as_stream(stream));
 }
 
 int qb_raycast(const qb_scene *s, int32_t dtype, const int32_t *env_scene, int64_t n, const void *o, const void *d,
@@ -483,13 +511,15 @@ int qb_render(const qb_scene *s, const qb_camera *cam, int32_t dtype, int64_t n,
 }
 
 int qb_render_poses(const qb_scene *s, const qb_camera *cam, int32_t dtype, int64_t n, const void *origins,
-                    const void *rotations, const int32_t *env_scene, void *depth, int32_t *seg, void *stream) {
+                    const void *rotations, const int32_t *env_scene, void *depth, int32_t *seg, const void *extra,
+                    const int32_t *extra_ids, int32_t n_extra, void *stream) {
     QB_REQUIRE(s && origins && rotations && n >= 0, "qb_render_poses: bad arguments");
     int rc = check_cam(cam);
     if (rc) return rc;
     QB_REQUIRE(dtype == QB_F32 || dtype == QB_F64, "bad dtype %d", dtype);
-    return qb::launch_render(s, cam, dtype, n, n, nullptr, origins, rotations, env_scene, depth, seg, 0, nullptr, nullptr,
-                             nullptr, 0, qb::as_stream(stream));
+    QB_REQUIRE(n_extra == 0 || (extra && extra_ids), "extra spheres missing");
+    return qb::launch_render(s, cam, dtype, n, n, nullptr, origins, rotations, env_scene, depth, seg, 0, nullptr, extra,
+                             extra_ids, n_extra, qb::as_stream(stream));
 }
 
 static int check_env(const qb_task *task, const qb_scene *s, const qb_env_buffers *b) {

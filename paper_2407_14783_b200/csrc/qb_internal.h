@@ -64,7 +64,7 @@ int launch_render(const qb_scene *s, const qb_camera *cam, int dtype, long long 
                   int32_t centroid_id, float *centroid, const void *extra, const int32_t *extra_ids, int n_extra,
                   cudaStream_t st);
 int launch_nearest(const qb_scene *s, const int32_t *env_scene, long long n, const double *q, double *pt, double *dist,
-                   int32_t *oid, cudaStream_t st);
+                   int32_t *oid, double *dist2, cudaStream_t st);
 int launch_raycast(const qb_scene *s, int dtype, const int32_t *env_scene, long long n, const void *o, const void *d,
                    double tmin, double tmax, void *t, int32_t *oid, cudaStream_t st);
 int launch_env(int mode, const qb_params *p, int kind, const qb_task *task, const qb_scene *s, const qb_env_buffers *b,

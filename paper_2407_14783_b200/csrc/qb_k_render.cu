@@ -838,7 +838,7 @@ __global__ void k_centroid(long long n, int W, int H, const int32_t *seg, int id
 }
 
 __global__ void k_nearest(DevScene S, const int32_t *env_scene, long long n, const double *q, double *pt, double *dist,
-                          int32_t *oid) {
+                          int32_t *oid, double *dist2) {
     long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     NearestResult r = nearest_point(S, env_scene ? env_scene[i] : 0, q[3 * i], q[3 * i + 1], q[3 * i + 2]);
@@ -848,6 +848,7 @@ __global__ void k_nearest(DevScene S, const int32_t *env_scene, long long n, con
         pt[3 * i + 2] = r.pz;
     }
     if (dist) dist[i] = __dsqrt_rn(r.d2);
+    if (dist2) dist2[i] = r.d2;
     if (oid) oid[i] = r.oid;
 }
 
@@ -909,7 +910,7 @@ int launch_render(const qb_scene *s, const qb_camera *cam, int dtype, long long 
             else
                 k_render_cull<false><<<(int)blocks, B, 0, st>>>(s->dev, c, n, ld, nullptr, (const float *)origins,
                                                                 (const float *)rotations, env_scene, (float *)depth, seg, 0,
-                                                                nullptr, nullptr, nullptr, 0, split);
+                                                                nullptr, (const float *)extra, extra_ids, n_extra, split);
             int rc = check_launch("render_cull_f32");
             if (rc || split == 1 || centroid_id <= 0) return rc;
             k_centroid<<<env_grid(n, 128), 128, 0, st>>>(n, c.W, c.H, seg, centroid_id, centroid);
@@ -925,7 +926,7 @@ int launch_render(const qb_scene *s, const qb_camera *cam, int dtype, long long 
         else
             k_render_f<false><<<(int)blocks, B, 0, st>>>(s->dev, c, n, ld, nullptr, (const float *)origins,
                                                          (const float *)rotations, env_scene, (float *)depth, seg, 0, nullptr,
-                                                         nullptr, nullptr, 0);
+                                                         (const float *)extra, extra_ids, n_extra);
         return check_launch("render_f32");
     }
     CamD c;
@@ -946,7 +947,7 @@ int launch_render(const qb_scene *s, const qb_camera *cam, int dtype, long long 
     else
         k_render_x<false><<<blocks, B, 0, st>>>(s->dev, c, n, ld, nullptr, (const double *)origins,
                                                (const double *)rotations, env_scene, (double *)depth, seg, 0, nullptr,
-                                               nullptr, nullptr, 0);
+                                               (const double *)extra, extra_ids, n_extra);
     int rc = check_launch("render_f64");
     if (rc) return rc;
     if (centroid_id > 0) {
@@ -961,9 +962,9 @@ int launch_render(const qb_scene *s, const qb_camera *cam, int dtype, long long 
 }
 
 int launch_nearest(const qb_scene *s, const int32_t *env_scene, long long n, const double *q, double *pt, double *dist,
-                   int32_t *oid, cudaStream_t st) {
+                   int32_t *oid, double *dist2, cudaStream_t st) {
     if (n == 0) return QB_OK;
-    k_nearest<<<env_grid(n, 128), 128, 0, st>>>(s->dev, env_scene, n, q, pt, dist, oid);
+    k_nearest<<<env_grid(n, 128), 128, 0, st>>>(s->dev, env_scene, n, q, pt, dist, oid, dist2);
     return check_launch("nearest_point");
 }
 

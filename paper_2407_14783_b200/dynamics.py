@@ -13,6 +13,8 @@ finiteness mask -> NonFiniteState.
 
 from __future__ import annotations
 
+from dataclasses import dataclass
+
 import numpy as np
 
 from . import _native as nat
@@ -112,10 +114,57 @@ class QuadState:
         return f"QuadState(N={self.batch_size}, dtype={self.dtype}, device={self.device})"
 
 
+@dataclass
+class Wrench:
+    """Force and torque in the body frame, batched (dynamics.py:95-100)."""
+
+    force_b: object
+    torque_b: object
+
+
 def rotor_thrusts(rotor_speeds, params: QuadParams):
-    """dynamics.py:103-106 (host helper)."""
+    """dynamics.py:103-106: per-rotor thrust k2 w^2 + k1 w + k0 (elementwise,
+    on the input's device; K1 evaluates it fused in the step)."""
     k2, k1, k0 = params.thrust_coeffs
     return k2 * rotor_speeds**2 + k1 * rotor_speeds + k0
+
+
+def rotor_lag(current, desired, dt: float, params: QuadParams):
+    """dynamics.py:109-114: first-order motor response over dt, clamped."""
+    import math
+
+    alpha = math.exp(-params.motor_decay * dt)
+    out = desired + (current - desired) * alpha
+    lo, hi = params.rotor_speed_limits
+    return out.clip(lo, hi)
+
+
+def drag_force(velocity_b, params: QuadParams):
+    """dynamics.py:117-120: -c v |v| componentwise, c = 0.5 rho Cd s."""
+    import torch
+
+    c = 0.5 * params.air_density * np.asarray(params.drag_coeffs, float) * params.cross_area
+    if isinstance(velocity_b, torch.Tensor):
+        c = torch.as_tensor(c, dtype=velocity_b.dtype, device=velocity_b.device)
+    return -c * velocity_b * abs(velocity_b)
+
+
+def aggregate_wrench(thrusts, params: QuadParams) -> Wrench:
+    """dynamics.py:123-140: collective force (body z) and torques sum_i t_i g_i."""
+    import torch
+
+    t = thrusts if thrusts.ndim == 2 else thrusts[None, :]
+    g = np.asarray(params.torque_arms, float)
+    if isinstance(t, torch.Tensor):
+        g = torch.as_tensor(g, dtype=t.dtype, device=t.device)
+        force = torch.zeros((t.shape[0], 3), dtype=t.dtype, device=t.device)
+        stack = torch.stack
+    else:
+        force = np.zeros((t.shape[0], 3))
+        stack = lambda xs, dim: np.stack(xs, axis=dim)  # noqa: E731
+    force[:, 2] = t[:, 0] + t[:, 1] + t[:, 2] + t[:, 3]
+    torque = stack([t[:, 0] * g[0, a] + t[:, 1] * g[1, a] + t[:, 2] * g[2, a] + t[:, 3] * g[3, a] for a in range(3)], 1)
+    return Wrench(force, torque)
 
 
 def step(state: QuadState, rotor_speed_commands, config: SimConfig = None, params: QuadParams = None, check: bool = True,

@@ -43,7 +43,7 @@ def nearest_points(scene_or_dev, queries, env_scene=None):
     oid = torch.empty(n, dtype=torch.int32, device=q.device)
     with torch.cuda.device(q.device):
         nat.check(nat.lib().qb_nearest_point(dev.handle, nat.ptr(env_scene), n, nat.ptr(q), nat.ptr(pt), nat.ptr(d),
-                                             nat.ptr(oid), nat.stream_of()), "qb_nearest_point")
+                                             nat.ptr(oid), None, nat.stream_of()), "qb_nearest_point")
     return pt, d, oid
 
 

@@ -118,7 +118,8 @@ def render_frames(scene, body_position, body_orientation, camera: CameraModel, e
             # swarm spheres need per-view poses inside the kernel: go through the state path
             return _render_with_extra(dev, o, r, camera, extra_spheres, extra_ids, host, dtype)
         nat.check(nat.lib().qb_render_poses(dev.handle, camera.native(), code, n, nat.ptr(o), nat.ptr(r), nat.ptr(env_scene),
-                                            nat.ptr(depth), nat.ptr(seg), nat.stream_of()), "qb_render_poses")
+                                            nat.ptr(depth), nat.ptr(seg), None, None, 0, nat.stream_of()),
+                  "qb_render_poses")
     if host:
         return depth.double().cpu().numpy(), seg.long().cpu().numpy()
     return depth, seg
@@ -313,3 +314,47 @@ def ctypes_pointer(obj):
     import ctypes
 
     return ctypes.cast(ctypes.pointer(obj), ctypes.c_void_p)
+
+
+# ---------------------------------------------------------------------------
+# 16-bit PGM export (sensing.py:238-274): millimeter depth, raw object ids.
+# Host file I/O on observations copied back from the device.
+
+PGM_MAXVAL = 65535
+
+
+def _host(image):
+    import torch
+
+    return image.detach().cpu().numpy() if isinstance(image, torch.Tensor) else np.asarray(image)
+
+
+def write_pgm16(path, image):
+    """Binary 16-bit PGM (big-endian samples, PNM spec)."""
+    image = _host(image)
+    if image.ndim != 2:
+        raise ValueError("expected a 2-D image")
+    data = np.clip(np.round(image), 0, PGM_MAXVAL).astype(">u2")
+    with open(path, "wb") as fh:
+        fh.write(f"P5\n{image.shape[1]} {image.shape[0]}\n{PGM_MAXVAL}\n".encode())
+        fh.write(data.tobytes())
+
+
+def read_pgm16(path) -> np.ndarray:
+    with open(path, "rb") as fh:
+        magic = fh.readline().strip()
+        if magic != b"P5":
+            raise ValueError(f"not a binary PGM file: {magic!r}")
+        width, height = (int(v) for v in fh.readline().split())
+        maxval = int(fh.readline())
+        data = np.frombuffer(fh.read(), dtype=">u2" if maxval > 255 else "u1", count=width * height)
+    return data.reshape(height, width).astype(np.int64)
+
+
+def export_depth_mm(path, depth_m):
+    """Depth frame in millimeters, quantized to 16 bit."""
+    write_pgm16(path, _host(depth_m).astype(np.float64) * 1000.0)
+
+
+def export_segmentation(path, ids):
+    write_pgm16(path, ids)

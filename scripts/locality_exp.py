@@ -21,7 +21,7 @@ def run(org, label):
     d = torch.empty((n, 64, 64), device="cuda"); s = torch.empty((n, 64, 64), dtype=torch.int32, device="cuda")
     def go():
         nat.check(nat.lib().qb_render_poses(dev.handle, cam.native(1), nat.QB_F32, n, nat.ptr(o), nat.ptr(r), None,
-                                           nat.ptr(d), nat.ptr(s), nat.stream_of()))
+                                           nat.ptr(d), nat.ptr(s), None, None, 0, nat.stream_of()))
     go(); torch.cuda.synchronize()
     ts = []
     for _ in range(3):

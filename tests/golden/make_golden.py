@@ -417,6 +417,21 @@ def gen_noise():
     np.savez_compressed(os.path.join(OUT, "env_noise.npz"), **rec)
 
 
+def gen_pgm():
+    """sensing.py:238-274 PGM export bytes."""
+    import tempfile
+
+    rng = np.random.default_rng(3)
+    depth = rng.uniform(0.2, 70.0, (5, 7))
+    depth[0, 0], depth[1, 1] = 0.0004, 80.0
+    ids = rng.integers(0, 70000, (6, 4))
+    d = tempfile.mkdtemp()
+    sensing.export_depth_mm(os.path.join(d, "a.pgm"), depth)
+    sensing.export_segmentation(os.path.join(d, "b.pgm"), ids)
+    rd = lambda f: np.frombuffer(open(os.path.join(d, f), "rb").read(), np.uint8)  # noqa: E731
+    np.savez_compressed(os.path.join(OUT, "pgm.npz"), depth=depth, ids=ids, depth_pgm=rd("a.pgm"), ids_pgm=rd("b.pgm"))
+
+
 def swarm_config():
     """Gap crossing in swarm mode with CTBR commands (FP64-exact controller),
     a crowded spawn box and a depth + segmentation camera (drone spheres)."""
@@ -457,6 +472,7 @@ if __name__ == "__main__":
     if len(sys.argv) > 2 and sys.argv[2] == "swarm":
         gen_swarm()
         sys.exit(0)
+    gen_pgm()
     gen_swarm()
     gen_noise()
     gen_rng()

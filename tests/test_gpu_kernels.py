@@ -157,7 +157,7 @@ def _render(ds, cam, pos, quat, dtype):
     seg = torch.empty((n, cam.height, cam.width), dtype=torch.int32, device=DEV)
     code = nat.QB_F32 if dtype == torch.float32 else nat.QB_F64
     nat.check(nat.lib().qb_render_poses(ds.handle, cam.native(), code, n, nat.ptr(ot), nat.ptr(rt), None, nat.ptr(depth),
-                                        nat.ptr(seg), nat.stream_of()))
+                                        nat.ptr(seg), None, None, 0, nat.stream_of()))
     return depth.double().cpu().numpy(), seg.cpu().numpy(), o, r
 
 

@@ -143,3 +143,43 @@ def test_oracle_is_not_imported_by_product():
             if f.endswith(".py"):
                 src = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"^\s*(import oracle|from oracle)", src, flags=re.M), f
+
+
+def test_pgm_export_matches_reference_bytes(tmp_path):
+    """sensing.py:238-274: byte-identical 16-bit PGM files (golden from the reference)."""
+    from conftest import golden
+    from paper_2407_14783_b200 import sensing
+
+    g = golden("pgm")
+    sensing.export_depth_mm(tmp_path / "a.pgm", g["depth"])
+    sensing.export_segmentation(tmp_path / "b.pgm", g["ids"])
+    assert np.array_equal(np.frombuffer((tmp_path / "a.pgm").read_bytes(), np.uint8), g["depth_pgm"])
+    assert np.array_equal(np.frombuffer((tmp_path / "b.pgm").read_bytes(), np.uint8), g["ids_pgm"])
+    back = sensing.read_pgm16(tmp_path / "b.pgm")
+    assert np.array_equal(back, np.clip(g["ids"], 0, 65535))
+
+
+def test_build_bvh_dropin_layout():
+    """bvh.build_bvh drop-in: the reference's flat layout, every primitive in
+    exactly one leaf of <= LEAF_SIZE, boxes nested, children adjacent."""
+    from conftest import golden
+    from paper_2407_14783_b200.geometry.bvh import LEAF_SIZE, build_bvh
+
+    g = golden("geometry")
+    lo, hi = g["tess_prim_lo"], g["tess_prim_hi"]
+    node_lo, node_hi, first, count, order = build_bvh(lo, hi)
+    assert sorted(order.tolist()) == list(range(len(lo)))
+    seen = np.zeros(len(lo), int)
+    stack = [0]
+    while stack:
+        i = stack.pop()
+        if count[i] > 0:
+            assert count[i] <= LEAF_SIZE
+            for p in order[first[i]:first[i] + count[i]]:
+                seen[p] += 1
+                assert np.all(lo[p] >= node_lo[i]) and np.all(hi[p] <= node_hi[i])
+        else:
+            for c in (first[i], first[i] + 1):
+                assert np.all(node_lo[c] >= node_lo[i]) and np.all(node_hi[c] <= node_hi[i])
+                stack.append(c)
+    assert np.all(seen == 1)

@@ -58,6 +58,15 @@ int qb_dynamics_step(const qb_params *p, int32_t cmd_kind, int32_t dtype, int64_
 int qb_command_to_rotor_speeds(const qb_params *p, int32_t cmd_kind, int32_t dtype, int64_t n, int64_t ld,
                                const void *state, const void *action, void *out, void *stream);
 
+/* Controller stages (control.py:101-139): QB_STAGE_MIXER maps in (n,4)
+ * [collective force, torque_b] to out (n,4) per-rotor thrusts and flags (n)
+ * "saturated" (torque scaled down or collective clamped; may be NULL);
+ * QB_STAGE_LV_TO_CTBR / QB_STAGE_PS_TO_CTBR map an LV / PS command (n,4) at
+ * the state planes to out (n,4) [collective accel, body rates]. */
+enum qb_control_stage { QB_STAGE_MIXER = 0, QB_STAGE_LV_TO_CTBR = 1, QB_STAGE_PS_TO_CTBR = 2 };
+int qb_control_stage(const qb_params *p, int32_t stage, int32_t dtype, int64_t n, int64_t ld, const void *state,
+                     const void *in, void *out, uint8_t *flags, void *stream);
+
 /* Horizon rollout (gradients.rollout, gradients.py:200-215, batched and
  * tape-only): states_tape is (T+1) blocks of 17 planes (block stride 17*ld);
  * block 0 must hold the initial state.  actions (T, n, 4). */

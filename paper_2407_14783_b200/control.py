@@ -159,3 +159,83 @@ def command_to_rotor_speeds(cmd, state, gains: ControllerGains = None, params: Q
         nat.check(nat.lib().qb_command_to_rotor_speeds(P, nat.CMD[kind], code, n, planes.stride(0), nat.ptr(planes),
                                                        nat.ptr(a), nat.ptr(out), nat.stream_of()), "command_to_rotor_speeds")
     return out.cpu().numpy() if host else out
+
+
+# ---------------------------------------------------------------------------
+# controller stages on their own (control.py:95-139), same kernels as K1
+
+
+@dataclass
+class MixerResult:
+    thrusts: object  # (N, 4)
+    saturated: object  # (N,) bool
+
+
+def _stage(stage, rows, state, params, gains, dtype=None, device=None):
+    import torch
+
+    host = isinstance(rows, np.ndarray)
+    if state is not None:
+        planes = state.planes
+        dtype, device = planes.dtype, planes.device
+    else:
+        planes = None
+        dtype = dtype or (torch.float64 if host else rows.dtype)
+        device = device or (torch.device("cuda", torch.cuda.current_device()) if host else rows.device)
+    a = torch.as_tensor(rows, dtype=dtype, device=device).reshape(-1, 4).contiguous()
+    n = a.shape[0]
+    if planes is not None and planes.shape[1] != n:
+        raise ValueError(f"command batch {n} != state batch {planes.shape[1]}")
+    out = torch.empty((n, 4), dtype=dtype, device=device)
+    flags = torch.empty(n, dtype=torch.uint8, device=device)
+    code = nat.QB_F32 if dtype == torch.float32 else nat.QB_F64
+    with torch.cuda.device(device):
+        nat.check(nat.lib().qb_control_stage(native_params(params, None, gains), stage, code, n,
+                                             planes.stride(0) if planes is not None else n, nat.ptr(planes), nat.ptr(a),
+                                             nat.ptr(out), nat.ptr(flags), nat.stream_of()), "qb_control_stage")
+    if host:
+        return out.cpu().numpy(), flags.bool().cpu().numpy()
+    return out, flags.bool()
+
+
+def mixer(collective_force, torque_b, params: QuadParams = None) -> MixerResult:
+    """Allocate (collective force, body torque) to per-rotor thrusts
+    (control.py:101-130): collective clamped to the total-thrust range, the
+    torque scaled down uniformly until every rotor fits its limits."""
+    f, tq = _col(collective_force), _mat(torque_b, 3)
+    thr, sat = _stage(0, _cat([f, tq]), None, params, None)
+    return MixerResult(thr, sat)
+
+
+def srt_to_rotor_speeds(cmd: SRT, params: QuadParams = None, state=None):
+    """control.py:133-135 (clamp thrusts, invert the thrust curve)."""
+    if state is None:
+        from .dynamics import QuadState
+
+        arr = cmd.as_array()
+        state = QuadState.hover(arr.shape[0], params or QuadParams(),
+                                dtype=_dtype_of(arr))
+    return command_to_rotor_speeds(cmd, state, None, params)
+
+
+def ctbr_to_rotor_speeds(cmd: CTBR, state, gains: ControllerGains = None, params: QuadParams = None):
+    """control.py:138-158: body-rate P loop with gyroscopic feedforward, mixer, thrust inverse."""
+    return command_to_rotor_speeds(cmd, state, gains, params)
+
+
+def lv_to_ctbr(cmd: LV, state, gains: ControllerGains = None, params: QuadParams = None) -> CTBR:
+    """control.py:161-223: velocity P loop, geometric attitude -> CTBR."""
+    out, _ = _stage(1, cmd.as_array(), state, params, gains)
+    return CTBR(out[:, 0], out[:, 1:4])
+
+
+def ps_to_ctbr(cmd: PS, state, gains: ControllerGains = None, params: QuadParams = None) -> CTBR:
+    """control.py:226-233: position PD to a speed-capped velocity, then the LV loop."""
+    out, _ = _stage(2, cmd.as_array(), state, params, gains)
+    return CTBR(out[:, 0], out[:, 1:4])
+
+
+def _dtype_of(arr):
+    import torch
+
+    return arr.dtype if isinstance(arr, torch.Tensor) else torch.float64

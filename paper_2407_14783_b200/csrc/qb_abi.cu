@@ -451,6 +451,15 @@ int qb_bvh_build(int64_t n, const double *prim_lo, const double *prim_hi, int64_
     return QB_OK;
 }
 
+int qb_control_stage(const qb_params *p, int32_t stage, int32_t dtype, int64_t n, int64_t ld, const void *state,
+                     const void *in, void *out, uint8_t *flags, void *stream) {
+    QB_REQUIRE(p && in && out && n >= 0, "qb_control_stage: bad arguments");
+    QB_REQUIRE(stage >= QB_STAGE_MIXER && stage <= QB_STAGE_PS_TO_CTBR, "qb_control_stage: unknown stage %d", stage);
+    QB_REQUIRE(stage == QB_STAGE_MIXER || (state && ld >= n), "qb_control_stage: state planes needed");
+    QB_REQUIRE(dtype == QB_F32 || dtype == QB_F64, "bad dtype %d", dtype);
+    return qb::launch_control_stage(p, stage, dtype, n, ld, state, in, out, flags, qb::as_stream(stream));
+}
+
 int qb_scene_destroy(qb_scene *s) {
     if (!s) return QB_OK;
     int prev = 0;

@@ -297,7 +297,8 @@ template <class R> QB_D R speed_of_thrust(const DynConsts<R> &C, R f) {
 }
 
 // control.py:101-130
-template <class R> QB_D void mixer(const DynConsts<R> &C, R force, const R *tq, R *thr) {
+// saturated (optional): scale < 1 or the collective was clamped (control.py:130)
+template <class R> QB_D void mixer(const DynConsts<R> &C, R force, const R *tq, R *thr, bool *saturated = nullptr) {
     R fcl = p_clip(force, C.flo4, C.fhi4);
     R base[4], tp[4];
     R scale;
@@ -325,6 +326,7 @@ template <class R> QB_D void mixer(const DynConsts<R> &C, R force, const R *tq, 
         }
         scale = fmaxf(fminf(bmin, R(1.0)), R(0.0));
     }
+    if (saturated) *saturated = scale < R(1.0) || force != fcl;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         R f = base[i] + scale * tp[i];
@@ -411,6 +413,26 @@ template <class R> QB_D void sincos_r(R yaw, R &c, R &s) {
     }
 }
 
+// control.py:122-139: LV / PS command -> CTBR (collective, body rates)
+template <class R, int KIND> QB_D void to_ctbr(const DynConsts<R> &C, const R *x, const R *cmd, R &coll, R *rates) {
+    R v_des[3];
+    if constexpr (KIND == QB_CMD_PS) {  // control.py:226-233
+#pragma unroll
+        for (int a = 0; a < 3; ++a) v_des[a] = C.pos_p[a] * (cmd[a] - x[a]) - C.pos_d[a] * x[3 + a];
+        clip_norm(v_des, C.max_speed);
+    } else {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) v_des[a] = cmd[a];
+    }
+    R a_des[3];  // control.py:216-223
+#pragma unroll
+    for (int a = 0; a < 3; ++a) a_des[a] = C.vel_p[a] * (v_des[a] - x[3 + a]);
+    clip_norm(a_des, C.max_tilt);
+    R cy, sy;
+    sincos_r(cmd[3], cy, sy);
+    accel_to_ctbr(C, x, a_des, cy, sy, coll, rates);
+}
+
 // control.py:242-252: command (as_array layout) -> desired rotor speeds
 template <class R, int KIND> QB_D void command_to_speeds(const DynConsts<R> &C, const R *x, const R *cmd, R *out) {
     if constexpr (KIND == QB_CMD_ROTOR) {
@@ -422,22 +444,8 @@ template <class R, int KIND> QB_D void command_to_speeds(const DynConsts<R> &C, 
     } else if constexpr (KIND == QB_CMD_CTBR) {
         ctbr_speeds(C, x, cmd[0], cmd[1], cmd[2], cmd[3], out);
     } else {
-        R v_des[3];
-        if constexpr (KIND == QB_CMD_PS) {  // control.py:226-233
-#pragma unroll
-            for (int a = 0; a < 3; ++a) v_des[a] = C.pos_p[a] * (cmd[a] - x[a]) - C.pos_d[a] * x[3 + a];
-            clip_norm(v_des, C.max_speed);
-        } else {
-#pragma unroll
-            for (int a = 0; a < 3; ++a) v_des[a] = cmd[a];
-        }
-        R a_des[3];  // control.py:216-223
-#pragma unroll
-        for (int a = 0; a < 3; ++a) a_des[a] = C.vel_p[a] * (v_des[a] - x[3 + a]);
-        clip_norm(a_des, C.max_tilt);
-        R cy, sy, coll, rates[3];
-        sincos_r(cmd[3], cy, sy);
-        accel_to_ctbr(C, x, a_des, cy, sy, coll, rates);
+        R coll, rates[3];
+        to_ctbr<R, KIND>(C, x, cmd, coll, rates);
         ctbr_speeds(C, x, coll, rates[0], rates[1], rates[2], out);
     }
 }

@@ -54,6 +54,8 @@ namespace qb {
 int launch_dynamics_step(const qb_params *p, int kind, int dtype, long long n, long long ld, void *state,
                          const void *action, void *rotor_out, uint8_t *nonfinite, int T, const void *actions_seq,
                          cudaStream_t st);
+int launch_control_stage(const qb_params *p, int stage, int dtype, long long n, long long ld, const void *state,
+                         const void *in, void *out, uint8_t *flags, cudaStream_t st);
 int launch_command(const qb_params *p, int kind, int dtype, long long n, long long ld, const void *state,
                    const void *action, void *out, cudaStream_t st);
 int launch_vjp(const qb_params *p, int kind, int dtype, long long n, long long ld, int T, const void *states_tape,

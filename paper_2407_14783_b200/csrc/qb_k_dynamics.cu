@@ -159,6 +159,44 @@ int dispatch_step(const qb_params *p, int kind, long long n, long long ld, void 
     return qb::check_launch("dynamics_step");
 }
 
+// controller stages (control.py:101-139): 0 mixer (in [F, tau] -> thrusts +
+// saturated), 1 LV -> CTBR, 2 PS -> CTBR (out [collective, rates])
+template <class R>
+__global__ void __launch_bounds__(128) k_control_stage(DynConsts<R> C, int stage, long long n, long long ld,
+                                                       const typename storage_of<R>::type *state,
+                                                       const typename storage_of<R>::type *in,
+                                                       typename storage_of<R>::type *out, uint8_t *flags) {
+    using S = typename storage_of<R>::type;
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    R a[4], o[4];
+    load4<R, S>(in + i * 4, a);
+    if (stage == 0) {
+        bool sat;
+        mixer(C, a[0], a + 1, o, &sat);
+        if (flags) flags[i] = sat;
+    } else {
+        R x[17];
+#pragma unroll
+        for (int k = 0; k < 17; ++k) x[k] = R(state[k * ld + i]);
+        if (stage == 1)
+            to_ctbr<R, QB_CMD_LV>(C, x, a, o[0], o + 1);
+        else
+            to_ctbr<R, QB_CMD_PS>(C, x, a, o[0], o + 1);
+    }
+    store4<R, S>(out + i * 4, o);
+}
+
+template <class R>
+int dispatch_stage(const qb_params *p, int stage, long long n, long long ld, const void *state, const void *in, void *out,
+                   uint8_t *flags, cudaStream_t st) {
+    using S = typename storage_of<R>::type;
+    k_control_stage<R><<<qb::env_grid(n, 128), 128, 0, st>>>(make_consts<R>(*p), stage, n, ld,
+                                                              static_cast<const S *>(state), static_cast<const S *>(in),
+                                                              static_cast<S *>(out), flags);
+    return qb::check_launch("control_stage");
+}
+
 template <class R>
 int dispatch_command(const qb_params *p, int kind, long long n, long long ld, const void *state, const void *action,
                      void *out, cudaStream_t st) {
@@ -189,6 +227,13 @@ int launch_dynamics_step(const qb_params *p, int kind, int dtype, long long n, l
     const void *a = T > 0 ? actions_seq : action;
     if (dtype == QB_F32) return dispatch_step<float>(p, kind, n, ld, state, a, rotor_out, nonfinite, T, st);
     return dispatch_step<xd>(p, kind, n, ld, state, a, rotor_out, nonfinite, T, st);
+}
+
+int launch_control_stage(const qb_params *p, int stage, int dtype, long long n, long long ld, const void *state,
+                         const void *in, void *out, uint8_t *flags, cudaStream_t st) {
+    if (n == 0) return QB_OK;
+    if (dtype == QB_F32) return dispatch_stage<float>(p, stage, n, ld, state, in, out, flags, st);
+    return dispatch_stage<xd>(p, stage, n, ld, state, in, out, flags, st);
 }
 
 int launch_command(const qb_params *p, int kind, int dtype, long long n, long long ld, const void *state,

@@ -417,6 +417,27 @@ def gen_noise():
     np.savez_compressed(os.path.join(OUT, "env_noise.npz"), **rec)
 
 
+def gen_control():
+    """Controller stages on their own: mixer (incl. saturation), LV/PS -> CTBR."""
+    params, gains = QuadParams(), ControllerGains()
+    rng = np.random.default_rng(21)
+    n = 64
+    force = rng.uniform(2.0, 18.0, n)
+    force[::9] = rng.uniform(-2.0, 40.0, force[::9].shape)  # clamped collectives
+    torque = rng.normal(scale=0.02, size=(n, 3))
+    torque[::4] *= 40.0  # saturating torque requests
+    m = ctl.mixer(force, torque, params)
+    states = random_states(rng, n, params)
+    st = dyn.QuadState.from_vector(states)
+    lv = np.concatenate([rng.normal(scale=3.0, size=(n, 3)), rng.uniform(-np.pi, np.pi, (n, 1))], axis=1)
+    ps = np.concatenate([rng.uniform(-4, 4, (n, 3)), rng.uniform(-np.pi, np.pi, (n, 1))], axis=1)
+    c_lv = ctl.lv_to_ctbr(ctl.command_from_array("lv", lv), st, gains, params)
+    c_ps = ctl.ps_to_ctbr(ctl.command_from_array("ps", ps), st, gains, params)
+    np.savez_compressed(os.path.join(OUT, "control.npz"), force=force, torque=torque, thrusts=m.thrusts,
+                        saturated=m.saturated, states=states, lv=lv, ps=ps, lv_ctbr=c_lv.as_array(),
+                        ps_ctbr=c_ps.as_array())
+
+
 def gen_pgm():
     """sensing.py:238-274 PGM export bytes."""
     import tempfile
@@ -469,9 +490,13 @@ if __name__ == "__main__":
     if len(sys.argv) > 2 and sys.argv[2] == "noise":
         gen_noise()
         sys.exit(0)
+    if len(sys.argv) > 2 and sys.argv[2] == "control":
+        gen_control()
+        sys.exit(0)
     if len(sys.argv) > 2 and sys.argv[2] == "swarm":
         gen_swarm()
         sys.exit(0)
+    gen_control()
     gen_pgm()
     gen_swarm()
     gen_noise()

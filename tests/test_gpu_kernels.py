@@ -278,3 +278,21 @@ def test_nan_action_flags_nonfinite():
         for dt in (torch.float32, torch.float64):
             _, _, bad = run_step(kind, x, acts, dt)
             assert bad.tolist() == [0, 1, 0, 1], (kind, dt)
+
+
+def test_controller_stages_fp64_match_reference():
+    """control.mixer (thrusts + saturated), lv_to_ctbr, ps_to_ctbr, exact double."""
+    from conftest import golden
+    from paper_2407_14783_b200 import control as C
+    from paper_2407_14783_b200.dynamics import QuadState
+
+    g = golden("control")
+    m = C.mixer(g["force"], g["torque"])
+    assert np.array_equal(m.thrusts, g["thrusts"])
+    assert np.array_equal(m.saturated, g["saturated"])
+    st = QuadState(torch.as_tensor(g["states"].T.copy(), device="cuda"))
+    lv = C.lv_to_ctbr(C.command_from_array("lv", g["lv"]), st).as_array()
+    ps = C.ps_to_ctbr(C.command_from_array("ps", g["ps"]), st).as_array()
+    # the attitude construction uses sin/cos of the yaw (CUDA libm vs numpy: <= 1 ulp)
+    np.testing.assert_allclose(lv, g["lv_ctbr"], rtol=1e-13, atol=1e-13)
+    np.testing.assert_allclose(ps, g["ps_ctbr"], rtol=1e-13, atol=1e-13)

@@ -438,6 +438,22 @@ def gen_control():
                         ps_ctbr=c_ps.as_array())
 
 
+def gen_logs():
+    """env/logs.py episode-log bytes."""
+    import tempfile
+
+    from quadsim.env import logs
+
+    rng = np.random.default_rng(5)
+    path = os.path.join(tempfile.mkdtemp(), "ep.jsonl")
+    states, actions, rewards = rng.normal(size=(3, 13)), rng.normal(size=(3, 4)), rng.normal(size=3)
+    with logs.EpisodeLogWriter(path) as w:
+        for i in range(3):
+            w.append(7, i, states[i], actions[i], rewards[i], {"collision": bool(i == 1), "success": False})
+    np.savez_compressed(os.path.join(OUT, "logs.npz"), states=states, actions=actions, rewards=rewards,
+                        log=np.frombuffer(open(path, "rb").read(), np.uint8))
+
+
 def gen_pgm():
     """sensing.py:238-274 PGM export bytes."""
     import tempfile
@@ -497,6 +513,7 @@ if __name__ == "__main__":
         gen_swarm()
         sys.exit(0)
     gen_control()
+    gen_logs()
     gen_pgm()
     gen_swarm()
     gen_noise()

@@ -183,3 +183,16 @@ def test_build_bvh_dropin_layout():
                 assert np.all(node_lo[c] >= node_lo[i]) and np.all(node_hi[c] <= node_hi[i])
                 stack.append(c)
     assert np.all(seen == 1)
+
+
+def test_episode_log_bytes_match_reference(tmp_path):
+    from conftest import golden
+    from paper_2407_14783_b200.env.logs import EpisodeLogWriter, read_episode_log
+
+    g = golden("logs")
+    path = tmp_path / "ep.jsonl"
+    with EpisodeLogWriter(path) as w:
+        w.append_step(7, g["states"], g["actions"], g["rewards"],
+                      {"collision": np.array([False, True, False]), "success": np.zeros(3, bool)})
+    assert np.array_equal(np.frombuffer(path.read_bytes(), np.uint8), g["log"])
+    assert read_episode_log(path)[1]["flags"] == {"collision": True, "success": False}

@@ -286,41 +286,62 @@ def run_env(args, rank, world, kind):
 
 
 def run_e2e(env, world, kind):
-    """Public API end to end: host (pinned) actions in, observations +
-    reward/terminated/truncated back to host memory, every step."""
+    """Public API end to end: host (pinned) numpy actions in, observations +
+    reward/terminated/truncated back to pinned host memory, every step.  The
+    step's outputs are snapshotted on the device (D2D, ~3 TB/s) and read back
+    on a copy stream, so step k+1 computes while step k's results cross PCIe
+    (double-buffered snapshots and host buffers); the timed region ends when
+    the last step's results are in host memory."""
     import torch
 
     from paper_2407_14783_b200.control import CTBR, LV
 
     n = env.num_agents
-    K = 5 if n > 4096 else 50
+    K = 6 if n > 4096 else 50
     rng = np.random.default_rng(0)
     host = [np.ascontiguousarray(np.concatenate([rng.normal(size=(n, 3)), rng.uniform(-3, 3, (n, 1))], 1), np.float32)
             for _ in range(K + 1)]
-    outs = {}
+    copy_stream = torch.cuda.Stream()
+    snap, outs, done = [{}, {}], [{}, {}], [None, None]
 
-    def one(a):
+    def one(k, a):
         cmd = CTBR(a[:, 0] + 9.81, a[:, 1:]) if kind == "c1" else LV(a[:, :3], a[:, 3])
         r = env.step(cmd)
+        b = k % 2
+        if done[b] is not None:  # buffers of step k-2 fully read back
+            torch.cuda.current_stream().wait_event(done[b])
         d2h = 0
         for name, t in list(r.observations.items()) + [("reward", r.reward), ("terminated", r.terminated),
                                                          ("truncated", r.truncated)]:
-            if name not in outs:
-                outs[name] = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
-            outs[name].copy_(t, non_blocking=True)
+            if name not in snap[b]:
+                snap[b][name] = torch.empty(t.shape, dtype=t.dtype, device=t.device)
+                outs[b][name] = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+            snap[b][name].copy_(t)
             d2h += t.numel() * t.element_size()
-        torch.cuda.current_stream().synchronize()
+        ready = torch.cuda.Event()
+        ready.record()
+        copy_stream.wait_event(ready)
+        with torch.cuda.stream(copy_stream):
+            for name, t in snap[b].items():
+                outs[b][name].copy_(t, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record()
+        done[b] = ev
         return a.nbytes, d2h
 
-    one(host[0])
-    barrier(world)
+    one(0, host[0])  # allocate both buffer sets (pinned host allocation is slow) outside the timed region
+    one(1, host[1])
     torch.cuda.synchronize()
+    barrier(world)
     t = time.perf_counter()
     for k in range(K):
-        h2d, d2h = one(host[k + 1])
+        h2d, d2h = one(k + 2, host[k + 1])
+    for ev in done:
+        ev.synchronize()
     dt = max_over_ranks(time.perf_counter() - t, world)
     return {"value": n * world * K / dt, "unit": "env-steps/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-            "steps": K, "path": "env.step(LV numpy) -> observations/reward/flags to pinned host memory"}
+            "steps": K, "path": "env.step(LV numpy) -> observations/reward/flags to pinned host memory "
+                                "(D2H of step k overlaps step k+1)"}
 
 
 def run_dynamics_roofline(pk):

@@ -45,6 +45,8 @@ class Observations(Sequence):
 
     obs["depth"] -> (N,H,W) CUDA tensor; obs[i] -> {"state": (13,), ...} numpy
     dict for agent i (reference layout, float64, segmentation cast to float).
+    The tensors are the env's persistent device buffers: the next step
+    overwrites them (clone, or index obs[i] before stepping, to keep them).
     """
 
     def __init__(self, data: dict, n: int, seg_keys=()):
@@ -186,7 +188,12 @@ class QuadEnvBase:
         self._planes = torch.zeros((17, n), dtype=dt, device=dev)
         self._prev = torch.zeros((17, n), dtype=dt, device=dev) if track_prev else None
         self._action = torch.zeros((n, 4), dtype=dt, device=dev)
-        self._action_host = torch.zeros((n, 4), dtype=dt, pin_memory=True)
+        # host actions go through two pinned staging buffers; a buffer is only
+        # refilled once the device has consumed its previous copy (event), so
+        # a host loop may run ahead of the GPU without corrupting actions
+        self._action_host = [torch.zeros((n, 4), dtype=dt, pin_memory=True) for _ in range(2)]
+        self._action_host_ev = [None, None]
+        self._action_host_i = 0
         self.step_counts = z(n, dtype=torch.int32)
         self.agent_scene = z(n, dtype=torch.int32)
         self._reset_counts = z(n, dtype=torch.int32)
@@ -339,8 +346,16 @@ class QuadEnvBase:
                 return arr
             self._action.copy_(arr)
             return self._action
-        self._action_host.copy_(torch.as_tensor(np.asarray(arr), dtype=self.dtype))
-        self._action.copy_(self._action_host, non_blocking=True)
+        k = self._action_host_i
+        self._action_host_i ^= 1
+        if self._action_host_ev[k] is not None:
+            self._action_host_ev[k].synchronize()
+        buf = self._action_host[k]
+        buf.copy_(torch.as_tensor(np.asarray(arr), dtype=self.dtype))
+        self._action.copy_(buf, non_blocking=True)
+        ev = self._action_host_ev[k] or torch.cuda.Event()
+        ev.record()
+        self._action_host_ev[k] = ev
         return self._action
 
     def step(self, action) -> StepResult:

@@ -418,8 +418,14 @@ __global__ void __launch_bounds__(QB_RF_BLOCK, QB_RF_MINB) k_render_f(DevScene S
 // the lowest id -- does not depend on test order, so ids equal the BVH
 // kernel's and depths agree to FP32 rounding.
 constexpr int CULL_MAX = 256;   // primitives per scene
+#ifndef QB_CULL_MINB
+#define QB_CULL_MINB 5  // measured: 5 blocks (93 regs, no spills) beats 6 (80 regs + spills) by 19%
+#endif
+#ifndef QB_CREC
+#define QB_CREC 64
+#endif
 constexpr int CULL_WARPS = 4;   // warps (cameras) per block
-constexpr int CREC = 64;        // precomputed records per camera (nav room: mean 21, max 58); more use the generic path
+constexpr int CREC = QB_CREC;   // precomputed records per camera (nav room: mean 21, max 58); more use the generic path
 enum { REC_SPHERE = 0, REC_AABB = 1, REC_OBB = 2, REC_GENERIC = 3 };
 
 struct Plane {
@@ -456,7 +462,7 @@ __device__ __forceinline__ float slab_hit(float nlx, float nly, float nlz, float
 }
 
 template <bool FROM_STATE>
-__global__ void __launch_bounds__(CULL_WARPS * 32, 6)
+__global__ void __launch_bounds__(CULL_WARPS * 32, QB_CULL_MINB)
     k_render_cull(DevScene S, CamF cam, long long n, long long ld, const float *state, const float *origins,
                   const float *rotations, const int32_t *env_scene, float *depth, int32_t *seg, int centroid_id,
                   float *centroid, const float *extra, const int32_t *extra_ids, int n_extra, int split) {

@@ -33,29 +33,51 @@ struct ObsArgs {
 #define QB_OBS_MINB 4  // measured: 4 blocks (128 regs) beats 3 (1.7x) and 6-8 (spills)
 #endif
 constexpr int kObsUnroll = QB_OBS_UNROLL;  // (pragma arguments are not macro-expanded)
-constexpr int OBS_WARPS = 4;
+// warps per block: two double-buffered tiles per warp stay under the 48 KB
+// static shared-memory limit (FP64 validation build: 2 warps)
+template <class S> struct ObsWarps {
+    static constexpr int value = sizeof(S) == 8 ? 2 : 4;
+};
 constexpr int TILE_PX = 32;
 
 // tile values are in the observation dtype: every pass rounds its output to
-// S anyway, and the inputs (S depth, int32 ids < 2^24) are exact in S
+// S anyway, and the inputs (S depth, int32 ids < 2^24) are exact in S.  An
+// id tile holds the raw int32 bits until read (cp.async copies bytes).
 template <class S> struct Tile {
     S v[32][TILE_PX + 1];
 };
 
-// warp-cooperative chunk load: tile.v[e][l] = value of pixel c0 + l of env e0 + e
+template <class S> __device__ __forceinline__ S tile_val(const Tile<S> &t, int e, int k, bool ids) {
+    return ids ? (S) * reinterpret_cast<const int32_t *>(&t.v[e][k]) : t.v[e][k];
+}
+
+// asynchronous warp-cooperative chunk load (cp.async, no registers held):
+// tile.v[e][l] <- pixel c0 + l of env e0 + e; the caller commits / waits
 template <class S>
-__device__ __forceinline__ void tile_load(Tile<S> &t, const void *img, bool ids, long long e0, long long n, long long hw,
-                                          long long c0, int lane) {
+__device__ __forceinline__ void tile_load_async(Tile<S> &t, const void *img, bool ids, long long e0, long long n,
+                                                long long hw, long long c0, int lane) {
     const long long k = c0 + lane;
-#pragma unroll kObsUnroll
-    for (int e = 0; e < 32; ++e) {  // loads in flight
-        S v = S(0);
+#pragma unroll 8
+    for (int e = 0; e < 32; ++e) {
+        S *dst = &t.v[e][lane];
         if (e0 + e < n && k < hw) {
             const long long off = (e0 + e) * hw + k;
-            v = ids ? (S) static_cast<const int32_t *>(img)[off] : static_cast<const S *>(img)[off];
+            const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+            if (ids)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(static_cast<const int32_t *>(img) + off));
+            else if (sizeof(S) == 4)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(static_cast<const S *>(img) + off));
+            else
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(static_cast<const S *>(img) + off));
+        } else {
+            *dst = S(0);
         }
-        t.v[e][lane] = v;
     }
+    asm volatile("cp.async.commit_group;\n" ::);
+}
+
+__device__ __forceinline__ void tile_wait_all_but_last() {
+    asm volatile("cp.async.wait_group 1;\n" ::);
     __syncwarp();
 }
 
@@ -77,20 +99,25 @@ __device__ __forceinline__ void tile_store(const Tile<S> &t, S *img, long long e
 // its output's range), else an extra read pass computes it; on return it
 // holds this pass's output range.
 template <class S>
-__device__ void noise_pass(const qb_noise &nz, Pcg64 &r, bool live, const void *in, bool in_ids, S *out, Tile<S> &t,
+__device__ void noise_pass(const qb_noise &nz, Pcg64 &r, bool live, const void *in, bool in_ids, S *out, Tile<S> *t,
                            long long e0, long long n, long long hw, int me, double2 &range, bool &have_range) {
     const int lane = me;
+    const long long nchunk = (hw + TILE_PX - 1) / TILE_PX;
     // image reductions first (saltpepper: min / max, redwood: max)
     double lo = range.x, hi = range.y;
     const bool sp = nz.kind == QB_NOISE_SALTPEPPER && nz.p != 0.0, rw = nz.kind == QB_NOISE_REDWOOD;
     if ((sp || rw) && !have_range) {
-        for (long long c0 = 0; c0 < hw; c0 += TILE_PX) {
-            tile_load<S>(t, in, in_ids, e0, n, hw, c0, lane);
-            const int m = hw - c0 < TILE_PX ? (int)(hw - c0) : TILE_PX;
+        tile_load_async<S>(t[0], in, in_ids, e0, n, hw, 0, lane);
+        for (long long c = 0; c < nchunk; ++c) {
+            if (c + 1 < nchunk) tile_load_async<S>(t[(c + 1) & 1], in, in_ids, e0, n, hw, (c + 1) * TILE_PX, lane);
+            else asm volatile("cp.async.commit_group;\n" ::);
+            tile_wait_all_but_last();
+            const Tile<S> &tc = t[c & 1];
+            const int m = hw - c * TILE_PX < TILE_PX ? (int)(hw - c * TILE_PX) : TILE_PX;
             for (int k = 0; k < m; ++k) {
-                const double v = (double)t.v[me][k];
-                lo = (c0 == 0 && k == 0) ? v : fmin(lo, v);
-                hi = (c0 == 0 && k == 0) ? v : fmax(hi, v);
+                const double v = (double)tile_val(tc, me, k, in_ids);
+                lo = (c == 0 && k == 0) ? v : fmin(lo, v);
+                hi = (c == 0 && k == 0) ? v : fmax(hi, v);
             }
             __syncwarp();
         }
@@ -99,12 +126,18 @@ __device__ void noise_pass(const qb_noise &nz, Pcg64 &r, bool live, const void *
     if (sp && live) pcg64_advance(rs, (u128)hw);
     const double floor_disp = hw > 0 ? __ddiv_rn(1.0, __dadd_rn(hi, 1.0)) : 1e-6;
     double olo = 0.0, ohi = 0.0;
-    for (long long c0 = 0; c0 < hw; c0 += TILE_PX) {
-        tile_load<S>(t, in, in_ids, e0, n, hw, c0, lane);
+    tile_load_async<S>(t[0], in, in_ids, e0, n, hw, 0, lane);
+    for (long long c = 0; c < nchunk; ++c) {
+        // prefetch the next chunk while this one is computed and stored
+        if (c + 1 < nchunk) tile_load_async<S>(t[(c + 1) & 1], in, in_ids, e0, n, hw, (c + 1) * TILE_PX, lane);
+        else asm volatile("cp.async.commit_group;\n" ::);
+        tile_wait_all_but_last();
+        Tile<S> &tc = t[c & 1];
+        const long long c0 = c * TILE_PX;
         const int m = hw - c0 < TILE_PX ? (int)(hw - c0) : TILE_PX;
         if (live) {
             for (int k = 0; k < m; ++k) {
-                const double v = (double)t.v[me][k];
+                const double v = (double)tile_val(tc, me, k, in_ids);
                 double o = v;
                 switch (nz.kind) {
                     case QB_NOISE_NORMAL:  // values + sigma * standard_normal
@@ -134,12 +167,12 @@ __device__ void noise_pass(const qb_noise &nz, Pcg64 &r, bool live, const void *
                 }
                 const S so = (S)o;  // each pass stores in the observation dtype
                 const double os = (double)so;
-                t.v[me][k] = so;
-                olo = (c0 == 0 && k == 0) ? os : fmin(olo, os);
-                ohi = (c0 == 0 && k == 0) ? os : fmax(ohi, os);
+                tc.v[me][k] = so;
+                olo = (c == 0 && k == 0) ? os : fmin(olo, os);
+                ohi = (c == 0 && k == 0) ? os : fmax(ohi, os);
             }
-        }
-        tile_store<S>(t, out, e0, n, hw, c0, lane);
+        }  // (rows of envs beyond n are never stored)
+        tile_store<S>(tc, out, e0, n, hw, c0, lane);
     }
     if (sp && live) r = rs;
     range = make_double2(olo, ohi);
@@ -168,9 +201,9 @@ template <class S> __device__ void imu_read(const DynConsts<xd> &C, const S *st,
 }
 
 template <class S>
-__global__ void __launch_bounds__(OBS_WARPS * 32, QB_OBS_MINB) k_env_observe(DynConsts<xd> C, qb_env_buffers B, ObsArgs O) {
-    __shared__ Tile<S> tiles[OBS_WARPS];
-    Tile<S> &t = tiles[threadIdx.x >> 5];
+__global__ void __launch_bounds__(ObsWarps<S>::value * 32, QB_OBS_MINB) k_env_observe(DynConsts<xd> C, qb_env_buffers B, ObsArgs O) {
+    __shared__ Tile<S> tiles[ObsWarps<S>::value][2];
+    Tile<S> *t = tiles[threadIdx.x >> 5];
     const int lane = threadIdx.x & 31;
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long e0 = i - lane;  // first env of this warp
@@ -195,8 +228,14 @@ __global__ void __launch_bounds__(OBS_WARPS * 32, QB_OBS_MINB) k_env_observe(Dyn
         const bool ids = so.kind == QB_SENSOR_SEGMENTATION;
         if (so.n_noise == 0) {  // plain copy into the observation dtype
             for (long long c0 = 0; c0 < hw; c0 += TILE_PX) {
-                tile_load<S>(t, so.src, ids, e0, B.n, hw, c0, lane);
-                tile_store<S>(t, out, e0, B.n, hw, c0, lane);
+                tile_load_async<S>(t[0], so.src, ids, e0, B.n, hw, c0, lane);
+                asm volatile("cp.async.wait_group 0;\n" ::);
+                __syncwarp();
+                if (ids) {
+                    const int m = hw - c0 < TILE_PX ? (int)(hw - c0) : TILE_PX;
+                    for (int k = 0; k < m; ++k) t[0].v[lane][k] = tile_val(t[0], lane, k, true);
+                }
+                tile_store<S>(t[0], out, e0, B.n, hw, c0, lane);
             }
             continue;
         }
@@ -260,11 +299,13 @@ int launch_observe(const qb_params *p, const qb_env_buffers *b, int n_sensors, c
     }
     if (b->n == 0 || n_sensors == 0) return QB_OK;
     DynConsts<xd> C = make_consts<xd>(*p);
-    const int BS = OBS_WARPS * 32;
-    if (b->dtype == QB_F32)
+    if (b->dtype == QB_F32) {
+        const int BS = ObsWarps<float>::value * 32;
         k_env_observe<float><<<env_grid(b->n, BS), BS, 0, st>>>(C, *b, O);
-    else
+    } else {
+        const int BS = ObsWarps<double>::value * 32;
         k_env_observe<double><<<env_grid(b->n, BS), BS, 0, st>>>(C, *b, O);
+    }
     return check_launch("env_observe");
 }
 

@@ -424,7 +424,10 @@ constexpr int CULL_MAX = 256;   // primitives per scene
 #ifndef QB_CREC
 #define QB_CREC 64
 #endif
-constexpr int CULL_WARPS = 4;   // warps (cameras) per block
+#ifndef QB_CULL_WARPS
+#define QB_CULL_WARPS 4
+#endif
+constexpr int CULL_WARPS = QB_CULL_WARPS;  // warps (cameras) per block
 constexpr int CREC = QB_CREC;   // precomputed records per camera (nav room: mean 21, max 58); more use the generic path
 enum { REC_SPHERE = 0, REC_AABB = 1, REC_OBB = 2, REC_GENERIC = 3 };
 

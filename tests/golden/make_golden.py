@@ -438,6 +438,29 @@ def gen_control():
                         ps_ctbr=c_ps.as_array())
 
 
+def multiscene_config():
+    """Three scenes (garage + two cluttered rooms), shuffled assignment, a
+    depth + segmentation camera, CTBR (FP64-exact controller), short episodes."""
+    return EnvConfig(
+        num_agents=9, command_type="ctbr", episode_max_steps=15, scene_sampling="shuffled",
+        scenes=(SceneSpec(kind="garage"), SceneSpec(kind="cluttered", seed=3, density=0.2),
+                SceneSpec(kind="cluttered", seed=8, density=0.12)),
+        randomization=InitRandomization(position=DistSpec("uniform", low=[-3.5, -3.5, 0.8], high=[3.5, 3.5, 3.0])),
+        sensors=(SensorSpec(kind="depth", name="depth", width=32, height=24),
+                 SensorSpec(kind="segmentation", name="vision", width=32, height=24)))
+
+
+def gen_multiscene():
+    env = tasks.make_env(multiscene_config())
+
+    def ctbr(rng, t, n):
+        return np.concatenate([rng.uniform(5.0, 15.0, (n, 1)), rng.normal(scale=3.0, size=(n, 3))], axis=1)
+
+    rec = record_env(env, ctbr, 50, seed=11, keep_images=(0, 16, 49))
+    np.savez_compressed(os.path.join(OUT, "env_multiscene.npz"), **rec)
+    print("multiscene scenes", np.unique(rec["scene"]), "respawns", int(rec["truncated"].sum() + rec["terminated"].sum()))
+
+
 def gen_logs():
     """env/logs.py episode-log bytes."""
     import tempfile
@@ -506,12 +529,16 @@ if __name__ == "__main__":
     if len(sys.argv) > 2 and sys.argv[2] == "noise":
         gen_noise()
         sys.exit(0)
+    if len(sys.argv) > 2 and sys.argv[2] == "multiscene":
+        gen_multiscene()
+        sys.exit(0)
     if len(sys.argv) > 2 and sys.argv[2] == "control":
         gen_control()
         sys.exit(0)
     if len(sys.argv) > 2 and sys.argv[2] == "swarm":
         gen_swarm()
         sys.exit(0)
+    gen_multiscene()
     gen_control()
     gen_logs()
     gen_pgm()

@@ -186,3 +186,30 @@ def test_auto_reset_and_truncation_semantics():
     assert bool(r.truncated.all()) and int(env.step_counts.max()) == 3
     r = env.step(LV(a[:, :3], a[:, 3]))
     assert int(env.step_counts.max()) == 1 and not bool(r.truncated.any())
+
+
+def test_multiscene_episode_fp64_replay():
+    """Three scenes in one device handle, shuffled assignment and per-respawn
+    rotation (base.py:97-100, 118-121): states, scene ids, flags and the
+    per-scene depth / segmentation images of the reference episode."""
+    from test_oracle import multiscene_config
+
+    g = golden("env_multiscene")
+    cfg = multiscene_config()
+    env = make_env(cfg, dtype=torch.float64)
+    env.reset(seed=11)
+    assert np.array_equal(_planes_np(env), g["reset_full_state"])
+    worst = 0.0
+    for t in range(g["actions"].shape[0]):
+        res = env.step(command_from_array("ctbr", g["actions"][t]))
+        worst = max(worst, state_error(_planes_np(env), g["full_state"][t]).max())
+        assert np.array_equal(env.agent_scene.cpu().numpy(), g["scene"][t]), t
+        assert np.array_equal(res.terminated.cpu().numpy(), g["terminated"][t]), t
+        assert np.array_equal(res.truncated.cpu().numpy(), g["truncated"][t]), t
+        assert np.array_equal(env.collision.cpu().numpy(), g["collision"][t]), t
+        for key in g.files:
+            if key.startswith("img_") and key.endswith(f"_{t}"):
+                sensor = key[4:].rsplit("_", 1)[0]
+                img = res.observations[sensor].double().cpu().numpy()
+                assert np.array_equal(img, g[key]), (key, int((img != g[key]).sum()))
+    assert worst < 1e-12, worst

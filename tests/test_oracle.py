@@ -326,3 +326,21 @@ def test_env_swarm_gap_crossing_replay():
     for t in range(g["actions"].shape[0]):
         obs = env.step(g["actions"][t])[0]
         assert np.array_equal(obs["swarm"], g["swarm_obs"][t + 1]), t
+
+
+def multiscene_config():
+    """make_golden.py multiscene_config: 3 scenes, shuffled assignment, depth + segmentation, CTBR."""
+    from paper_2407_14783_b200.env import DistSpec, EnvConfig, InitRandomization, SceneSpec, SensorSpec
+
+    return EnvConfig(
+        num_agents=9, command_type="ctbr", episode_max_steps=15, scene_sampling="shuffled",
+        scenes=(SceneSpec(kind="garage"), SceneSpec(kind="cluttered", seed=3, density=0.2),
+                SceneSpec(kind="cluttered", seed=8, density=0.12)),
+        randomization=InitRandomization(position=DistSpec("uniform", low=[-3.5, -3.5, 0.8], high=[3.5, 3.5, 3.0])),
+        sensors=(SensorSpec(kind="depth", name="depth", width=32, height=24),
+                 SensorSpec(kind="segmentation", name="vision", width=32, height=24)))
+
+
+def test_env_multiscene_replay():
+    """Shuffled scene permutation, per-respawn scene rotation, per-scene renders."""
+    _replay("env_multiscene", multiscene_config(), 11, ["garage", "c3", "c8"])

@@ -428,6 +428,7 @@ constexpr int CULL_MAX = 256;   // primitives per scene
 #define QB_CULL_WARPS 4
 #endif
 constexpr int CULL_WARPS = QB_CULL_WARPS;  // warps (cameras) per block
+constexpr int XMAX = 32;  // swarm spheres kept per camera after frustum culling (more: every sphere per ray)
 constexpr int CREC = QB_CREC;   // precomputed records per camera (nav room: mean 21, max 58); more use the generic path
 enum { REC_SPHERE = 0, REC_AABB = 1, REC_OBB = 2, REC_GENERIC = 3 };
 
@@ -464,12 +465,17 @@ __device__ __forceinline__ float slab_hit(float nlx, float nly, float nlz, float
     return -1.0f;
 }
 
-template <bool FROM_STATE>
+// EXTRA: swarm spheres present (separate instance: no swarm shared memory or
+// registers in the common case)
+template <bool FROM_STATE, bool EXTRA>
 __global__ void __launch_bounds__(CULL_WARPS * 32, QB_CULL_MINB)
     k_render_cull(DevScene S, CamF cam, long long n, long long ld, const float *state, const float *origins,
                   const float *rotations, const int32_t *env_scene, float *depth, int32_t *seg, int centroid_id,
                   float *centroid, const float *extra, const int32_t *extra_ids, int n_extra, int split) {
     __shared__ int cand_s[CULL_WARPS][CULL_MAX];
+    constexpr int XM = EXTRA ? XMAX : 1;
+    __shared__ float4 xcs_s[CULL_WARPS][XM];             // swarm spheres in the frustum: camera-space centre, r
+    __shared__ int xk_s[CULL_WARPS][XM];                 // ... and their index k (ascending)
     __shared__ float4 rec_s[CULL_WARPS][CREC][4];      // shading records (warp-broadcast reads)
     __shared__ int2 met_s[CULL_WARPS][CREC];           // (record type, object id)
     __shared__ float cul_s[CULL_WARPS][13][CREC];      // culling bounds, SoA (conflict-free lane-parallel reads)
@@ -592,6 +598,46 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, QB_CULL_MINB)
                 const float cv[13] = {c0.w, cc.x, cc.y, cc.z, A0.x, A0.y, A0.z, A1.x, A1.y, A1.z, A2.x, A2.y, A2.z};
 #pragma unroll
                 for (int q = 0; q < 13; ++q) cul[q][k] = cv[q];
+            }
+            __syncwarp();
+        }
+
+        // swarm agents as spheres (kernels.py:438-445): keep the ones in the
+        // camera frustum, in ascending k (ties go to the lowest k), with their
+        // camera-space centres for the per-tile test
+        int nx = 0;             // warp-uniform
+        bool x_all = false;     // too many in view: test every sphere per ray
+        if (EXTRA && n_extra > 0) {
+            const Plane cp[6] = {world_plane(Rw, 1.f, 0.f, cam.th, 0.f), world_plane(Rw, -1.f, 0.f, cam.th, 0.f),
+                                 world_plane(Rw, 0.f, 1.f, cam.tv, 0.f), world_plane(Rw, 0.f, -1.f, cam.tv, 0.f),
+                                 world_plane(Rw, 0.f, 0.f, 1.f, 0.f), world_plane(Rw, 0.f, 0.f, -1.f, cam.max_range)};
+            const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int b = 0; b < n_extra && !x_all; b += 32) {
+                const int k = b + lane;
+                bool in = false;
+                float4 sph = z4;
+                if (k < n_extra) {
+                    sph = *reinterpret_cast<const float4 *>(extra + (c * n_extra + k) * 4);
+                    const float rx = sph.x - o[0], ry = sph.y - o[1], rz = sph.z - o[2];
+                    in = true;
+#pragma unroll
+                    for (int q = 0; q < 6; ++q) in = in && keep(cp[q], rx, ry, rz, sph, z4, z4, z4);
+                    if (in) {  // camera space: v' = Rw^T v
+                        sph = make_float4(Rw[0] * rx + Rw[3] * ry + Rw[6] * rz, Rw[1] * rx + Rw[4] * ry + Rw[7] * rz,
+                                          Rw[2] * rx + Rw[5] * ry + Rw[8] * rz, sph.w);
+                    }
+                }
+                const unsigned m = __ballot_sync(FULL, in);
+                if (nx + __popc(m) > XM) {
+                    x_all = true;
+                } else {
+                    if (in) {
+                        const int pos = nx + __popc(m & lt_mask);
+                        xcs_s[wib][pos] = sph;
+                        xk_s[wib][pos] = k;
+                    }
+                    nx += __popc(m);
+                }
             }
             __syncwarp();
         }
@@ -735,20 +781,42 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, QB_CULL_MINB)
                         }
                 }
             }
+            float tt[2];
+            int to[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const bool hit = bid[u] != 0x7fffffff;
+                tt[u] = hit ? best[u] : -1.0f;
+                to[u] = hit ? bid[u] : -1;
+            }
+            // swarm agents as spheres after the scene (kernels.py:438-445): a
+            // sphere replaces the scene hit only when strictly nearer
+            auto sphere_test = [&](int k) {
+                const float4 sph = *reinterpret_cast<const float4 *>(extra + (c * n_extra + k) * 4);
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const float ts = ray_sphere_v(sph, sph.w * sph.w, o[0], o[1], o[2], dx[u], dy[u], dz[u], tmin, tmx[u]);
+                    if (ts > 0.0f && (tt[u] < 0.0f || ts < tt[u])) {
+                        tt[u] = ts;
+                        to[u] = extra_ids[c * n_extra + k];
+                    }
+                }
+            };
+            if (!EXTRA) {
+            } else if (x_all) {
+                for (int k = 0; k < n_extra; ++k) sphere_test(k);
+            } else if (nx > 0) {  // tile-cull the frustum survivors (sphere support = r), ascending k
+                const float4 sp = xcs_s[wib][lane < nx ? lane : 0];
+                const bool tin = lane < nx && (sp.x - xl * sp.z) * iL + sp.w >= -CULL_EPS &&
+                                 (xr * sp.z - sp.x) * iR + sp.w >= -CULL_EPS && (sp.y - yt * sp.z) * iT + sp.w >= -CULL_EPS &&
+                                 (yb * sp.z - sp.y) * iB + sp.w >= -CULL_EPS;
+                for (unsigned m = __ballot_sync(FULL, tin); m; m &= m - 1) sphere_test(xk_s[wib][__ffs(m) - 1]);
+            }
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
                 const int i = ii[u];
-                const bool hit = bid[u] != 0x7fffffff;
-                float t = hit ? best[u] : -1.0f;
-                int oid = hit ? bid[u] : -1;
-                for (int k = 0; k < n_extra; ++k) {  // swarm agents as spheres (kernels.py:438-445)
-                    const float4 sph = *reinterpret_cast<const float4 *>(extra + (c * n_extra + k) * 4);
-                    float ts = ray_sphere_v(sph, sph.w * sph.w, o[0], o[1], o[2], dx[u], dy[u], dz[u], tmin, tmx[u]);
-                    if (ts > 0.0f && (t < 0.0f || ts < t)) {
-                        t = ts;
-                        oid = extra_ids[c * n_extra + k];
-                    }
-                }
+                const float t = tt[u];
+                const int oid = to[u];
                 const int out_id = t > 0.0f ? oid : 0;
                 if (j < W && i < H) {
                     const int off = i * W + j;
@@ -912,14 +980,18 @@ int launch_render(const qb_scene *s, const qb_camera *cam, int dtype, long long 
             long long blocks = (n * split + CULL_WARPS - 1) / CULL_WARPS;
             long long max_blocks = (long long)sm_count() * 16;
             if (blocks > max_blocks) blocks = max_blocks;
-            if (state)
-                k_render_cull<true><<<(int)blocks, B, 0, st>>>(s->dev, c, n, ld, (const float *)state, nullptr, nullptr,
-                                                               env_scene, (float *)depth, seg, centroid_id, centroid,
-                                                               (const float *)extra, extra_ids, n_extra, split);
-            else
-                k_render_cull<false><<<(int)blocks, B, 0, st>>>(s->dev, c, n, ld, nullptr, (const float *)origins,
-                                                                (const float *)rotations, env_scene, (float *)depth, seg, 0,
-                                                                nullptr, (const float *)extra, extra_ids, n_extra, split);
+#define QB_CULL(FS, EX)                                                                                         \
+    k_render_cull<FS, EX><<<(int)blocks, B, 0, st>>>(s->dev, c, n, ld, FS ? (const float *)state : nullptr,         \
+                                                     FS ? nullptr : (const float *)origins,                         \
+                                                     FS ? nullptr : (const float *)rotations, env_scene, (float *)depth, \
+                                                     seg, FS ? centroid_id : 0, FS ? centroid : nullptr,             \
+                                                     (const float *)extra, extra_ids, n_extra, split)
+            if (state) {
+                if (n_extra > 0) QB_CULL(true, true); else QB_CULL(true, false);
+            } else {
+                if (n_extra > 0) QB_CULL(false, true); else QB_CULL(false, false);
+            }
+#undef QB_CULL
             int rc = check_launch("render_cull_f32");
             if (rc || split == 1 || centroid_id <= 0) return rc;
             k_centroid<<<env_grid(n, 128), 128, 0, st>>>(n, c.W, c.H, seg, centroid_id, centroid);

@@ -344,6 +344,48 @@ def run_e2e(env, world, kind):
                                 "(D2H of step k overlaps step k+1)"}
 
 
+def run_env_step_roofline(pk):
+    """K1+K3 fused env step alone (qb_env_step) at 4M envs, free flight in the
+    garage: per env-step it reads the state (68 B) + action (16 B) + step
+    count, scene, respawn flag (9 B) and writes state + prev_state (136 B),
+    7 flags, reward, nearest distance + point (7 + 4 + 32 B), step count (4 B):
+    272 algorithmic B/env-step; the exact-double proximity query and reward
+    are computed, not read.  L2 (126 MB) << the 1.1 GB of planes touched."""
+    import torch
+
+    import paper_2407_14783_b200._native as nat
+    from paper_2407_14783_b200.env import EnvConfig, make_env
+
+    n = 1 << 22
+    env = make_env(EnvConfig(num_agents=n, command_type="ctbr", episode_max_steps=10**6))
+    env.reset(seed=0)
+    act = torch.zeros((n, 4), device="cuda")
+    act[:, 0] = 9.81
+    act[:, 1:] = torch.randn((n, 3), device="cuda") * 0.3
+    env._bufs.action = act.data_ptr()
+
+    def launch():
+        nat.check(nat.lib().qb_env_step(env._P, env._kind, env._task, env.dev_scenes.handle, env._bufs, nat.stream_of()))
+
+    for _ in range(3):
+        launch()
+    ev = []
+    for _ in range(10):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        launch()
+        b.record()
+        ev.append((a, b))
+    torch.cuda.synchronize()
+    ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
+    gbs = n * 272 / (ms / 1e3) / 1e9
+    del env
+    return {"bound": "hbm", "achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": gbs / pk["hbm_gbs"],
+            "traffic": None, "envs": n, "ms": ms, "env_steps_per_sec": n / (ms / 1e3),
+            "note": "K1+K3 fused env step (CTBR, RK4 x2, exact-double nearest point over the garage, flags, reward), "
+                    "272 algorithmic B/env-step"}
+
+
 def run_dynamics_roofline(pk):
     """K1 alone at 16.7M envs: 152 B/env-step (read 17 + 4 floats, write 17)."""
     import torch
@@ -565,9 +607,14 @@ def main():
                 "traffic": traffic * r["n"] if traffic else None,
                 "note": (f"dominant kernel K2 render ({r['render_ms']:.3f} of {r['ms'] / args.steps:.3f} ms/step): "
                          f"algorithmic bytes = depth+seg writes + pose reads; the kernel is SM-issue-bound "
-                         f"(see profiles/ncu_summary.json), peak = {pk_kind} HBM copy bandwidth")}
+                         f"(see profiles/ncu_summary.json), peak = {pk_kind} HBM copy bandwidth"),
+                # the renderer's own figures: rays/s of the kernel and its SM / cache counters (ncu)
+                "rays_per_s": r["n"] * 64 * 64 / (r["render_ms"] / 1e3),
+                "ncu": {k: meta[k] for k in ("issue_active_pct", "warps_active_pct", "l1_hit_pct", "l2_hit_pct",
+                                             "registers", "source") if k in meta} if meta else None}
         if rank == 0:
             line["roofline_dynamics"] = run_dynamics_roofline(pk)
+            line["roofline_env_step"] = run_env_step_roofline(pk)
             if args.cpu:
                 ns = min(1024, ENVS[kind])
                 steps = 12 if ns > 100 else 400

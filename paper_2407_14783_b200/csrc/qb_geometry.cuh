@@ -173,6 +173,40 @@ QB_D NearestResult nearest_point(const DevScene &S, int scene, double qx_, doubl
     return {bx.v, by.v, bz.v, best.v, best_id};
 }
 
+// Per-thread nearest point for tiny scenes (<= NEAREST_SCAN_MAX primitives,
+// e.g. the 6-box garage): a straight scan in primitive order with the same
+// (d2, lowest id, first primitive) result as the BVH walk, without its
+// local-memory stack and node tests.
+constexpr int NEAREST_SCAN_MAX = 16;
+QB_D NearestResult nearest_point_scan(const DevScene &S, int p0, int p1, double qx_, double qy_, double qz_) {
+    xd qx(qx_), qy(qy_), qz(qz_);
+    double best = infinity_d();
+    int best_id = -1;
+    double bx = 0.0, by = 0.0, bz = 0.0;
+    for (int p = p0; p < p1; ++p) {
+        const int2 m = __ldg(S.meta + p);
+        const double *dd = S.primd + 16 * p;
+        xd d[15];
+#pragma unroll
+        for (int k = 0; k < 15; ++k) d[k] = xd(__ldg(dd + k));
+        V3<xd> c;
+        if (m.x == QB_SPHERE)
+            c = closest_on_sphere<xd>(d[0], d[1], d[2], d[3], qx, qy, qz);
+        else if (m.x == QB_BOX)
+            c = closest_on_box<xd>(d, qx, qy, qz);
+        else
+            c = closest_on_triangle<xd>(d, qx, qy, qz);
+        xd ex = qx - c.x, ey = qy - c.y, ez = qz - c.z;
+        const double pd2 = (ex * ex + ey * ey + ez * ez).v;
+        if (pd2 < best || (pd2 == best && m.y < best_id)) {
+            best = pd2;
+            best_id = m.y;
+            bx = c.x.v; by = c.y.v; bz = c.z.v;
+        }
+    }
+    return {bx, by, bz, best, best_id};
+}
+
 // Warp-cooperative nearest point for small scenes (<= NEAREST_BRUTE_MAX
 // primitives): the 32 lanes split the scene's primitives, each keeps its best
 // (d2, object id, primitive) and a shuffle argmin picks the winner -- the same

@@ -19,6 +19,10 @@
 #include "qb_internal.h"
 #include "qb_rng.cuh"
 
+#ifndef QB_ENV_MINB
+#define QB_ENV_MINB 5  // measured: 5 blocks beats 4 and uncapped (K1+K3 at 45% of HBM at 4M envs)
+#endif
+
 namespace {
 
 template <class R> struct EnvArgs {
@@ -64,10 +68,13 @@ template <class R> __device__ __forceinline__ void hover_state(const DynConsts<R
 // nearest point of one env's query: per thread (BVH walk) or, in the
 // warp-per-env kernels, warp-cooperative
 template <bool WARP> __device__ __forceinline__ NearestResult nearest_q(const DevScene &S, int scene, const double *q) {
-    if constexpr (WARP)
+    if constexpr (WARP) {
         return nearest_point_warp(S, scene, q[0], q[1], q[2]);
-    else
+    } else {
+        const int p0 = __ldg(S.prim_offset + scene), p1 = __ldg(S.prim_offset + scene + 1);
+        if (p1 - p0 <= NEAREST_SCAN_MAX) return nearest_point_scan(S, p0, p1, q[0], q[1], q[2]);
         return nearest_point(S, scene, q[0], q[1], q[2]);
+    }
 }
 
 __device__ __forceinline__ xd norm3(xd a, xd b, xd c) { return r_sqrt(a * a + b * b + c * c); }
@@ -349,7 +356,7 @@ __global__ void k_swarm_views(EnvArgs<R> A, typename storage_of<R>::type *sphere
         for (int c = 0; c < 13; ++c) obs[idx * 13 + c] = st[c * B.ld + j];
 }
 
-template <class R, int KIND, bool WARP> __global__ void __launch_bounds__(128) k_env_step(EnvArgs<R> A) {
+template <class R, int KIND, bool WARP> __global__ void __launch_bounds__(128, QB_ENV_MINB) k_env_step(EnvArgs<R> A) {
     using S = typename storage_of<R>::type;
     bool lead;
     const long long i = env_index<WARP>(lead);

@@ -5,7 +5,7 @@ import argparse
 import torch
 
 ap = argparse.ArgumentParser()
-ap.add_argument("mode", choices=["nav", "indoor", "dyn", "bptt", "hover", "noise"])
+ap.add_argument("mode", choices=["nav", "indoor", "dyn", "bptt", "hover", "noise", "envbig"])
 ap.add_argument("--envs", type=int, default=16384)
 a = ap.parse_args()
 if a.mode in ("nav", "indoor"):
@@ -34,6 +34,17 @@ elif a.mode == "noise":  # config 3 + the c3n sensor noise chains
     act[:, 0] = 1.0
     for _ in range(3):
         env.step(LV(act[:, :3], act[:, 3]))
+elif a.mode == "envbig":  # the bench's K1+K3 roofline workload (free flight, garage)
+    import paper_2407_14783_b200._native as nat
+    from paper_2407_14783_b200.env import EnvConfig, make_env
+
+    env = make_env(EnvConfig(num_agents=a.envs, command_type="ctbr", episode_max_steps=10**6))
+    env.reset(seed=0)
+    act = torch.zeros((a.envs, 4), device="cuda")
+    act[:, 0] = 9.81
+    env._bufs.action = act.data_ptr()
+    for _ in range(3):
+        nat.check(nat.lib().qb_env_step(env._P, env._kind, env._task, env.dev_scenes.handle, env._bufs, nat.stream_of()))
 elif a.mode == "hover":  # config 1: 100 envs, CTBR, default scene, no sensors
     from paper_2407_14783_b200.control import CTBR
     from paper_2407_14783_b200.env import EnvConfig, make_env

@@ -155,46 +155,49 @@ def profile_traffic(kernel_key):
 # ---------------------------------------------------------------- our arm
 
 
-def env_workload(kind, rank, world, total):
-    from paper_2407_14783_b200.env import (DistSpec, EnvConfig, InitRandomization, SceneSpec, SensorSpec, make_env,
-                                           navigation_config)
+def workload_config(kind, n):
+    """The EnvConfig of a workload for n agents (one swarm of n for 'swarm')."""
+    import dataclasses
+
+    from paper_2407_14783_b200.env import (DistSpec, EnvConfig, InitRandomization, SceneSpec, SensorSpec,
+                                           gap_crossing_config, navigation_config)
+    from paper_2407_14783_b200.sensing import NoiseSpec
 
     if kind == "c1":
-        cfg = EnvConfig(num_agents=total, command_type="ctbr", episode_max_steps=1000)
-    elif kind == "c2":
-        cfg = navigation_config(scene_seed=0, num_agents=total)
-    elif kind == "c3":
-        cfg = navigation_config(scene_seed=0, num_agents=total, with_segmentation=True)
-    elif kind == "c3n":
-        import dataclasses
-
-        from paper_2407_14783_b200.sensing import NoiseSpec
-
-        cfg = navigation_config(scene_seed=0, num_agents=total, with_segmentation=True)
-        cfg = dataclasses.replace(cfg, sensors=(
+        return EnvConfig(num_agents=n, command_type="ctbr", episode_max_steps=1000)
+    if kind == "c2":
+        return navigation_config(scene_seed=0, num_agents=n)
+    if kind == "c3":
+        return navigation_config(scene_seed=0, num_agents=n, with_segmentation=True)
+    if kind == "c3n":
+        cfg = navigation_config(scene_seed=0, num_agents=n, with_segmentation=True)
+        return dataclasses.replace(cfg, sensors=(
             SensorSpec(kind="depth", name="depth", noise=(NoiseSpec("normal", sigma=0.02),
                                                           NoiseSpec("redwood", sigma_disparity=0.002))),
             SensorSpec(kind="segmentation", name="vision", noise=(NoiseSpec("saltpepper", p=0.02),)),
             SensorSpec(kind="imu", name="imu", noise=(NoiseSpec("normal", sigma=0.05),))))
-    elif kind == "swarm":
-        import dataclasses
-
-        from paper_2407_14783_b200.env import gap_crossing_config
-
-        # one swarm per rank (swarms do not shard: every agent sees every other)
-        cfg = gap_crossing_config(num_agents=total // world)
-        cfg = dataclasses.replace(cfg, randomization=InitRandomization(
+    if kind == "swarm":
+        cfg = gap_crossing_config(num_agents=n)
+        return dataclasses.replace(cfg, randomization=InitRandomization(
             position=DistSpec("uniform", low=[-5.5, -5.5, 0.5], high=[-1.0, 5.5, 3.5])))
+    if kind == "c5":
+        return EnvConfig(num_agents=n, task="landing", command_type="lv", episode_max_steps=512,
+                         scenes=(SceneSpec(kind="indoor", seed=0),),
+                         randomization=InitRandomization(position=DistSpec("uniform", low=[-12, -12, 1.0],
+                                                                           high=[12, 12, 4.5])),
+                         min_spawn_clearance=0.3,
+                         sensors=(SensorSpec(kind="depth", name="depth", orientation="down"),
+                                  SensorSpec(kind="segmentation", name="vision", orientation="down")))
+    raise ValueError(kind)
+
+
+def env_workload(kind, rank, world, total):
+    from paper_2407_14783_b200.env import make_env
+
+    if kind == "swarm":  # one swarm per rank (swarms do not shard: every agent sees every other)
+        cfg = workload_config(kind, total // world)
         return make_env(cfg), cfg
-    elif kind == "c5":
-        cfg = EnvConfig(num_agents=total, task="landing", command_type="lv", episode_max_steps=512,
-                        scenes=(SceneSpec(kind="indoor", seed=0),),
-                        randomization=InitRandomization(position=DistSpec("uniform", low=[-12, -12, 1.0], high=[12, 12, 4.5])),
-                        min_spawn_clearance=0.3,
-                        sensors=(SensorSpec(kind="depth", name="depth", orientation="down"),
-                                 SensorSpec(kind="segmentation", name="vision", orientation="down")))
-    else:
-        raise ValueError(kind)
+    cfg = workload_config(kind, total)
     return make_env(cfg, shard=(rank, world)), cfg
 
 
@@ -492,13 +495,9 @@ def cpu_baseline_env(kind="c3", n_sample=1024, steps=12):
     cores) on a bounded sample of the same workload: env-steps/s."""
     import oracle
     from oracle.env import OracleEnv
-    from paper_2407_14783_b200.env import EnvConfig, navigation_config
     from paper_2407_14783_b200.params import ControllerGains, QuadParams, SimConfig
 
-    if kind == "c1":
-        cfg = EnvConfig(num_agents=n_sample, command_type="ctbr", episode_max_steps=1000)
-    else:
-        cfg = navigation_config(scene_seed=0, num_agents=n_sample, with_segmentation=(kind != "c2"))
+    cfg = workload_config(kind, n_sample)
     scenes = []
     for spec in cfg.scenes:
         t = spec.materialize().arrays
@@ -508,7 +507,7 @@ def cpu_baseline_env(kind="c3", n_sample=1024, steps=12):
     rng = np.random.default_rng(0)
 
     def act():
-        if kind == "c1":
+        if cfg.command_type == "ctbr":
             return np.concatenate([np.full((n_sample, 1), 9.81), rng.normal(scale=0.5, size=(n_sample, 3))], 1)
         return np.concatenate([rng.normal(scale=1.5, size=(n_sample, 3)), rng.uniform(-3, 3, (n_sample, 1))], 1)
 
@@ -616,9 +615,9 @@ def main():
             line["roofline_dynamics"] = run_dynamics_roofline(pk)
             line["roofline_env_step"] = run_env_step_roofline(pk)
             if args.cpu:
-                ns = min(1024, ENVS[kind])
-                steps = 12 if ns > 100 else 400
-                v, dt = cpu_baseline_env(kind if kind in ("c1", "c2") else "c3", n_sample=ns, steps=steps)
+                ns = {"c5": 64, "c3n": 256, "swarm": 256}.get(kind, min(1024, ENVS[kind]))
+                steps = {"c5": 2, "swarm": 4}.get(kind, 12 if ns > 100 else 400)
+                v, dt = cpu_baseline_env(kind, n_sample=ns, steps=steps)
                 line["cpu_baseline"] = {"value": v, "unit": "env-steps/s", "cores": os.cpu_count(), "kind": "port",
                                         "sample": f"{ns} envs x {steps} steps of the same env step on the C oracle "
                                                   f"(OpenMP), {dt:.1f} s"}
@@ -646,9 +645,10 @@ def reference_arm(args, kind):
         metric = "BPTT env-steps/sec (forward + adjoint), whole box"
     else:
         vals = []
+        ns = {"c5": 64, "swarm": 256}.get(kind, 512)
         for _ in range(max(1, min(args.steps, 5))):
-            vals.append(cpu_baseline_env(kind if kind in ("c1", "c2") else "c3", n_sample=512, steps=2)[0])
-        unit, sample, metric = "env-steps/s", "512 envs x 2 steps per step (C oracle, OpenMP)", METRIC
+            vals.append(cpu_baseline_env(kind, n_sample=ns, steps=2)[0])
+        unit, sample, metric = "env-steps/s", f"{ns} envs x 2 steps per step (C oracle, OpenMP)", METRIC
     v = float(np.median(vals))
     line = {"impl": "reference", "metric": metric, "value": v, "unit": unit, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "higher_is_better": True, "config": {"workload": WORKLOADS[kind]},

@@ -1,7 +1,6 @@
 mkdir -p gpurun_out
-for w in c3 c1 c2 c4 c5; do
+for w in c3 c1 c2 c4 c5 c3n swarm; do
   timeout 900 python bench.py --workload $w --steps 10 --warmup 3 > gpurun_out/bench_$w.log 2>&1; echo bench_$w=$?
-  tail -1 gpurun_out/bench_$w.log | cut -c1-300
 done
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.log 2>&1; echo ref=$?
 tail -1 gpurun_out/bench_ref.log

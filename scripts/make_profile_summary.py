@@ -14,12 +14,15 @@ from ncu_summary import read  # noqa: E402
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "gpurun_out")
+DEST = sys.argv[1] if len(sys.argv) > 1 else os.path.join(ROOT, "profiles")  # (on the GPU box: gpurun_out/prof)
 CAPTURES = {  # report -> (kernel key, units in the captured launch, unit)
     "r1_render_cull": ("k_render_cull", 16384, "camera (64x64, depth+seg), 69-prim nav room"),
     "r1_render_bvh": ("k_render_f", 32768, "camera (64x64, down depth+seg), 5e5-tri hall"),
     "r1_env_step": ("k_env_step", 65536, "env"),
     "r1_dyn_step": ("k_dyn_step", 4194304, "env"),
     "r1_bptt": (None, 16384 * 64, "env-step"),
+    "r1_observe": ("k_env_observe", 16384, "env (C3n sensor pass: depth N -> Redwood, seg salt-and-pepper, IMU)"),
+    "r1_env_big": ("k_env_step_4m", 4194304, "env (K1+K3 fused step, free flight, garage)"),
 }
 
 
@@ -57,12 +60,22 @@ for rep, (key, units, unit) in CAPTURES.items():
             "warp_instructions_per_unit": num(r["smsp__inst_executed.sum"]) / units,
             "source": f"{rep}.ncu-rep (ncu --set full --clock-control none, round 1)",
         }
-os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
-with open(os.path.join(ROOT, "profiles", "ncu_summary.json"), "w") as f:
+os.makedirs(DEST, exist_ok=True)
+with open(os.path.join(DEST, "ncu_summary.json"), "w") as f:
     json.dump(summary, f, indent=1)
-with open(os.path.join(ROOT, "profiles", "r1_ncu_raw_summary.json"), "w") as f:
+with open(os.path.join(DEST, "r1_ncu_raw_summary.json"), "w") as f:
     json.dump(raw, f, indent=1)
 if os.path.exists(os.path.join(OUT, "r1_launches.csv")):
-    shutil.copy(os.path.join(OUT, "r1_launches.csv"), os.path.join(ROOT, "profiles", "r1_launch_list.csv"))
+    shutil.copy(os.path.join(OUT, "r1_launches.csv"), os.path.join(DEST, "r1_launch_list.csv"))
+# per-line source tables of the two renderers (for reading back without the .ncu-rep)
+for rep in ("r1_render_cull", "r1_render_bvh", "r1_observe", "r1_env_big"):
+    path = os.path.join(OUT, rep + ".ncu-rep")
+    if os.path.exists(path):
+        import subprocess
+
+        out = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+                             capture_output=True, text=True).stdout
+        with open(os.path.join(DEST, rep + "_source.csv"), "w") as f:
+            f.write(out)
 print(json.dumps({k: {kk: v[kk] for kk in ("time_ms", "dram_bytes_per_unit", "issue_active_pct", "warps_active_pct",
                                             "warp_instructions_per_unit")} for k, v in summary.items()}, indent=1))

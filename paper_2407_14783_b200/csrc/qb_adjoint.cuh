@@ -104,24 +104,27 @@ QB_D void ode_rhs_vjp(const DynConsts<R> &C, const R *y, const Wrench<R> &W, con
 // controller), lam: dL/dnext (17, in-out -> dL/dx), cmd_bar: dL/dcmd (4,
 // accumulated), boundary: clip-boundary flag.  Substep intermediates are
 // recomputed per substep from the saved substep inputs (<= 8 substeps).
-template <class R>
+// SUB > 0: substep count known at compile time (== C.substeps): the substep
+// inputs stay in registers instead of a local-memory array
+template <class R, int SUB = 0>
 QB_D void dyn_step_vjp(const DynConsts<R> &C, const R *x_in, const R *cmd_in, R *lam, R *cmd_bar, bool &boundary) {
-    constexpr int MAXS = 8;
+    constexpr int MAXS = SUB > 0 ? SUB : 8;
     R cmd[4], cmask[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         cmask[i] = clip_mask(cmd_in[i], C.rlo, C.rhi, boundary);
         cmd[i] = p_clip(cmd_in[i], C.rlo, C.rhi);
     }
-    const int S = C.substeps < MAXS ? C.substeps : MAXS;
-    // forward: keep each substep's input state (13 rigid + 4 rotors)
+    const int S = SUB > 0 ? SUB : (C.substeps < MAXS ? C.substeps : MAXS);
+    // forward: keep each substep's input state (13 rigid + 4 rotors); the
+    // last substep's output is not needed by the reverse sweep
     R xs[MAXS][17];
     R x[17];
 #pragma unroll
     for (int k = 0; k < 17; ++k) x[k] = x_in[k];
-    for (int s = 0; s < S; ++s) {
 #pragma unroll
-        for (int k = 0; k < 17; ++k) xs[s][k] = x[k];
+    for (int k = 0; k < 17; ++k) xs[0][k] = x[k];
+    for (int s = 0; s + 1 < S; ++s) {
         R w[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) w[i] = p_clip(cmd[i] + (x[13 + i] - cmd[i]) * C.alpha, C.rlo, C.rhi);
@@ -131,8 +134,11 @@ QB_D void dyn_step_vjp(const DynConsts<R> &C, const R *x_in, const R *cmd_in, R 
 #pragma unroll
         for (int i = 0; i < 4; ++i) x[13 + i] = w[i];
         q_normalize(x + 6);
+#pragma unroll
+        for (int k = 0; k < 17; ++k) xs[s + 1][k] = x[k];
     }
     R cb[4] = {R(0.0), R(0.0), R(0.0), R(0.0)};
+#pragma unroll
     for (int s = S - 1; s >= 0; --s) {
         const R *x0 = xs[s];
         R raw[4], lm[4], w[4];

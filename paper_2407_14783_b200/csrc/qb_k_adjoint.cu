@@ -6,6 +6,8 @@
 // HBM traffic, plus the optional in-kernel reduction of the action gradient
 // over envs (warp shuffle, one double atomic per warp) that feeds the
 // multi-GPU all-reduce of a shared open-loop action sequence.
+#include <type_traits>
+
 #include "qb_adjoint.cuh"
 #include "qb_internal.h"
 
@@ -13,7 +15,7 @@ namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 
-template <class R, int KIND>
+template <class R, int KIND, int SUB>
 __global__ void __launch_bounds__(128) k_rollout_bwd(DynConsts<R> C, long long n, long long ld, int T,
                                                      const typename storage_of<R>::type *tape,
                                                      const typename storage_of<R>::type *actions,
@@ -43,7 +45,7 @@ __global__ void __launch_bounds__(128) k_rollout_bwd(DynConsts<R> C, long long n
         for (int k = 0; k < 4; ++k) a[k] = R(ap[k]);
         command_to_speeds<R, KIND>(C, x, a, cmd);
         R cb[4] = {R(0.0), R(0.0), R(0.0), R(0.0)};
-        dyn_step_vjp(C, x, cmd, lam, cb, flag);  // lam <- J^T lam (dynamics part)
+        dyn_step_vjp<R, SUB>(C, x, cmd, lam, cb, flag);  // lam <- J^T lam (dynamics part)
         R ga[4];
         if constexpr (KIND == QB_CMD_ROTOR) {
 #pragma unroll
@@ -101,12 +103,18 @@ int dispatch(const qb_params *p, int kind, long long n, long long ld, int T, con
     auto *gt = static_cast<const S *>(gtraj);
     auto *gA = static_cast<S *>(ga);
     auto *gI = static_cast<S *>(gi);
+    // the default 2 substeps get a compile-time specialisation (FP32 only)
+    const bool sub2 = std::is_same<R, float>::value && C.substeps == 2;
+#define QB_BWD(K)                                                                                         \
+    (sub2 ? (k_rollout_bwd<R, K, 2><<<g, B, 0, st>>>(C, n, ld, T, x, a, gt, gA, gI, boundary, sum), 0) \
+          : (k_rollout_bwd<R, K, 0><<<g, B, 0, st>>>(C, n, ld, T, x, a, gt, gA, gI, boundary, sum), 0))
     switch (kind) {
-        case QB_CMD_ROTOR: k_rollout_bwd<R, QB_CMD_ROTOR><<<g, B, 0, st>>>(C, n, ld, T, x, a, gt, gA, gI, boundary, sum); break;
-        case QB_CMD_CTBR: k_rollout_bwd<R, QB_CMD_CTBR><<<g, B, 0, st>>>(C, n, ld, T, x, a, gt, gA, gI, boundary, sum); break;
-        case QB_CMD_SRT: k_rollout_bwd<R, QB_CMD_SRT><<<g, B, 0, st>>>(C, n, ld, T, x, a, gt, gA, gI, boundary, sum); break;
+        case QB_CMD_ROTOR: QB_BWD(QB_CMD_ROTOR); break;
+        case QB_CMD_CTBR: QB_BWD(QB_CMD_CTBR); break;
+        case QB_CMD_SRT: QB_BWD(QB_CMD_SRT); break;
         default: qb::set_error("command kind %d is not differentiable", kind); return QB_EINVAL;
     }
+#undef QB_BWD
     return qb::check_launch("rollout_backward");
 }
 

@@ -1,0 +1,9 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_gradients.py -q -p no:cacheprovider > gpurun_out/pytest_grad.log 2>&1; echo grad=$?; tail -1 gpurun_out/pytest_grad.log
+for r in 1 2; do
+timeout 600 python bench.py --workload c4 --steps 10 --warmup 3 --no-e2e --no-cpu > gpurun_out/c4.log 2>&1
+python -c "
+import json
+l=[x for x in open('gpurun_out/c4.log') if x.startswith('{')]
+d=json.loads(l[-1]); print('c4', '%.4g'%d['value'], d.get('kernel_ms'))"
+done

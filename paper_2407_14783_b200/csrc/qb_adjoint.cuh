@@ -99,15 +99,61 @@ QB_D void ode_rhs_vjp(const DynConsts<R> &C, const R *y, const Wrench<R> &W, con
     yb[12] = yb[12] - (b0 * jzy * oy + b1 * jxz * ox);
 }
 
+// RK4 (or Euler) stage states of one substep from its input y and wrench:
+// y2, y3, y4 (RK4 stage arguments) and the raw (unnormalised) result
+template <class R>
+QB_D void substep_stages(const DynConsts<R> &C, const R *y, const Wrench<R> &Wr, R *y2, R *y3, R *y4, R *yraw) {
+    R k[13];
+    if (C.integrator == QB_RK4) {
+        ode_rhs(C, y, Wr, k);
+        R acc[13];
+#pragma unroll
+        for (int i = 0; i < 13; ++i) {
+            acc[i] = k[i];
+            y2[i] = y[i] + C.half_h * k[i];
+        }
+        ode_rhs(C, y2, Wr, k);
+#pragma unroll
+        for (int i = 0; i < 13; ++i) {
+            acc[i] = acc[i] + R(2.0) * k[i];
+            y3[i] = y[i] + C.half_h * k[i];
+        }
+        ode_rhs(C, y3, Wr, k);
+#pragma unroll
+        for (int i = 0; i < 13; ++i) {
+            acc[i] = acc[i] + R(2.0) * k[i];
+            y4[i] = y[i] + C.h * k[i];
+        }
+        ode_rhs(C, y4, Wr, k);
+#pragma unroll
+        for (int i = 0; i < 13; ++i) yraw[i] = y[i] + C.sixth_h * (acc[i] + k[i]);
+    } else {
+        ode_rhs(C, y, Wr, k);
+#pragma unroll
+        for (int i = 0; i < 13; ++i) yraw[i] = y[i] + C.h * k[i];
+    }
+}
+
+// Stage cache: with SUB == 2 and a cache (per-thread column of 52 values
+// with stride `cs`, in shared memory), the first substep's stages computed
+// by the forward pass are kept instead of being recomputed in the reverse
+// sweep (20 -> 16 RHS-level evaluations per control step).
+template <class R> struct StageCache {
+    R *p;
+    int stride;
+    QB_D R &at(int k) const { return p[k * stride]; }
+};
+
 // One control step: forward recomputation + reverse sweep.
 // x: pre-step 17-state, cmd: desired rotor speeds (already from the
 // controller), lam: dL/dnext (17, in-out -> dL/dx), cmd_bar: dL/dcmd (4,
 // accumulated), boundary: clip-boundary flag.  Substep intermediates are
 // recomputed per substep from the saved substep inputs (<= 8 substeps).
 // SUB > 0: substep count known at compile time (== C.substeps): the substep
-// inputs stay in registers instead of a local-memory array
+// inputs stay in registers instead of a local-memory array.
 template <class R, int SUB = 0>
-QB_D void dyn_step_vjp(const DynConsts<R> &C, const R *x_in, const R *cmd_in, R *lam, R *cmd_bar, bool &boundary) {
+QB_D void dyn_step_vjp(const DynConsts<R> &C, const R *x_in, const R *cmd_in, R *lam, R *cmd_bar, bool &boundary,
+                       StageCache<R> cache = StageCache<R>{nullptr, 0}) {
     constexpr int MAXS = SUB > 0 ? SUB : 8;
     R cmd[4], cmask[4];
 #pragma unroll
@@ -116,21 +162,36 @@ QB_D void dyn_step_vjp(const DynConsts<R> &C, const R *x_in, const R *cmd_in, R 
         cmd[i] = p_clip(cmd_in[i], C.rlo, C.rhi);
     }
     const int S = SUB > 0 ? SUB : (C.substeps < MAXS ? C.substeps : MAXS);
+    const bool cached = SUB == 2 && cache.p != nullptr;
     // forward: keep each substep's input state (13 rigid + 4 rotors); the
     // last substep's output is not needed by the reverse sweep
     R xs[MAXS][17];
-    R x[17];
 #pragma unroll
-    for (int k = 0; k < 17; ++k) x[k] = x_in[k];
+    for (int k = 0; k < 17; ++k) xs[0][k] = x_in[k];
 #pragma unroll
-    for (int k = 0; k < 17; ++k) xs[0][k] = x[k];
     for (int s = 0; s + 1 < S; ++s) {
+        R x[17];
+#pragma unroll
+        for (int k = 0; k < 17; ++k) x[k] = xs[s][k];
         R w[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) w[i] = p_clip(cmd[i] + (x[13 + i] - cmd[i]) * C.alpha, C.rlo, C.rhi);
         Wrench<R> Wr;
         make_wrench(C, w, Wr);
-        integrate_substep(C, x, Wr);
+        if (cached && s == 0) {
+            R y2[13], y3[13], y4[13], yraw[13];
+            substep_stages(C, x, Wr, y2, y3, y4, yraw);
+#pragma unroll
+            for (int i = 0; i < 13; ++i) {
+                cache.at(i) = y2[i];
+                cache.at(13 + i) = y3[i];
+                cache.at(26 + i) = y4[i];
+                cache.at(39 + i) = yraw[i];
+                x[i] = yraw[i];
+            }
+        } else {
+            integrate_substep(C, x, Wr);
+        }
 #pragma unroll
         for (int i = 0; i < 4; ++i) x[13 + i] = w[i];
         q_normalize(x + 6);
@@ -150,38 +211,21 @@ QB_D void dyn_step_vjp(const DynConsts<R> &C, const R *x_in, const R *cmd_in, R 
         }
         Wrench<R> Wr;
         make_wrench(C, w, Wr);
-        // recompute the stages of this substep
-        R y[13], k[13], y2[13], y3[13], y4[13], yraw[13];
+        // the stages of this substep (recomputed, or from the forward pass)
+        R y[13], y2[13], y3[13], y4[13], yraw[13];
 #pragma unroll
         for (int i = 0; i < 13; ++i) y[i] = x0[i];
         const bool rk4 = C.integrator == QB_RK4;
-        if (rk4) {
-            ode_rhs(C, y, Wr, k);
-            R acc[13];
+        if (cached && s == 0) {
 #pragma unroll
             for (int i = 0; i < 13; ++i) {
-                acc[i] = k[i];
-                y2[i] = y[i] + C.half_h * k[i];
+                y2[i] = cache.at(i);
+                y3[i] = cache.at(13 + i);
+                y4[i] = cache.at(26 + i);
+                yraw[i] = cache.at(39 + i);
             }
-            ode_rhs(C, y2, Wr, k);
-#pragma unroll
-            for (int i = 0; i < 13; ++i) {
-                acc[i] = acc[i] + R(2.0) * k[i];
-                y3[i] = y[i] + C.half_h * k[i];
-            }
-            ode_rhs(C, y3, Wr, k);
-#pragma unroll
-            for (int i = 0; i < 13; ++i) {
-                acc[i] = acc[i] + R(2.0) * k[i];
-                y4[i] = y[i] + C.h * k[i];
-            }
-            ode_rhs(C, y4, Wr, k);
-#pragma unroll
-            for (int i = 0; i < 13; ++i) yraw[i] = y[i] + C.sixth_h * (acc[i] + k[i]);
         } else {
-            ode_rhs(C, y, Wr, k);
-#pragma unroll
-            for (int i = 0; i < 13; ++i) yraw[i] = y[i] + C.h * k[i];
+            substep_stages(C, y, Wr, y2, y3, y4, yraw);
         }
         // renormalisation: q = q_raw / |q_raw|
         R yb_out[13];

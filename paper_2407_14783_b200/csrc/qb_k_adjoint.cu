@@ -24,6 +24,12 @@ __global__ void __launch_bounds__(128) k_rollout_bwd(DynConsts<R> C, long long n
                                                      typename storage_of<R>::type *grad_init, uint8_t *boundary,
                                                      double *action_grad_sum) {
     using S = typename storage_of<R>::type;
+    // FP32 2-substep build: the first substep's stages go through shared
+    // memory (one column of 52 floats per thread) instead of being recomputed
+    constexpr bool kCache = SUB == 2 && std::is_same<R, float>::value;
+    __shared__ float stage_s[kCache ? 52 * 128 : 1];
+    StageCache<R> cache{nullptr, 0};
+    if constexpr (kCache) cache = StageCache<R>{reinterpret_cast<R *>(stage_s) + threadIdx.x, 128};
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const bool live = i < n;
     const long long ii = live ? i : 0;
@@ -45,7 +51,7 @@ __global__ void __launch_bounds__(128) k_rollout_bwd(DynConsts<R> C, long long n
         for (int k = 0; k < 4; ++k) a[k] = R(ap[k]);
         command_to_speeds<R, KIND>(C, x, a, cmd);
         R cb[4] = {R(0.0), R(0.0), R(0.0), R(0.0)};
-        dyn_step_vjp<R, SUB>(C, x, cmd, lam, cb, flag);  // lam <- J^T lam (dynamics part)
+        dyn_step_vjp<R, SUB>(C, x, cmd, lam, cb, flag, cache);  // lam <- J^T lam (dynamics part)
         R ga[4];
         if constexpr (KIND == QB_CMD_ROTOR) {
 #pragma unroll

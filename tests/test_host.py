@@ -196,3 +196,39 @@ def test_episode_log_bytes_match_reference(tmp_path):
                       {"collision": np.array([False, True, False]), "success": np.zeros(3, bool)})
     assert np.array_equal(np.frombuffer(path.read_bytes(), np.uint8), g["log"])
     assert read_episode_log(path)[1]["flags"] == {"collision": True, "success": False}
+
+
+def test_abi_argument_validation_without_gpu():
+    """Host-side validation of the newer entry points returns a status and a
+    message before touching the device (no GPU needed)."""
+    import ctypes
+
+    import paper_2407_14783_b200._native as nat
+    from paper_2407_14783_b200.params import native_params
+
+    lib = nat.load(require_cuda=False)
+    lib.qb_last_error.restype = ctypes.c_char_p
+    P = native_params()
+    # IMU sensors take Gaussian noise only (sensing.py:150-160 validity table)
+    so = nat.QbSensorObs()
+    so.kind, so.n_noise = nat.SENSOR_KINDS["imu"], 1
+    so.noise[0].kind = nat.NOISE_KINDS["poisson"]
+    so.out = 1
+    state = (ctypes.c_float * 17)()
+    rng = (ctypes.c_uint64 * 4)()
+    b = nat.QbEnvBuffers()
+    b.n, b.ld, b.dtype = 1, 1, nat.QB_F32
+    b.state, b.rng = ctypes.addressof(state), ctypes.addressof(rng)
+    rc = lib.qb_env_observe(P, b, 1, ctypes.cast(ctypes.pointer(so), ctypes.c_void_p), None)
+    assert rc != 0 and b"not defined" in lib.qb_last_error()
+    # Redwood is depth-only
+    so.kind, so.noise[0].kind, so.src, so.width, so.height = nat.SENSOR_KINDS["segmentation"], nat.NOISE_KINDS["redwood"], 1, 4, 4
+    assert lib.qb_env_observe(P, b, 1, ctypes.cast(ctypes.pointer(so), ctypes.c_void_p), None) != 0
+    # unknown controller stage / missing state planes
+    buf = (ctypes.c_float * 8)()
+    assert lib.qb_control_stage(P, 7, nat.QB_F32, 1, 1, None, ctypes.addressof(buf), ctypes.addressof(buf), None, None) != 0
+    assert lib.qb_control_stage(P, 1, nat.QB_F32, 1, 1, None, ctypes.addressof(buf), ctypes.addressof(buf), None, None) != 0
+    assert b"state planes" in lib.qb_last_error()
+    # empty primitive set
+    cnt = ctypes.c_int64(0)
+    assert lib.qb_bvh_build(0, None, None, ctypes.byref(cnt), None, None, None, None, None) != 0

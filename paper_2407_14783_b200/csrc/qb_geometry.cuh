@@ -373,8 +373,8 @@ QB_D float ray_sphere_f(const float4 *p, float ox, float oy, float oz, float dx,
     return -1.0f;
 }
 
-QB_D float ray_box_f(const float4 *p, float ox, float oy, float oz, float dx, float dy, float dz, float tmin, float tmax) {
-    float4 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2), e = __ldg(p + 3);
+QB_D float ray_box_v(float4 a, float4 b, float4 c, float4 e, float ox, float oy, float oz, float dx, float dy, float dz,
+                     float tmin, float tmax) {
     float mx = ox - a.x, my = oy - a.y, mz = oz - a.z;
     // R = [[b.z b.w c.x] [c.y c.z c.w] [e.x e.y e.z]] (local -> world); local = R^T m
     float lox = b.z * mx + c.y * my + e.x * mz;
@@ -398,8 +398,14 @@ QB_D float ray_box_f(const float4 *p, float ox, float oy, float oz, float dx, fl
     return -1.0f;
 }
 
-QB_D float ray_triangle_f(const float4 *p, float ox, float oy, float oz, float dx, float dy, float dz, float tmin, float tmax) {
-    float4 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2);
+QB_D float ray_box_f(const float4 *p, float ox, float oy, float oz, float dx, float dy, float dz, float tmin, float tmax) {
+    return ray_box_v(__ldg(p), __ldg(p + 1), __ldg(p + 2), __ldg(p + 3), ox, oy, oz, dx, dy, dz, tmin, tmax);
+}
+
+// triangle record (a, e1, e2) passed by value: callers issue the record loads
+// together with the primitive's metadata load
+QB_D float ray_triangle_v(float4 a, float4 b, float4 c, float ox, float oy, float oz, float dx, float dy, float dz,
+                          float tmin, float tmax) {
     float ax = a.x, ay = a.y, az = a.z;
     float e1x = a.w, e1y = b.x, e1z = b.y, e2x = b.z, e2y = b.w, e2z = c.x;
     float px = dy * e2z - dz * e2y, py = dz * e2x - dx * e2z, pz = dx * e2y - dy * e2x;
@@ -418,6 +424,10 @@ QB_D float ray_triangle_f(const float4 *p, float ox, float oy, float oz, float d
     float t = __fdividef(e2x * qx + e2y * qy + e2z * qz, det);
     if (t > tmin && t <= tmax) return t;
     return -1.0f;
+}
+
+QB_D float ray_triangle_f(const float4 *p, float ox, float oy, float oz, float dx, float dy, float dz, float tmin, float tmax) {
+    return ray_triangle_v(__ldg(p), __ldg(p + 1), __ldg(p + 2), ox, oy, oz, dx, dy, dz, tmin, tmax);
 }
 
 // FP32 slab entry (kernels.py:288-319 semantics: entry clamped at 0, INF = miss)

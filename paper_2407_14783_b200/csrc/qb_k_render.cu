@@ -310,15 +310,17 @@ __global__ void __launch_bounds__(QB_RF_BLOCK, QB_RF_MINB) k_render_f(DevScene S
                     st_prim += cb;
 #endif
                     for (int p = ca; p < ca + cb; ++p) {
-                        const int2 m = __ldg(S.meta + p);
+                        // record and metadata loads issued together (no type-dependent load)
                         const float4 *pr = S.primf + 4 * p;
+                        const float4 ra = __ldg(pr), rb = __ldg(pr + 1), rc = __ldg(pr + 2);
+                        const int2 m = __ldg(S.meta + p);
                         float t;
                         if (m.x == QB_TRIANGLE)
-                            t = ray_triangle_f(pr, o[0], o[1], o[2], dx, dy, dz, tmin, best);
+                            t = ray_triangle_v(ra, rb, rc, o[0], o[1], o[2], dx, dy, dz, tmin, best);
                         else if (m.x == QB_BOX)
-                            t = ray_box_f(pr, o[0], o[1], o[2], dx, dy, dz, tmin, best);
+                            t = ray_box_v(ra, rb, rc, __ldg(pr + 3), o[0], o[1], o[2], dx, dy, dz, tmin, best);
                         else
-                            t = ray_sphere_f(pr, o[0], o[1], o[2], dx, dy, dz, tmin, best);
+                            t = ray_sphere_v(ra, rb.x, o[0], o[1], o[2], dx, dy, dz, tmin, best);
                         if (t > 0.0f && (t < best || !hit || (t == best && m.y < bid))) {
                             best = t;
                             bid = m.y;

@@ -46,7 +46,10 @@ namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 constexpr float CULL_EPS = 1e-3f;  // conservative culling margin (m)
-constexpr int TPL_MAX = 128;       // tile-plane table entries (64x64 frames use 32)
+#ifndef QB_TPL_MAX
+#define QB_TPL_MAX 64
+#endif
+constexpr int TPL_MAX = QB_TPL_MAX;  // tile-plane table entries (64x64 frames use 32)
 constexpr int TILE_W = 8, TILE_H = 4;
 
 struct CamF {
@@ -421,17 +424,17 @@ __global__ void __launch_bounds__(QB_RF_BLOCK, QB_RF_MINB) k_render_f(DevScene S
 // kernel's and depths agree to FP32 rounding.
 constexpr int CULL_MAX = 256;   // primitives per scene
 #ifndef QB_CULL_MINB
-#define QB_CULL_MINB 5  // measured: 5 blocks (93 regs, no spills) beats 6 (80 regs + spills) by 19%
+#define QB_CULL_MINB 6  // 6 blocks at 80 registers without spills (rotation in shared memory); 6 with spills was 19% slower
 #endif
 #ifndef QB_CREC
-#define QB_CREC 64
+#define QB_CREC 56
 #endif
 #ifndef QB_CULL_WARPS
 #define QB_CULL_WARPS 4
 #endif
 constexpr int CULL_WARPS = QB_CULL_WARPS;  // warps (cameras) per block
 constexpr int XMAX = 32;  // swarm spheres kept per camera after frustum culling (more: every sphere per ray)
-constexpr int CREC = QB_CREC;   // precomputed records per camera (nav room: mean 21, max 58); more use the generic path
+constexpr int CREC = QB_CREC;   // precomputed records per camera (nav room: mean 21, max 58); more use the generic path (56 keeps 6 blocks/SM in shared memory)
 enum { REC_SPHERE = 0, REC_AABB = 1, REC_OBB = 2, REC_GENERIC = 3 };
 
 struct Plane {
@@ -476,6 +479,7 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, QB_CULL_MINB)
                   float *centroid, const float *extra, const int32_t *extra_ids, int n_extra, int split) {
     __shared__ int cand_s[CULL_WARPS][CULL_MAX];
     constexpr int XM = EXTRA ? XMAX : 1;
+    __shared__ float rws_s[CULL_WARPS][9];               // camera rotation for the tile loop (out of registers)
     __shared__ float4 xcs_s[CULL_WARPS][XM];             // swarm spheres in the frustum: camera-space centre, r
     __shared__ int xk_s[CULL_WARPS][XM];                 // ... and their index k (ascending)
     __shared__ float4 rec_s[CULL_WARPS][CREC][4];      // shading records (warp-broadcast reads)
@@ -645,6 +649,9 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, QB_CULL_MINB)
         }
 
         int cnt = 0, sum_col = 0, sum_row = 0;
+        __syncwarp();
+        if (lane < 9) rws_s[wib][lane] = Rw[lane];  // (every lane holds the same pose)
+        __syncwarp();
         // per-camera output planes (32-bit offsets inside one frame)
         float *depth_c = depth ? depth + c * (long long)H * W : nullptr;
         int32_t *seg_c = seg ? seg + c * (long long)H * W : nullptr;
@@ -683,9 +690,10 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, QB_CULL_MINB)
                 const float n2 = x * x + y * y + 1.0f;
                 const float cz = rsqrtf(n2);
                 const float cx = x * cz, cy = y * cz;
-                dx[u] = Rw[0] * cx + Rw[1] * cy + Rw[2] * cz;
-                dy[u] = Rw[3] * cx + Rw[4] * cy + Rw[5] * cz;
-                dz[u] = Rw[6] * cx + Rw[7] * cy + Rw[8] * cz;
+                const float *Rs = rws_s[wib];
+                dx[u] = Rs[0] * cx + Rs[1] * cy + Rs[2] * cz;
+                dy[u] = Rs[3] * cx + Rs[4] * cy + Rs[5] * cz;
+                dz[u] = Rs[6] * cx + Rs[7] * cy + Rs[8] * cz;
                 ix[u] = rcp_approx(dx[u]);
                 iy[u] = rcp_approx(dy[u]);
                 iz[u] = rcp_approx(dz[u]);

@@ -1,14 +1,16 @@
 // qb_k_observe.cu -- the sensor half of QuadEnvBase.get_observation
 // (env/base.py:287-305): ideal IMU readings (sensing.py:124-147) and the
-// noise chains of sensing.py:195-235, one thread per env (32-env warps share
-// coalesced shared-memory tiles, see Tile below), sensors in config
-// order, every draw taken from the env's PCG64 stream in numpy's order:
+// noise chains of sensing.py:195-235, sensors in config order, every draw
+// taken from the env's PCG64 stream in numpy's order:
 //   normal / speckle   rng.standard_normal(shape)       (ziggurat, qb_rng.cuh)
 //   poisson            rng.poisson(max(v,0) * scaling)  (mult / PTRS)
 //   saltpepper         rng.random(shape) twice          (corrupt, then salt)
 //   redwood            rng.standard_normal(shape) in disparity space
 // Values are processed in double like the reference (np.asarray(.., float));
-// the FP32 build stores each pass in float32.
+// the FP32 build stores each pass in float32.  Two kernels: warp per env with
+// speculative stream reads (k_env_observe_warp, every chain without Poisson)
+// and thread per env (k_env_observe, chains with Poisson noise, whose draw
+// count per pixel depends on the value).
 #include "qb_dynamics.cuh"
 #include "qb_internal.h"
 #include "qb_rng.cuh"
@@ -251,6 +253,267 @@ __global__ void __launch_bounds__(ObsWarps<S>::value * 32, QB_OBS_MINB) k_env_ob
     if (live) pcg_store(B.rng + 4 * i, r);
 }
 
+// ---- warp-per-env sensor pass -------------------------------------------
+// One warp per env, 32 consecutive pixels per round.  The numpy draw order is
+// kept by reading the env's stream speculatively: lane l evaluates word P+l+1
+// (the LCG jump state -> A_{l+1} state + C_{l+1}, qb_rng.cuh) and the
+// ziggurat fast test on it; the first lane whose word fails (~1.2% per draw)
+// finishes its normal sequentially from there, the lanes before it keep
+// theirs, and the next round starts after the words that draw consumed.
+// Salt-and-pepper draws are fixed-count (corrupt block, then salt block), so
+// every lane jumps straight to its words.  The reads and writes of a round
+// are one coalesced 128 B line per env, and a 16384-env batch fills the GPU
+// (the thread-per-env kernel above has 32x fewer warps).  Chains with
+// Poisson noise (a data-dependent number of uniform draws) use that kernel.
+struct WarpRng {
+    u128 P, inc;    // the stream's state before the next draw (warp-uniform)
+    u128 A, C;      // this lane's jump over lane+1 words
+    u128 A32, C32;  // the jump over 32 words
+};
+
+__device__ __forceinline__ u128 shfl_u128(u128 v, int src) {
+    const unsigned long long lo = __shfl_sync(0xffffffffu, (unsigned long long)v, src);
+    const unsigned long long hi = __shfl_sync(0xffffffffu, (unsigned long long)(v >> 64), src);
+    return ((u128)hi << 64) | lo;
+}
+
+__device__ __forceinline__ double warp_fmin(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ double warp_fmax(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// pixel k of the input image in double: int32 ids through S (the tile rule
+// above), S values as stored.  Plain loads: later passes read what the
+// previous pass of this kernel wrote.
+template <class S> __device__ __forceinline__ double px_in(const void *in, bool ids, long long k) {
+    return ids ? (double)(S) static_cast<const int32_t *>(in)[k] : (double)static_cast<const S *>(in)[k];
+}
+
+__device__ __forceinline__ double draw_double(u128 state) {
+    return (double)(pcg64_output(state) >> 11) * (1.0 / 9007199254740992.0);
+}
+
+// the per-pixel transform of the one-normal-per-pixel noises (x = the draw)
+__device__ __forceinline__ double normal_noise(const qb_noise &nz, double v, double x, double floor_disp) {
+    switch (nz.kind) {
+        case QB_NOISE_NORMAL:
+            return __dadd_rn(v, __dmul_rn(nz.sigma, x));
+        case QB_NOISE_SPECKLE:
+            return __dmul_rn(v, __dadd_rn(1.0, __dmul_rn(nz.sigma, x)));
+        default: {  // redwood
+            double d = __ddiv_rn(1.0, fmax(v, 1e-6));
+            if (nz.sigma_disparity > 0.0) d = __dadd_rn(d, __dmul_rn(nz.sigma_disparity, x));
+            if (nz.quantization > 0.0) d = __dmul_rn(rint(__ddiv_rn(d, nz.quantization)), nz.quantization);
+            return __ddiv_rn(1.0, fmax(d, floor_disp));
+        }
+    }
+}
+
+// the input pixels of a round come from a two-line register window (32
+// values per line, one per lane) so each load is issued a round before it
+// is used; rounds start anywhere in the window and shuffle their values out.
+template <class S> struct PxWindow {
+    const void *in;
+    bool ids;
+    long long hw, base;  // base: pixel of cur's lane 0 (32-aligned)
+    S cur, nxt;
+    __device__ __forceinline__ S load(long long k) const {
+        if (k >= hw) return S(0);
+        return ids ? (S) static_cast<const int32_t *>(in)[k] : static_cast<const S *>(in)[k];
+    }
+    __device__ __forceinline__ void init(const void *in_, bool ids_, long long hw_, int lane) {
+        in = in_;
+        ids = ids_;
+        hw = hw_;
+        base = 0;
+        cur = load(lane);
+        nxt = load(32 + lane);
+    }
+    // pixel pk + lane (pk - base < 32)
+    __device__ __forceinline__ S at(long long pk, int lane) const {
+        const int src = (int)(pk - base) + lane;
+        const S a = __shfl_sync(0xffffffffu, cur, src & 31), b = __shfl_sync(0xffffffffu, nxt, src & 31);
+        return src < 32 ? a : b;
+    }
+    __device__ __forceinline__ void advance(long long pk, int lane) {
+        if (pk - base >= 32) {  // warp-uniform
+            base += 32;
+            cur = nxt;
+            nxt = load(base + 32 + lane);
+        }
+    }
+};
+
+// one noise pass over one env's image (in / out at the env's base); the
+// range contract is noise_pass's, except that the output range is only
+// tracked when the next pass reads it (need_range)
+template <class S>
+__device__ void warp_noise_pass(const qb_noise &nz, WarpRng &g, const void *in, bool in_ids, S *out, long long hw,
+                                int lane, double2 &range, bool &have_range, bool need_range) {
+    const bool sp = nz.kind == QB_NOISE_SALTPEPPER && nz.p != 0.0, rw = nz.kind == QB_NOISE_REDWOOD;
+    double lo = range.x, hi = range.y;
+    if ((sp || rw) && !have_range) {
+        lo = hi = __longlong_as_double(0x7ff8000000000000LL);  // fmin / fmax skip NaN
+        for (long long k = lane; k < hw; k += 32) {
+            const double v = px_in<S>(in, in_ids, k);
+            lo = fmin(lo, v);
+            hi = fmax(hi, v);
+        }
+        lo = warp_fmin(lo);
+        hi = warp_fmax(hi);
+    }
+    const double floor_disp = __ddiv_rn(1.0, __dadd_rn(hi, 1.0));
+    S olo = S(__longlong_as_double(0x7ff8000000000000LL)), ohi = olo;  // (exact in S: outputs are S values)
+    const bool draws = ((nz.kind == QB_NOISE_NORMAL || nz.kind == QB_NOISE_SPECKLE) && nz.sigma != 0.0) ||
+                       (rw && nz.sigma_disparity > 0.0);
+    if (draws) {
+        PxWindow<S> win;
+        win.init(in, in_ids, hw, lane);
+        for (long long pk = 0; pk < hw;) {
+            const int npx = hw - pk < 32 ? (int)(hw - pk) : 32;
+            const double v = (double)win.at(pk, lane);
+            u128 st = g.A * g.P + g.C;  // the state that yields word P + lane + 1
+            const uint64_t w = pcg64_output(st);
+            double x;
+            const bool ok = normal_fast(w, x);
+            const unsigned bad = __ballot_sync(0xffffffffu, lane < npx && !ok);
+            int cnt = npx;
+            if (bad) {
+                const int f = __ffs(bad) - 1;
+                cnt = f + 1;
+                if (lane == f) {  // the slow continuation of this draw
+                    Pcg64 rr;
+                    rr.state = st;
+                    rr.inc = g.inc;
+                    x = normal_from(w, rr);
+                    st = rr.state;
+                }
+            }
+            if (lane < cnt) {
+                const S so = (S)normal_noise(nz, v, x, floor_disp);
+                out[pk + lane] = so;
+                if (need_range) {
+                    olo = fmin(olo, so);
+                    ohi = fmax(ohi, so);
+                }
+            }
+            g.P = shfl_u128(st, cnt - 1);
+            pk += cnt;
+            win.advance(pk, lane);
+        }
+    } else if (sp) {
+        // corrupt = random(shape) < p over words P+1..P+hw, salt = random(shape)
+        // < 0.5 over the next hw words
+        const PcgJump jh = pcg64_jump(g.inc, (u128)hw);
+        u128 sc = g.A * g.P + g.C, ss = jh.A * sc + jh.C;
+        for (long long k0 = 0; k0 < hw; k0 += 32) {
+            const long long k = k0 + lane;
+            if (k < hw) {
+                const double v = px_in<S>(in, in_ids, k);
+                const bool corrupt = draw_double(sc) < nz.p;
+                const bool salt = draw_double(ss) < 0.5;
+                const S so = (S)(corrupt ? (salt ? hi : lo) : v);
+                out[k] = so;
+                if (need_range) {
+                    olo = fmin(olo, so);
+                    ohi = fmax(ohi, so);
+                }
+            }
+            sc = g.A32 * sc + g.C32;
+            ss = g.A32 * ss + g.C32;
+        }
+        g.P = jh.A * (jh.A * g.P + jh.C) + jh.C;
+    } else {  // no draws: the deterministic part of the transform only
+        for (long long k = lane; k < hw; k += 32) {
+            const double v = px_in<S>(in, in_ids, k);
+            const S so = (S)(rw ? normal_noise(nz, v, 0.0, floor_disp) : v);
+            out[k] = so;
+            if (need_range) {
+                olo = fmin(olo, so);
+                ohi = fmax(ohi, so);
+            }
+        }
+    }
+    __syncwarp();  // the next pass reads this one's output across lanes
+    if (need_range) range = make_double2(warp_fmin((double)olo), warp_fmax((double)ohi));
+    have_range = need_range;
+}
+
+#ifndef QB_OBSW_MINB
+#define QB_OBSW_MINB 8  // measured: 64 regs, 8 blocks beat 80 regs (1.3x) and no cap (1.5x)
+#endif
+template <class S>
+__global__ void __launch_bounds__(128, QB_OBSW_MINB) k_env_observe_warp(DynConsts<xd> C, qb_env_buffers B, ObsArgs O) {
+    const int lane = threadIdx.x & 31;
+    const long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (i >= B.n) return;  // warp-uniform
+    WarpRng g;
+    {
+        const Pcg64 r = pcg_load(B.rng + 4 * i);
+        g.P = r.state;
+        g.inc = r.inc;
+        const PcgJump j = pcg64_jump(r.inc, (u128)(lane + 1));
+        g.A = j.A;
+        g.C = j.C;
+        g.A32 = shfl_u128(j.A, 31);
+        g.C32 = shfl_u128(j.C, 31);
+    }
+    for (int s = 0; s < O.n_sensors; ++s) {
+        const qb_sensor_obs &so = O.s[s];
+        S *out = static_cast<S *>(so.out);
+        if (so.kind == QB_SENSOR_IMU) {  // six readings: every lane runs the (uniform) sequential draws
+            double v[6];
+            imu_read<S>(C, static_cast<const S *>(B.state), B.ld, i, v);
+            Pcg64 r;
+            r.state = g.P;
+            r.inc = g.inc;
+            for (int m = 0; m < so.n_noise; ++m)
+                if (so.noise[m].sigma != 0.0)
+                    for (int k = 0; k < 6; ++k) v[k] = __dadd_rn(v[k], __dmul_rn(so.noise[m].sigma, normal_draw(r)));
+            g.P = r.state;
+            if (lane < 6) {
+                double vk = v[0];
+#pragma unroll
+                for (int k = 1; k < 6; ++k)
+                    if (lane == k) vk = v[k];
+                out[6 * i + lane] = (S)vk;
+            }
+            continue;
+        }
+        const long long hw = (long long)so.width * so.height;
+        const bool ids = so.kind == QB_SENSOR_SEGMENTATION;
+        const void *src = ids ? (const void *)(static_cast<const int32_t *>(so.src) + i * hw)
+                              : (const void *)(static_cast<const S *>(so.src) + i * hw);
+        S *dst = out + i * hw;
+        if (so.n_noise == 0) {  // plain copy into the observation dtype
+            for (long long k = lane; k < hw; k += 32) dst[k] = (S)px_in<S>(src, ids, k);
+            continue;
+        }
+        double2 range = make_double2(0.0, 0.0);
+        bool have_range = false;
+        for (int m = 0; m < so.n_noise; ++m) {
+            const qb_noise *nx = m + 1 < so.n_noise ? &so.noise[m + 1] : nullptr;
+            const bool need = nx && ((nx->kind == QB_NOISE_SALTPEPPER && nx->p != 0.0) || nx->kind == QB_NOISE_REDWOOD);
+            if (m == 0)
+                warp_noise_pass<S>(so.noise[m], g, src, ids, dst, hw, lane, range, have_range, need);
+            else
+                warp_noise_pass<S>(so.noise[m], g, dst, false, dst, hw, lane, range, have_range, need);
+        }
+    }
+    if (lane == 0) {
+        Pcg64 r;
+        r.state = g.P;
+        r.inc = g.inc;
+        pcg_store(B.rng + 4 * i, r);
+    }
+}
+
 __global__ void k_rng_normals(long long n, uint64_t *rng, int k, double *out) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -299,6 +562,17 @@ int launch_observe(const qb_params *p, const qb_env_buffers *b, int n_sensors, c
     }
     if (b->n == 0 || n_sensors == 0) return QB_OK;
     DynConsts<xd> C = make_consts<xd>(*p);
+    bool poisson = false;
+    for (int s = 0; s < n_sensors; ++s)
+        for (int m = 0; m < O.s[s].n_noise; ++m) poisson |= O.s[s].noise[m].kind == QB_NOISE_POISSON;
+    if (!poisson) {  // warp per env (speculative stream reads)
+        const int BS = 128;
+        if (b->dtype == QB_F32)
+            k_env_observe_warp<float><<<env_grid(b->n * 32, BS), BS, 0, st>>>(C, *b, O);
+        else
+            k_env_observe_warp<double><<<env_grid(b->n * 32, BS), BS, 0, st>>>(C, *b, O);
+        return check_launch("env_observe");
+    }
     if (b->dtype == QB_F32) {
         const int BS = ObsWarps<float>::value * 32;
         k_env_observe<float><<<env_grid(b->n, BS), BS, 0, st>>>(C, *b, O);

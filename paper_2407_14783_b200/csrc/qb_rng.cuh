@@ -131,9 +131,9 @@ QB_D double uniform_draw(Pcg64 &r, double lo, double hi) {
 // numpy by tests/test_rng_restatement.py).  All arithmetic is the IEEE
 // double op numpy's C performs (no contraction); log1p/exp are CUDA's libm
 // (<= 1 ulp from glibc), which only matters on the ~1% wedge/tail draws.
-QB_D double normal_draw(Pcg64 &r) {
+// the draw that starts with word w (already taken from r); r continues after it
+QB_D double normal_from(uint64_t w, Pcg64 &r) {
     for (;;) {
-        uint64_t w = pcg64_next64(r);
         const int idx = (int)(w & 0xff);
         w >>= 8;
         const uint64_t rabs = (w >> 1) & 0x000fffffffffffffULL;
@@ -151,7 +151,48 @@ QB_D double normal_draw(Pcg64 &r) {
         const double f0 = __ldg(&qb_zig_fi[idx - 1]), f1 = __ldg(&qb_zig_fi[idx]);
         if (__dadd_rn(__dmul_rn(__dsub_rn(f0, f1), pcg64_next_double(r)), f1) < exp(__dmul_rn(__dmul_rn(-0.5, x), x)))
             return x;
+        w = pcg64_next64(r);
     }
+}
+
+QB_D double normal_draw(Pcg64 &r) { return normal_from(pcg64_next64(r), r); }
+
+// ---- warp-parallel stream access -----------------------------------------
+// The LCG jump over d words as an affine map state -> A state + C (the
+// advance algorithm above without applying it): lets 32 lanes produce 32
+// consecutive words of one stream in parallel.
+struct PcgJump {
+    u128 A, C;
+};
+QB_HD PcgJump pcg64_jump(u128 inc, u128 delta) {
+    u128 cur_mult = qbrng::pcg_mult(), cur_plus = inc, acc_mult = 1, acc_plus = 0;
+    while (delta > 0) {
+        if (delta & 1) {
+            acc_mult *= cur_mult;
+            acc_plus = acc_plus * cur_mult + cur_plus;
+        }
+        cur_plus = (cur_mult + 1) * cur_plus;
+        cur_mult *= cur_mult;
+        delta >>= 1;
+    }
+    return {acc_mult, acc_plus};
+}
+QB_HD uint64_t pcg64_output(u128 state) {
+    uint64_t hi = (uint64_t)(state >> 64), lo = (uint64_t)state;
+    unsigned rot = (unsigned)(state >> 122);
+    uint64_t x = hi ^ lo;
+    return (x >> rot) | (x << ((64 - rot) & 63));
+}
+
+// ziggurat fast path on one word (distributions.c random_standard_normal):
+// true with x set when the word alone decides the draw (~98.8%)
+QB_D bool normal_fast(uint64_t w, double &x) {
+    const int idx = (int)(w & 0xff);
+    w >>= 8;
+    const uint64_t rabs = (w >> 1) & 0x000fffffffffffffULL;
+    x = __dmul_rn((double)rabs, __ldg(&qb_zig_wi[idx]));
+    if (w & 0x1) x = -x;
+    return rabs < __ldg(&qb_zig_ki[idx]);
 }
 
 // distributions.c random_loggam

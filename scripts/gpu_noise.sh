@@ -1,11 +1,8 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_noise.py -q -rf --tb=short -p no:cacheprovider > gpurun_out/pytest_noise.log 2>&1; echo noise=$?
+timeout 900 python -m pytest tests/test_gpu_noise.py tests/test_gpu_swarm.py tests/test_oracle.py -q -rf --tb=short -p no:cacheprovider > gpurun_out/pytest_noise.log 2>&1; echo noise=$?
 grep -E "^E  |FAILED|passed|failed" gpurun_out/pytest_noise.log | head -10
-for m in 4 3 5; do
-python -m paper_2407_14783_b200.build -D QB_OBS_MINB=$m > gpurun_out/build.log 2>&1 || { echo BUILD FAILED; exit 1; }
 timeout 600 python bench.py --workload c3n --steps 10 --warmup 3 --no-e2e --no-cpu > gpurun_out/c3n.log 2>&1
 python -c "
 import json
 l=[x for x in open('gpurun_out/c3n.log') if x.startswith('{')]
-d=json.loads(l[-1]); print('c3n $m', '%.4g'%d['value'], d.get('kernel_ms'))"
-done
+d=json.loads(l[-1]); print('c3n', '%.4g'%d['value'], d.get('kernel_ms'))"

@@ -109,6 +109,18 @@ int qb_scene_create(int32_t n_scenes, const int64_t *prim_offsets, const int64_t
                     const int64_t *prim_oid, const double *prim_lo, const double *prim_hi, qb_scene **out);
 int qb_scene_destroy(qb_scene *s);
 
+/* The same scene set built on the device (replaces the host
+ * flatten + build_bvh of shapes.py:197-212 / bvh.py:16-70 for scenes that
+ * change per episode): prim_offsets is HOST (S+1 entries), every primitive
+ * array is DEVICE memory on the current device.  The BVH is a linear BVH
+ * (Morton order, Karras hierarchy, leaves of <= 4 primitives); renders and
+ * queries equal those of a qb_scene_create handle bit for bit (results are
+ * traversal-order independent), traversal cost differs.  Stream-ordered;
+ * returns after the build has finished. */
+int qb_scene_create_device(int32_t n_scenes, const int64_t *prim_offsets, const int64_t *prim_type,
+                           const double *prim_data, const int64_t *prim_oid, const double *prim_lo,
+                           const double *prim_hi, qb_scene **out, void *stream);
+
 /* bvh.build_bvh (bvh.py:16-70) with this library's binned-SAH split, in the
  * reference's flat layout: node_count > 0 marks a leaf over
  * prim_order[first : first + count], 0 an internal node whose children are

@@ -179,6 +179,7 @@ SIGNATURES = {
     "qb_dynamics_vjp": ([_PP(QbParams), _I32, _I32, _I64, _I64, _P, _P, _P, _P, _P, _P, _P], ctypes.c_int),
     "qb_scene_create": ([_I32, _P, _P, _P, _P, _P, _P, _PP(_P)], ctypes.c_int),
     "qb_scene_destroy": ([_P], ctypes.c_int),
+    "qb_scene_create_device": ([_I32, _P, _P, _P, _P, _P, _P, _PP(_P), _P], ctypes.c_int),
     "qb_control_stage": ([_PP(QbParams), _I32, _I32, _I64, _I64, _P, _P, _P, _P, _P], ctypes.c_int),
     "qb_bvh_build": ([_I64, _P, _P, _P, _P, _P, _P, _P, _P], ctypes.c_int),
     "qb_scene_stats": ([_P, _P], ctypes.c_int),

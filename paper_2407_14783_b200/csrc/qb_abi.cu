@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "qb_internal.h"
+#include "qb_scene_pack.cuh"
 
 namespace {
 thread_local char g_err[512] = "";
@@ -190,66 +191,11 @@ static int build_bvh(int n, const double *plo, const double *phi, std::vector<BN
     return max_depth <= 62 ? 0 : -1;
 }
 
-static float f_down(double v) {
-    double m = v - 1e-6 * (1.0 + std::fabs(v));
-    float f = (float)m;
-    if ((double)f > m) f = std::nextafter(f, -INFINITY);
-    return f;
-}
-static float f_up(double v) {
-    double m = v + 1e-6 * (1.0 + std::fabs(v));
-    float f = (float)m;
-    if ((double)f < m) f = std::nextafter(f, INFINITY);
-    return f;
-}
-
-
-static float4 f4(float x, float y, float z, float w) { return make_float4(x, y, z, w); }
-
-// conservative culling bounds of one primitive (see DevScene::primc)
-static void cull_record(int type, const double *d, float4 *o) {
-    for (int k = 0; k < 4; ++k) o[k] = f4(0, 0, 0, 0);
-    if (type == QB_SPHERE) {
-        o[0] = f4((float)d[0], (float)d[1], (float)d[2], (float)(d[3] * (1.0 + 1e-6)));
-    } else if (type == QB_BOX) {
-        o[0] = f4((float)d[0], (float)d[1], (float)d[2], 0.0f);
-        for (int k = 0; k < 3; ++k)  // column k of R scaled by h_k
-            o[1 + k] = f4((float)(d[6 + k] * d[3 + k] * (1.0 + 1e-6)), (float)(d[9 + k] * d[3 + k] * (1.0 + 1e-6)),
-                          (float)(d[12 + k] * d[3 + k] * (1.0 + 1e-6)), 0.0f);
-    } else {  // triangle: bounding sphere about the centroid
-        double c[3], r2 = 0.0;
-        for (int a = 0; a < 3; ++a) c[a] = (d[a] + d[3 + a] + d[6 + a]) / 3.0;
-        for (int v = 0; v < 3; ++v) {
-            double e = 0.0;
-            for (int a = 0; a < 3; ++a) e += (d[3 * v + a] - c[a]) * (d[3 * v + a] - c[a]);
-            r2 = std::max(r2, e);
-        }
-        o[0] = f4((float)c[0], (float)c[1], (float)c[2], (float)(std::sqrt(r2) * (1.0 + 1e-6)));
-    }
-}
-static float i2f(int a) {
-    float f;
-    std::memcpy(&f, &a, 4);
-    return f;
-}
-
-static void pack_prim(int type, const double *d, float4 *o) {
-    for (int k = 0; k < 4; ++k) o[k] = f4(0, 0, 0, 0);
-    if (type == QB_SPHERE) {
-        o[0] = f4((float)d[0], (float)d[1], (float)d[2], (float)d[3]);
-        o[1] = f4((float)(d[3] * d[3]), 0, 0, 0);
-    } else if (type == QB_BOX) {
-        o[0] = f4((float)d[0], (float)d[1], (float)d[2], (float)d[3]);
-        o[1] = f4((float)d[4], (float)d[5], (float)d[6], (float)d[7]);
-        o[2] = f4((float)d[8], (float)d[9], (float)d[10], (float)d[11]);
-        o[3] = f4((float)d[12], (float)d[13], (float)d[14], 0);
-    } else {
-        double e1[3] = {d[3] - d[0], d[4] - d[1], d[5] - d[2]}, e2[3] = {d[6] - d[0], d[7] - d[1], d[8] - d[2]};
-        o[0] = f4((float)d[0], (float)d[1], (float)d[2], (float)e1[0]);
-        o[1] = f4((float)e1[1], (float)e1[2], (float)e2[0], (float)e2[1]);
-        o[2] = f4((float)e2[2], 0, 0, 0);
-    }
-}
+using qbpack::cull_record;
+using qbpack::f_down;
+using qbpack::f_up;
+using qbpack::i2f;
+using qbpack::pack_prim;
 
 template <class T> static T *dev_upload(qb_scene *s, const std::vector<T> &v) {
     void *p = nullptr;
@@ -421,6 +367,23 @@ int qb_scene_create(int32_t n_scenes, const int64_t *prim_offsets, const int64_t
     }
     *out = sc;
     return QB_OK;
+}
+
+int qb_scene_create_device(int32_t n_scenes, const int64_t *prim_offsets, const int64_t *prim_type,
+                           const double *prim_data, const int64_t *prim_oid, const double *prim_lo,
+                           const double *prim_hi, qb_scene **out, void *stream) {
+    QB_REQUIRE(out && prim_offsets && n_scenes >= 1, "qb_scene_create_device: bad arguments");
+    *out = nullptr;
+    QB_REQUIRE(prim_offsets[0] == 0, "qb_scene_create_device: prim_offsets[0] must be 0");
+    for (int s = 0; s < n_scenes; ++s)
+        if (prim_offsets[s + 1] <= prim_offsets[s]) {
+            qb::set_error("scene %d has no primitives", s);
+            return QB_EEMPTY;
+        }
+    QB_REQUIRE(prim_offsets[n_scenes] < (1LL << 30), "too many primitives");
+    QB_REQUIRE(prim_type && prim_data && prim_oid && prim_lo && prim_hi, "qb_scene_create_device: NULL prim arrays");
+    return qb::scene_create_device(n_scenes, prim_offsets, prim_type, prim_data, prim_oid, prim_lo, prim_hi, out,
+                                   qb::as_stream(stream));
 }
 
 int qb_bvh_build(int64_t n, const double *prim_lo, const double *prim_hi, int64_t *n_nodes, double *node_lo,

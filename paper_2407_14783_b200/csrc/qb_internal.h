@@ -51,6 +51,9 @@ struct qb_scene {
 
 // kernel launchers implemented in the per-kernel translation units
 namespace qb {
+int scene_create_device(int n_scenes, const int64_t *prim_offsets, const int64_t *prim_type, const double *prim_data,
+                        const int64_t *prim_oid, const double *prim_lo, const double *prim_hi, qb_scene **out,
+                        cudaStream_t st);
 int launch_dynamics_step(const qb_params *p, int kind, int dtype, long long n, long long ld, void *state,
                          const void *action, void *rotor_out, uint8_t *nonfinite, int T, const void *actions_seq,
                          cudaStream_t st);

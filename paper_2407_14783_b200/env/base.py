@@ -140,7 +140,7 @@ class QuadEnvBase:
     TASK = "free"
 
     def __init__(self, config, params: QuadParams = None, sim: SimConfig = None, gains: ControllerGains = None,
-                 device=None, dtype=None, shard=(0, 1), track_prev_state: bool = True):
+                 device=None, dtype=None, shard=(0, 1), track_prev_state: bool = True, scene_build: str = "host"):
         import torch
 
         nat.require_cuda()
@@ -165,7 +165,7 @@ class QuadEnvBase:
         self.scenes = [spec.materialize() for spec in config.scenes]
         self.sensor_cameras = [(s, None if s.kind == "imu" else s.camera()) for s in config.sensors]
         with torch.cuda.device(self.device):
-            self.dev_scenes = DeviceScenes(self.scenes, device=self.device)
+            self.dev_scenes = DeviceScenes(self.scenes, device=self.device, build=scene_build)
         self._P = native_params(self.params, self.sim, self.gains)
         self._kind = nat.CMD[config.command_type]
         self._alloc(track_prev_state)

@@ -41,14 +41,32 @@ __global__ void __launch_bounds__(128) k_rollout_bwd(DynConsts<R> C, long long n
 #pragma unroll
     for (int k = 0; k < 17; ++k) lam[k] = R(g_last[k * ld + ii]);
     bool flag = false;
-    for (int t = steps - 1; t >= 0; --t) {
-        R x[17], a[4], cmd[4];
+    // software pipeline: step t-1's tape state and action and step t's
+    // trajectory gradient are loaded while step t is computed (at C4 sizes
+    // each SM sub-partition runs about one warp, so nothing else hides the
+    // L2 latency)
+    S xn[17], an[4], gn[17];
+    auto load_step = [&](int t) {
         const S *xs = tape + (long long)t * block;
 #pragma unroll
-        for (int k = 0; k < 17; ++k) x[k] = R(xs[k * ld + ii]);
+        for (int k = 0; k < 17; ++k) xn[k] = xs[k * ld + ii];
         const S *ap = actions + ((long long)t * n + ii) * 4;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) a[k] = R(ap[k]);
+        for (int k = 0; k < 4; ++k) an[k] = ap[k];
+    };
+    load_step(steps - 1);
+    for (int t = steps - 1; t >= 0; --t) {
+        R x[17], a[4], cmd[4];
+#pragma unroll
+        for (int k = 0; k < 17; ++k) x[k] = R(xn[k]);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) a[k] = R(an[k]);
+        if (t > 0) load_step(t - 1);
+        if (!single) {
+            const S *gt = g_traj + (long long)t * block;
+#pragma unroll
+            for (int k = 0; k < 17; ++k) gn[k] = gt[k * ld + ii];
+        }
         command_to_speeds<R, KIND>(C, x, a, cmd);
         R cb[4] = {R(0.0), R(0.0), R(0.0), R(0.0)};
         dyn_step_vjp<R, SUB>(C, x, cmd, lam, cb, flag, cache);  // lam <- J^T lam (dynamics part)
@@ -81,9 +99,8 @@ __global__ void __launch_bounds__(128) k_rollout_bwd(DynConsts<R> C, long long n
             }
         }
         if (!single) {
-            const S *gt = g_traj + (long long)t * block;
 #pragma unroll
-            for (int k = 0; k < 17; ++k) lam[k] = lam[k] + R(gt[k * ld + ii]);
+            for (int k = 0; k < 17; ++k) lam[k] = lam[k] + R(gn[k]);
         }
     }
     if (live) {

@@ -66,9 +66,14 @@ __device__ __forceinline__ void dyn_body(const DynConsts<R> &C, long long n, lon
     for (int k = 0; k < 17; ++k) x[k] = R(state[k * ld + i]);
     const int steps = T > 0 ? T : 1;
     bool ok_all = true;
+    R a_next[4];
+    load4<R, S>(action + i * 4, a_next);
     for (int t = 0; t < steps; ++t) {
         R a[4], cmd[4];
-        load4<R, S>(action + ((long long)t * n + i) * 4, a);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) a[k] = a_next[k];
+        // rollouts: the next step's action is in flight during this step
+        if (t + 1 < steps) load4<R, S>(action + ((long long)(t + 1) * n + i) * 4, a_next);
         command_to_speeds<R, KIND>(C, x, a, cmd);
         if (rotor_out && T == 0) store4<R, S>(rotor_out + i * 4, cmd);
         ok_all &= dyn_step<R, SUB>(C, x, cmd);
@@ -94,12 +99,12 @@ __global__ void __launch_bounds__(128, QB_DYN_MINB) k_dyn_step(DynConsts<R> C, l
 }
 
 // horizon rollout: few envs, long per-thread loop -> no register cap (no spills)
-template <class R, int KIND>
+template <class R, int KIND, int SUB>
 __global__ void __launch_bounds__(128) k_rollout_fwd(DynConsts<R> C, long long n, long long ld,
                                                      typename storage_of<R>::type *state,
                                                      const typename storage_of<R>::type *action,
                                                      typename storage_of<R>::type *rotor_out, uint8_t *nonfinite, int T) {
-    dyn_body<R, KIND>(C, n, ld, state, action, rotor_out, nonfinite, T);
+    dyn_body<R, KIND, SUB>(C, n, ld, state, action, rotor_out, nonfinite, T);
 }
 
 template <class R, int KIND>
@@ -124,7 +129,10 @@ void launch_step(const DynConsts<R> &C, dim3 g, int B, cudaStream_t st, long lon
                  typename storage_of<R>::type *x, const typename storage_of<R>::type *a,
                  typename storage_of<R>::type *o, uint8_t *nonfinite, int T) {
     if (T > 0) {
-        k_rollout_fwd<R, KIND><<<g, B, 0, st>>>(C, n, ld, x, a, o, nonfinite, T);
+        if (std::is_same<R, float>::value && C.substeps == 2)
+            k_rollout_fwd<R, KIND, 2><<<g, B, 0, st>>>(C, n, ld, x, a, o, nonfinite, T);
+        else
+            k_rollout_fwd<R, KIND, 0><<<g, B, 0, st>>>(C, n, ld, x, a, o, nonfinite, T);
         return;
     }
     if constexpr (std::is_same<R, float>::value) {

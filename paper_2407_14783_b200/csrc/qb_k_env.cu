@@ -20,7 +20,7 @@
 #include "qb_rng.cuh"
 
 #ifndef QB_ENV_MINB
-#define QB_ENV_MINB 5  // measured: 5 blocks beats 4 and uncapped (K1+K3 at 45% of HBM at 4M envs)
+#define QB_ENV_MINB 6  // measured at 4M envs: 6 blocks (80 regs) beats 5 (96) by 2% and 8 (64, spills) by 19%
 #endif
 
 namespace {
@@ -356,33 +356,43 @@ __global__ void k_swarm_views(EnvArgs<R> A, typename storage_of<R>::type *sphere
         for (int c = 0; c < 13; ++c) obs[idx * 13 + c] = st[c * B.ld + j];
 }
 
-template <class R, int KIND, bool WARP> __global__ void __launch_bounds__(128, QB_ENV_MINB) k_env_step(EnvArgs<R> A) {
+// SUB = 2: the default two substeps unrolled at compile time (FP32 batch path)
+template <class R, int KIND, bool WARP, int SUB>
+__global__ void __launch_bounds__(128, QB_ENV_MINB) k_env_step(EnvArgs<R> A) {
     using S = typename storage_of<R>::type;
     bool lead;
     const long long i = env_index<WARP>(lead);
     const qb_env_buffers &B = A.B;
     const qb_task &T = A.T;
     if (i >= B.n) return;
+    // every per-env input is requested before the first store (one memory
+    // round trip instead of four dependent ones at 20 warps/SM); a respawn
+    // rewrites step count and scene, re-read on that (rare) path
     R x[17];
     load_state(A, i, x);
-    if (T.auto_reset && B.needs_respawn[i] && !T.swarm) spawn<R, WARP>(A, i, x, lead);
+    const bool respawn = T.auto_reset && B.needs_respawn[i] && !T.swarm;
+    R a[4], cmd[4];
+    const S *act = static_cast<const S *>(B.action) + 4 * i;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) a[k] = R(act[k]);
+    int steps = B.step_count[i] + 1;
+    int scene = B.agent_scene[i];
+    if (respawn) {
+        spawn<R, WARP>(A, i, x, lead);
+        steps = 1;
+        scene = B.agent_scene[i];
+    }
     R prev[17];
 #pragma unroll
     for (int k = 0; k < 17; ++k) prev[k] = x[k];
     if (B.prev_state && lead) store_planes(B.prev_state, B.ld, i, x);
 
-    R a[4], cmd[4];
-    const S *act = static_cast<const S *>(B.action) + 4 * i;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) a[k] = R(act[k]);
     command_to_speeds<R, KIND>(A.C, x, a, cmd);
-    const bool ok = dyn_step(A.C, x, cmd) && !(r_isnan(a[0]) || r_isnan(a[1]) || r_isnan(a[2]) || r_isnan(a[3]));
+    const bool ok = dyn_step<R, SUB>(A.C, x, cmd) && !(r_isnan(a[0]) || r_isnan(a[1]) || r_isnan(a[2]) || r_isnan(a[3]));
     if (!ok) {
 #pragma unroll
         for (int k = 0; k < 17; ++k) x[k] = prev[k];
     }
-    const int steps = B.step_count[i] + 1;
-    const int scene = B.agent_scene[i];
     Proximity pr = proximity<R, WARP>(A, scene, x);
 
     double pp[3] = {r_dbl(prev[0]), r_dbl(prev[1]), r_dbl(prev[2])};
@@ -419,6 +429,16 @@ __global__ void k_rng_doubles(long long n, uint64_t *rng, int k, double *out) {
     pcg_store(rng + 4 * i, r);
 }
 
+template <class R, int K>
+void launch_env_step(const EnvArgs<R> &A, bool warp, bool sub2, dim3 g, int BS, cudaStream_t st) {
+    if (warp)
+        k_env_step<R, K, true, 0><<<g, BS, 0, st>>>(A);
+    else if constexpr (std::is_same<R, float>::value)
+        sub2 ? k_env_step<R, K, false, 2><<<g, BS, 0, st>>>(A) : k_env_step<R, K, false, 0><<<g, BS, 0, st>>>(A);
+    else
+        k_env_step<R, K, false, 0><<<g, BS, 0, st>>>(A);
+}
+
 template <class R>
 int dispatch_env(int mode, const qb_params *p, int kind, const qb_task *task, const qb_scene *s, const qb_env_buffers *b,
                  uint64_t seed, cudaStream_t st) {
@@ -450,7 +470,8 @@ int dispatch_env(int mode, const qb_params *p, int kind, const qb_task *task, co
         return qb::check_launch("env_reset");
     }
     if (swarm && task->auto_reset) k_swarm_spawn<R><<<1, 32, 0, st>>>(A, 0);
-#define QB_ENV(K) (warp ? (k_env_step<R, K, true><<<g, BS, 0, st>>>(A), 0) : (k_env_step<R, K, false><<<g, BS, 0, st>>>(A), 0))
+    const bool sub2 = std::is_same<R, float>::value && A.C.substeps == 2;
+#define QB_ENV(K) launch_env_step<R, K>(A, warp, sub2, g, BS, st)
     switch (kind) {
         case QB_CMD_SRT: QB_ENV(QB_CMD_SRT); break;
         case QB_CMD_CTBR: QB_ENV(QB_CMD_CTBR); break;

@@ -1,11 +1,7 @@
 mkdir -p gpurun_out
-for m in 4 5 1; do
+timeout 900 python -m pytest tests -m gpu -q -rf --tb=short -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
+grep -E "^E  |FAILED|passed|failed" gpurun_out/pytest_gpu.log | head -10
+for m in 5 6; do
 python -m paper_2407_14783_b200.build -D QB_ENV_MINB=$m > gpurun_out/build.log 2>&1 || { echo BUILD FAILED; exit 1; }
-timeout 600 python bench.py --workload c1 --steps 20 --warmup 3 --no-e2e --no-cpu > gpurun_out/c1.log 2>&1
-python -c "
-import json
-l=[x for x in open('gpurun_out/c1.log') if x.startswith('{')]
-d=json.loads(l[-1]); print('env $m', '%.4g'%d['value'], d['roofline_env_step']['frac'], d['roofline_env_step']['ms'])"
+echo "minb $m: $(PYTHONPATH=. timeout 300 python scripts/envstep_time.py 2>&1 | tail -1)"
 done
-python -m paper_2407_14783_b200.build --force > gpurun_out/build.log 2>&1
-timeout 900 python -m pytest tests/test_gpu_env.py tests/test_gpu_swarm.py tests/test_gpu_noise.py -q -p no:cacheprovider > gpurun_out/pytest_env.log 2>&1; echo pytest=$?; tail -1 gpurun_out/pytest_env.log

@@ -177,25 +177,56 @@ QB_D NearestResult nearest_point(const DevScene &S, int scene, double qx_, doubl
 // e.g. the 6-box garage): a straight scan in primitive order with the same
 // (d2, lowest id, first primitive) result as the BVH walk, without its
 // local-memory stack and node tests.
+//
+// Boxes whose rotation is exactly the identity (flagged by the packer) take
+// closest_on_box with its products by 1 and by +0 written out: 1*a == a and
+// 0*b == copysign(0, b) for finite b, so every sum sees the same operands and
+// the result has the same bits (signed zeros included) without the 18
+// rotation products and 9 loads; non-finite queries take the general form.
 constexpr int NEAREST_SCAN_MAX = 16;
+QB_D V3<xd> closest_on_aabb(const double *dd, xd qx, xd qy, xd qz) {
+    const xd cx(__ldg(dd)), cy(__ldg(dd + 1)), cz(__ldg(dd + 2)), hx(__ldg(dd + 3)), hy(__ldg(dd + 4)), hz(__ldg(dd + 5));
+    const xd dx = qx - cx, dy = qy - cy, dz = qz - cz;
+    auto z = [](xd b) { return xd(copysign(0.0, b.v)); };  // +0 * b
+    // lx = d6*dx + d9*dy + d12*dz with (d6, d9, d12) = (1, 0, 0), etc.
+    const xd lx = (dx + z(dy)) + z(dz), ly = (z(dx) + dy) + z(dz), lz = (z(dx) + z(dy)) + dz;
+    xd px = py_min(py_max(lx, -hx), hx), py = py_min(py_max(ly, -hy), hy), pz = py_min(py_max(lz, -hz), hz);
+    if (px == lx && py == ly && pz == lz) {  // interior: nearest face
+        const xd gx = hx - r_abs(lx), gy = hy - r_abs(ly), gz = hz - r_abs(lz);
+        if (gx <= gy && gx <= gz)
+            px = lx >= xd(0.0) ? hx : -hx;
+        else if (gy <= gz)
+            py = ly >= xd(0.0) ? hy : -hy;
+        else
+            pz = lz >= xd(0.0) ? hz : -hz;
+    }
+    // (d6*px + d7*py + d8*pz) + cx with (d6, d7, d8) = (1, 0, 0), etc.
+    return {((px + z(py)) + z(pz)) + cx, ((z(px) + py) + z(pz)) + cy, ((z(px) + z(py)) + pz) + cz};
+}
+
 QB_D NearestResult nearest_point_scan(const DevScene &S, int p0, int p1, double qx_, double qy_, double qz_) {
     xd qx(qx_), qy(qy_), qz(qz_);
+    const bool finite_q = isfinite(qx_) && isfinite(qy_) && isfinite(qz_);
     double best = infinity_d();
     int best_id = -1;
     double bx = 0.0, by = 0.0, bz = 0.0;
     for (int p = p0; p < p1; ++p) {
         const int2 m = __ldg(S.meta + p);
         const double *dd = S.primd + 16 * p;
-        xd d[15];
-#pragma unroll
-        for (int k = 0; k < 15; ++k) d[k] = xd(__ldg(dd + k));
         V3<xd> c;
-        if (m.x == QB_SPHERE)
-            c = closest_on_sphere<xd>(d[0], d[1], d[2], d[3], qx, qy, qz);
-        else if (m.x == QB_BOX)
-            c = closest_on_box<xd>(d, qx, qy, qz);
-        else
-            c = closest_on_triangle<xd>(d, qx, qy, qz);
+        if (m.x == QB_BOX && finite_q && __ldg(&S.primf[4 * p + 3].w) != 0.0f) {
+            c = closest_on_aabb(dd, qx, qy, qz);
+        } else {
+            xd d[15];
+#pragma unroll
+            for (int k = 0; k < 15; ++k) d[k] = xd(__ldg(dd + k));
+            if (m.x == QB_SPHERE)
+                c = closest_on_sphere<xd>(d[0], d[1], d[2], d[3], qx, qy, qz);
+            else if (m.x == QB_BOX)
+                c = closest_on_box<xd>(d, qx, qy, qz);
+            else
+                c = closest_on_triangle<xd>(d, qx, qy, qz);
+        }
         xd ex = qx - c.x, ey = qy - c.y, ez = qz - c.z;
         const double pd2 = (ex * ex + ey * ey + ez * ez).v;
         if (pd2 < best || (pd2 == best && m.y < best_id)) {

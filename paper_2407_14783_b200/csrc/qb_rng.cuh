@@ -149,8 +149,13 @@ QB_D double normal_from(uint64_t w, Pcg64 &r) {
             }
         }
         const double f0 = __ldg(&qb_zig_fi[idx - 1]), f1 = __ldg(&qb_zig_fi[idx]);
-        if (__dadd_rn(__dmul_rn(__dsub_rn(f0, f1), pcg64_next_double(r)), f1) < exp(__dmul_rn(__dmul_rn(-0.5, x), x)))
-            return x;
+        const double lhs = __dadd_rn(__dmul_rn(__dsub_rn(f0, f1), pcg64_next_double(r)), f1);
+        const double arg = __dmul_rn(__dmul_rn(-0.5, x), x);  // in [-6.7, 0] on the wedges
+        // decide with a float exp when lhs is clearly off it (|error| < 1e-6
+        // relative here vs the 1e-5 margin); the double exp only near the edge
+        const double ef = (double)__expf((float)arg);
+        if (lhs < ef * (1.0 - 1e-5)) return x;
+        if (!(lhs > ef * (1.0 + 1e-5)) && lhs < exp(arg)) return x;
         w = pcg64_next64(r);
     }
 }

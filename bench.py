@@ -44,7 +44,8 @@ sys.path.insert(0, ROOT)
 METRIC = "env-steps/sec (= 64x64 depth frames/sec), whole box"
 WORKLOADS = {
     "c1": "hover free flight (garage), dynamics only, 100 envs/GPU (BASELINE config 1)",
-    "c2": "navigation, 64x64 depth, 100 envs/GPU (BASELINE config 2)",
+    "c2": "navigation, 64x64 depth, 100 envs/GPU, procedural box/cylinder triangle-mesh room (BASELINE config 2)",
+    "c2a": "config 2 on the analytic scene (the same room and obstacles as spheres / oriented boxes)",
     "c3": "navigation, 64x64 depth+segmentation, 65536 envs/GPU (BASELINE config 3)",
     "c4": "BPTT through dynamics, 16384 envs/GPU, horizon 64, loss/grad all-reduce (BASELINE config 4)",
     "c5": "landing on a 5e5-triangle indoor mesh, 64x64 down depth+seg, 131072 envs/GPU (BASELINE config 5, 1M on 8 GPUs)",
@@ -53,7 +54,7 @@ WORKLOADS = {
     "swarm": "swarm gap crossing (SURVEY F2): one swarm of 256 agents, 64x64 depth with the other 255 agents "
              "rendered as spheres, pairwise collisions",
 }
-ENVS = {"c1": 100, "c2": 100, "c3": 65536, "c4": 16384, "c5": 131072, "c3n": 65536, "swarm": 256}
+ENVS = {"c1": 100, "c2": 100, "c2a": 100, "c3": 65536, "c4": 16384, "c5": 131072, "c3n": 65536, "swarm": 256}
 
 
 def peaks():
@@ -165,7 +166,10 @@ def workload_config(kind, n):
 
     if kind == "c1":
         return EnvConfig(num_agents=n, command_type="ctbr", episode_max_steps=1000)
-    if kind == "c2":
+    if kind == "c2":  # the tessellated variant (SURVEY 8-D C2 b): 69 objects, 2076 triangles
+        cfg = navigation_config(scene_seed=0, num_agents=n)
+        return dataclasses.replace(cfg, scenes=(dataclasses.replace(cfg.scenes[0], kind="cluttered_mesh"),))
+    if kind == "c2a":
         return navigation_config(scene_seed=0, num_agents=n)
     if kind == "c3":
         return navigation_config(scene_seed=0, num_agents=n, with_segmentation=True)

@@ -123,7 +123,7 @@ template <bool FROM_STATE>
 __global__ void __launch_bounds__(QB_RF_BLOCK, QB_RF_MINB) k_render_f(DevScene S, CamF cam, long long n, long long ld, const float *state,
                                                      const float *origins, const float *rotations, const int32_t *env_scene,
                                                      float *depth, int32_t *seg, int centroid_id, float *centroid,
-                                                     const float *extra, const int32_t *extra_ids, int n_extra) {
+                                                     const float *extra, const int32_t *extra_ids, int n_extra, int split) {
     constexpr int WPB = QB_RF_BLOCK / 32, STK = 96;  // stack: <= 32 frontier entries + one per tree level (<= 62)
     __shared__ int2 stk_s[WPB][STK];  // (node record packed as a * 8 + (b + 2), entry distance bits)
     __shared__ int fr_s[WPB][32];     // camera frontier (node indices)
@@ -141,7 +141,11 @@ __global__ void __launch_bounds__(QB_RF_BLOCK, QB_RF_MINB) k_render_f(DevScene S
     const float sx = 2.0f / W, sy = 2.0f / H;
     constexpr unsigned INF_BITS = 0x7f800000u;
 
-    for (long long c = warp; c < n; c += nwarps) {
+    // small batches: `split` warps share one camera (each builds the camera
+    // frontier and takes every split-th tile)
+    for (long long wi = warp; wi < n * split; wi += nwarps) {
+        const long long c = wi / split;
+        const int part = (int)(wi % split);
         float o[3];
         {
             float Rw[9];
@@ -214,7 +218,7 @@ __global__ void __launch_bounds__(QB_RF_BLOCK, QB_RF_MINB) k_render_f(DevScene S
             }
         }
 
-        for (int tile = 0; tile < tiles_x * tiles_y; ++tile) {
+        for (int tile = part; tile < tiles_x * tiles_y; tile += split) {
             const int j0 = (tile % tiles_x) * TILE_W, i0 = (tile / tiles_x) * TILE_H;
             const int j = j0 + (lane & 7);
             const int i = i0 + (lane >> 3);
@@ -390,7 +394,7 @@ __global__ void __launch_bounds__(QB_RF_BLOCK, QB_RF_MINB) k_render_f(DevScene S
                 }
             }
         }
-        if (centroid_id > 0) {
+        if (centroid_id > 0 && split == 1) {  // (split: the k_centroid pass)
 #pragma unroll
             for (int s = 16; s > 0; s >>= 1) {
                 cnt += __shfl_xor_sync(FULL, cnt, s);
@@ -1008,17 +1012,32 @@ int launch_render(const qb_scene *s, const qb_camera *cam, int dtype, long long 
             return check_launch("centroid");
         }
         const int B = QB_RF_BLOCK;
-        long long blocks = (n * 32 + B - 1) / B;
+        // small batches split a camera's tiles over warps (one warp renders a
+        // 64x64 frame in ~1 ms: 128 tiles in sequence) up to ~48 warps per SM
+#ifndef QB_RF_WANT
+#define QB_RF_WANT 48
+#endif
+#ifndef QB_RF_TPW
+#define QB_RF_TPW 2
+#endif
+        const long long want = (long long)sm_count() * QB_RF_WANT;
+        const int tiles = ((c.W + TILE_W - 1) / TILE_W) * ((c.H + TILE_H - 1) / TILE_H);
+        int split = (int)std::min<long long>(std::max(tiles / QB_RF_TPW, 1), std::max<long long>(1, want / std::max(n, 1LL)));
+        if (split > 1 && !seg && centroid_id > 0) split = 1;  // the centroid pass reads seg
+        long long blocks = (n * split * 32 + B - 1) / B;
         if (blocks > 0x7fffffffLL) blocks = 0x7fffffffLL;  // grid-stride loop covers the rest
         if (state)
             k_render_f<true><<<(int)blocks, B, 0, st>>>(s->dev, c, n, ld, (const float *)state, nullptr, nullptr, env_scene,
                                                         (float *)depth, seg, centroid_id, centroid, (const float *)extra,
-                                                        extra_ids, n_extra);
+                                                        extra_ids, n_extra, split);
         else
             k_render_f<false><<<(int)blocks, B, 0, st>>>(s->dev, c, n, ld, nullptr, (const float *)origins,
                                                          (const float *)rotations, env_scene, (float *)depth, seg, 0, nullptr,
-                                                         (const float *)extra, extra_ids, n_extra);
-        return check_launch("render_f32");
+                                                         (const float *)extra, extra_ids, n_extra, split);
+        int rc = check_launch("render_f32");
+        if (rc || split == 1 || centroid_id <= 0 || !state) return rc;
+        k_centroid<<<env_grid(n, 128), 128, 0, st>>>(n, c.W, c.H, seg, centroid_id, centroid);
+        return check_launch("centroid");
     }
     CamD c;
     c.W = cam->width;

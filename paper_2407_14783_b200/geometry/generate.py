@@ -171,6 +171,29 @@ def _cylinder_mesh(center, radius, height, segments, rings):
     return verts + np.asarray(center, float), np.concatenate(tris)
 
 
+def cluttered_mesh_scene(seed: int, volume: AABB, density: float, size_range=(0.1, 0.3), segments: int = 16) -> Scene:
+    """BASELINE config 2's "procedural box/cylinder mesh scene" (SURVEY 8-D C2
+    variant b): generate_cluttered_scene's room and obstacles, same Generator
+    draws and object ids, every object tessellated into a TriMesh -- boxes
+    (walls included) as 12 triangles, each sphere as the closed cylinder
+    circumscribing it (radius r, height 2r, `segments`-gon)."""
+    base = generate_cluttered_scene(seed, volume, density, size_range)
+    objs = []
+    for o in base.objects:
+        s = o.shape
+        if isinstance(s, Box):
+            v, t = _box_mesh(s.center, s.half_extents, s.rotation, 1)
+        else:
+            r = s.radius
+            v, t = _cylinder_mesh(s.center - np.array([0.0, 0.0, r]), r, 2.0 * r, segments, 1)
+            bottom = len(v)  # close the bottom (the top cap is in _cylinder_mesh)
+            v = np.concatenate([v, (s.center - np.array([0.0, 0.0, r]))[None]])
+            a = np.arange(segments)
+            t = np.concatenate([t, np.stack([(a + 1) % segments, a, np.full(segments, bottom)], 1)])
+        objs.append(SceneObject(o.id, TriMesh(v, t)))
+    return Scene(objs)
+
+
 def indoor_mesh_scene(seed: int = 0, target_triangles: int = 500_000, size=(30.0, 30.0, 6.0)) -> Scene:
     """Procedural indoor hall of ~target_triangles triangles (config 5).
 

@@ -119,3 +119,55 @@ def test_dynamics_ragged_batches(n):
             assert np.array_equal(got, ref)
         else:
             assert state_error(got, ref).max() < 1e-5
+
+
+def test_config2_mesh_scene_vs_oracle():
+    """BASELINE config 2's box/cylinder mesh room (SceneSpec cluttered_mesh):
+    FP64 renders bit-exact and FP32 within tolerance against the oracle on the
+    same triangles, and the exact nearest point against the oracle's."""
+    from paper_2407_14783_b200.env import SceneSpec
+
+    sc = SceneSpec(kind="cluttered_mesh", seed=0, volume_lo=[-5, -5, 0], volume_hi=[5, 5, 4]).materialize()
+    a = sc.arrays
+    t = oracle.OracleScene(a.prim_type, a.prim_data, a.prim_object_id, a.prim_aabb_lo, a.prim_aabb_hi)
+    ds = DeviceScenes([sc], device=DEV)
+    rng = np.random.default_rng(2)
+    n = 64
+    pos = rng.uniform([-4.0, -4.0, 0.5], [4.0, 4.0, 3.5], (n, 3))
+    q = rng.normal(size=(n, 4)) + np.array([2.0, 0, 0, 0])
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    cam = CameraModel(rotation=FORWARD)
+    pl64 = torch.zeros((17, n), dtype=torch.float64, device=DEV)
+    pl64[0:3] = torch.as_tensor(pos.T)
+    pl64[6:10] = torch.as_tensor(q.T)
+    st = pl64.T.cpu().numpy()
+    o, r = oracle.camera_pose_world(st[:, 0:3], st[:, 6:10], cam.rotation, cam.translation)
+    d64 = torch.empty((n, 64, 64), dtype=torch.float64, device=DEV)
+    s64 = torch.empty((n, 64, 64), dtype=torch.int32, device=DEV)
+    render_state(ds, cam, pl64, depth=d64, seg=s64)
+    d0, i0 = t.render(o, r, 64, 64, cam.tan_half_h, cam.tan_half_v, cam.max_range)
+    assert np.array_equal(s64.cpu().numpy(), i0) and np.array_equal(d64.cpu().numpy(), d0)
+    pl32 = pl64.float()
+    st32 = pl32.T.double().cpu().numpy()
+    o, r = oracle.camera_pose_world(st32[:, 0:3], st32[:, 6:10], cam.rotation, cam.translation)
+    graz, d0, i0 = grazing_mask(t, o, r, 64, 64, cam.tan_half_h, cam.tan_half_v, cam.max_range)
+    d = torch.empty((n, 64, 64), dtype=torch.float32, device=DEV)
+    sg = torch.empty((n, 64, 64), dtype=torch.int32, device=DEV)
+    render_state(ds, cam, pl32, depth=d, seg=sg)
+    dd, ss = d.double().cpu().numpy(), sg.cpu().numpy()
+    bad = (ss != i0) | (np.abs(dd - d0) > DEPTH_TOL)
+    nb = bad & ~graz
+    print("mesh config 2:", f"grazing {graz.mean():.2e} mismatched {bad.mean():.2e} non-grazing {int(nb.sum())}",
+          [(tuple(int(v) for v in k), float(dd[tuple(k)]), int(ss[tuple(k)]), float(d0[tuple(k)]), int(i0[tuple(k)]))
+           for k in np.argwhere(nb)[:6]])
+    # FP32 Moeller-Trumbore can open a crack along an edge two triangles of one
+    # mesh share (a ray through it reaches the object's far side): measured 1
+    # pixel in 262144 here; the exact-double renders above have none
+    assert nb.mean() <= 1e-5 and bad.mean() < 1e-3
+    from paper_2407_14783_b200.geometry.queries import nearest_points
+
+    qs = rng.uniform([-5, -5, 0], [5, 5, 4], (300, 3))
+    _, dist, oid = nearest_points(ds, qs)
+    _, rd, rid = t.nearest_point(qs)
+    assert np.array_equal(oid.cpu().numpy(), rid)
+    assert np.abs(dist.cpu().numpy() - rd).max() < 1e-12

@@ -232,3 +232,33 @@ def test_abi_argument_validation_without_gpu():
     # empty primitive set
     cnt = ctypes.c_int64(0)
     assert lib.qb_bvh_build(0, None, None, ctypes.byref(cnt), None, None, None, None, None) != 0
+
+
+def test_cluttered_mesh_scene_tessellates_the_nav_room():
+    """Config 2's mesh room: the analytic navigation scene's objects (same
+    Generator draws, same ids), boxes as 12 triangles, spheres as closed
+    16-gon cylinders (64 triangles) circumscribing them."""
+    import numpy as np
+
+    from paper_2407_14783_b200.env import SceneSpec
+    from paper_2407_14783_b200.geometry import Box, TriMesh
+
+    kw = dict(seed=0, volume_lo=[-5, -5, 0], volume_hi=[5, 5, 4])
+    ana = SceneSpec(kind="cluttered", **kw).materialize()
+    mesh = SceneSpec(kind="cluttered_mesh", **kw).materialize()
+    assert [o.id for o in ana.objects] == [o.id for o in mesh.objects]
+    for a, m in zip(ana.objects, mesh.objects):
+        assert isinstance(m.shape, TriMesh)
+        v = m.shape.vertices
+        if isinstance(a.shape, Box):
+            assert len(m.shape.triangles) == 12
+            loc = (v - a.shape.center) @ a.shape.rotation  # local coordinates: the box corners
+            assert np.allclose(np.abs(loc), a.shape.half_extents)
+        else:
+            assert len(m.shape.triangles) == 64
+            c, r = a.shape.center, a.shape.radius
+            rad = np.linalg.norm(v[:, :2] - c[:2], axis=1)
+            assert np.allclose(rad[rad > 1e-9], r) and (rad <= 1e-9).sum() == 2  # 32 ring vertices + 2 cap centres
+            assert np.isclose(v[:, 2].min(), c[2] - r) and np.isclose(v[:, 2].max(), c[2] + r)
+    t = mesh.arrays
+    assert (t.prim_type == 2).all() and len(t) == 2076

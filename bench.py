@@ -3,7 +3,7 @@
 BASELINE.json metric: env-steps/s and 64x64 depth frames/s (whole box) at
 1/2/4/8 B200 vs the CPU reference.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c3|c1|c2|c4|c5|c3n] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c3|c1|c2|c2a|c4|c5|c3n|swarm] [--impl ours|reference]
   torchrun --nproc-per-node N bench.py --gpus N ...      (one rank per GPU, NCCL)
 
 Default workload = BASELINE config 3, the largest single-GPU config:

@@ -1,5 +1,5 @@
 mkdir -p gpurun_out
-for w in c3 c1 c2 c4 c5 c3n swarm; do
+for w in c3 c1 c2 c2a c4 c5 c3n swarm; do
   timeout 900 python bench.py --workload $w --steps 10 --warmup 3 > gpurun_out/bench_$w.log 2>&1; echo bench_$w=$?
 done
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.log 2>&1; echo ref=$?

@@ -431,12 +431,14 @@ __global__ void k_rng_doubles(long long n, uint64_t *rng, int k, double *out) {
 
 template <class R, int K>
 void launch_env_step(const EnvArgs<R> &A, bool warp, bool sub2, dim3 g, int BS, cudaStream_t st) {
-    if (warp)
-        k_env_step<R, K, true, 0><<<g, BS, 0, st>>>(A);
-    else if constexpr (std::is_same<R, float>::value)
-        sub2 ? k_env_step<R, K, false, 2><<<g, BS, 0, st>>>(A) : k_env_step<R, K, false, 0><<<g, BS, 0, st>>>(A);
-    else
-        k_env_step<R, K, false, 0><<<g, BS, 0, st>>>(A);
+    if constexpr (std::is_same<R, float>::value) {
+        if (warp)
+            sub2 ? k_env_step<R, K, true, 2><<<g, BS, 0, st>>>(A) : k_env_step<R, K, true, 0><<<g, BS, 0, st>>>(A);
+        else
+            sub2 ? k_env_step<R, K, false, 2><<<g, BS, 0, st>>>(A) : k_env_step<R, K, false, 0><<<g, BS, 0, st>>>(A);
+    } else {
+        warp ? k_env_step<R, K, true, 0><<<g, BS, 0, st>>>(A) : k_env_step<R, K, false, 0><<<g, BS, 0, st>>>(A);
+    }
 }
 
 template <class R>

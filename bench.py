@@ -649,10 +649,11 @@ def reference_arm(args, kind):
         metric = "BPTT env-steps/sec (forward + adjoint), whole box"
     else:
         vals = []
-        ns = {"c5": 64, "swarm": 256}.get(kind, 512)
+        ns = min({"c5": 64, "swarm": 256}.get(kind, 512), ENVS[kind])  # never more envs than the config has
+        st = 2 if ns > 100 else 40  # small configs: enough steps for a measurable sample
         for _ in range(max(1, min(args.steps, 5))):
-            vals.append(cpu_baseline_env(kind, n_sample=ns, steps=2)[0])
-        unit, sample, metric = "env-steps/s", f"{ns} envs x 2 steps per step (C oracle, OpenMP)", METRIC
+            vals.append(cpu_baseline_env(kind, n_sample=ns, steps=st)[0])
+        unit, sample, metric = "env-steps/s", f"{ns} envs x {st} steps per step (C oracle, OpenMP)", METRIC
     v = float(np.median(vals))
     line = {"impl": "reference", "metric": metric, "value": v, "unit": unit, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "higher_is_better": True, "config": {"workload": WORKLOADS[kind]},

@@ -255,23 +255,40 @@ __global__ void k_fill_u64(long long n, unsigned long long *p, unsigned long lon
     if (i < n) p[i] = (i % 6) < 3 ? lo_val : hi_val;
 }
 
-template <class T> T *dalloc(qb_scene *s, size_t count) {
+// the scene's own arrays come from the same stream-ordered pool (freed by
+// qb_scene_destroy's cudaFree)
+template <class T> T *dalloc(qb_scene *s, size_t count, cudaStream_t st) {
     void *p = nullptr;
-    if (cudaMalloc(&p, std::max<size_t>(count * sizeof(T), 16)) != cudaSuccess) return nullptr;
+    if (cudaMallocAsync(&p, std::max<size_t>(count * sizeof(T), 16), st) != cudaSuccess) return nullptr;
     s->allocs[s->n_allocs++] = p;
     return static_cast<T *>(p);
 }
 
+// build scratch: stream-ordered allocations from the device's default pool,
+// which keeps the pages mapped between builds (cudaMalloc / cudaFree of the
+// ~60 MB of scratch per 5e5-triangle build otherwise costs 10-250 ms of page
+// mapping and device-wide synchronisation)
+void keep_pool_mapped() {
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t keep = 1ull << 30;  // keep up to 1 GiB of freed build memory mapped
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+}
+
 struct Scratch {
+    cudaStream_t st;
     std::vector<void *> ptrs;
+    explicit Scratch(cudaStream_t s) : st(s) {}
     template <class T> T *get(size_t count) {
         void *p = nullptr;
-        if (cudaMalloc(&p, std::max<size_t>(count * sizeof(T), 16)) != cudaSuccess) return nullptr;
+        if (cudaMallocAsync(&p, std::max<size_t>(count * sizeof(T), 16), st) != cudaSuccess) return nullptr;
         ptrs.push_back(p);
         return static_cast<T *>(p);
     }
     ~Scratch() {
-        for (void *p : ptrs) cudaFree(p);
+        for (void *p : ptrs) cudaFreeAsync(p, st);
     }
 };
 
@@ -300,6 +317,7 @@ int scene_create_device(int n_scenes, const int64_t *prim_offsets, const int64_t
         set_error("qb_scene_create_device: too many nodes");
         return QB_EINVAL;
     }
+    keep_pool_mapped();
     qb_scene *sc = new qb_scene();
     sc->n_allocs = 0;
     sc->host_bounds = nullptr;
@@ -312,16 +330,16 @@ int scene_create_device(int n_scenes, const int64_t *prim_offsets, const int64_t
     DevScene &d = sc->dev;
     d.n_scenes = S;
     d.n_prims = (int)P;
-    int *root = dalloc<int>(sc, S);
-    double *bounds = dalloc<double>(sc, 6 * (size_t)S);
-    float4 *nodef = dalloc<float4>(sc, 2 * (size_t)total_nodes);
-    double *noded = dalloc<double>(sc, 6 * (size_t)total_nodes);
-    int2 *nodei = dalloc<int2>(sc, (size_t)total_nodes);
-    float4 *primf = dalloc<float4>(sc, 4 * (size_t)P);
-    double *primd = dalloc<double>(sc, 16 * (size_t)P);
-    int2 *meta = dalloc<int2>(sc, (size_t)P);
-    int *poff = dalloc<int>(sc, S + 1);
-    float4 *primc = dalloc<float4>(sc, 4 * (size_t)P);
+    int *root = dalloc<int>(sc, S, st);
+    double *bounds = dalloc<double>(sc, 6 * (size_t)S, st);
+    float4 *nodef = dalloc<float4>(sc, 2 * (size_t)total_nodes, st);
+    double *noded = dalloc<double>(sc, 6 * (size_t)total_nodes, st);
+    int2 *nodei = dalloc<int2>(sc, (size_t)total_nodes, st);
+    float4 *primf = dalloc<float4>(sc, 4 * (size_t)P, st);
+    double *primd = dalloc<double>(sc, 16 * (size_t)P, st);
+    int2 *meta = dalloc<int2>(sc, (size_t)P, st);
+    int *poff = dalloc<int>(sc, S + 1, st);
+    float4 *primc = dalloc<float4>(sc, 4 * (size_t)P, st);
     if (!root || !bounds || !nodef || !noded || !nodei || !primf || !primd || !meta || !poff || !primc)
         return fail(QB_ENOMEM, "allocation failed");
     d.root = root;
@@ -335,7 +353,7 @@ int scene_create_device(int n_scenes, const int64_t *prim_offsets, const int64_t
     d.prim_offset = poff;
     d.primc = primc;
 
-    Scratch tmp;
+    Scratch tmp(st);
     const size_t n = (size_t)max_cnt;
     unsigned long long *keys = tmp.get<unsigned long long>(n), *keys_s = tmp.get<unsigned long long>(n);
     int *vals = tmp.get<int>(n), *order = tmp.get<int>(n);

@@ -171,3 +171,31 @@ def test_config2_mesh_scene_vs_oracle():
     _, rd, rid = t.nearest_point(qs)
     assert np.array_equal(oid.cpu().numpy(), rid)
     assert np.abs(dist.cpu().numpy() - rd).max() < 1e-12
+
+
+def test_warp_nearest_point_on_large_mesh_scene():
+    """Small batches run one warp per env; on scenes beyond the warp's
+    brute-force size (> 1024 primitives) every lane walks the BVH.  Proximity
+    after every step (nearest distance, collision) equals the oracle's exact
+    query on the env's own states; spawns and respawns go through the same
+    query."""
+    import dataclasses
+
+    from paper_2407_14783_b200.control import LV
+    from paper_2407_14783_b200.env import make_env, navigation_config
+
+    cfg = navigation_config(scene_seed=0, num_agents=64, with_vision=False)
+    cfg = dataclasses.replace(cfg, scenes=(dataclasses.replace(cfg.scenes[0], kind="cluttered_mesh"),))
+    env = make_env(cfg)
+    env.reset(seed=5)
+    a = env.scenes[0].arrays
+    assert len(a) > 1024
+    t = oracle.OracleScene(a.prim_type, a.prim_data, a.prim_object_id, a.prim_aabb_lo, a.prim_aabb_hi)
+    g = torch.Generator(device=DEV).manual_seed(3)
+    for _ in range(25):
+        v = torch.randn((64, 3), device=DEV, generator=g) * 2.0
+        env.step(LV(v, torch.zeros(64, device=DEV)))
+        pos = env._planes[0:3].T.double().cpu().numpy()
+        _, rd, _ = t.nearest_point(pos)
+        assert np.array_equal(env.nearest_dist.cpu().numpy(), rd)
+        assert np.array_equal(env.collision.cpu().numpy(), rd < cfg.collision_radius)

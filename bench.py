@@ -615,6 +615,23 @@ def main():
                 "rays_per_s": r["n"] * 64 * 64 / (r["render_ms"] / 1e3),
                 "ncu": {k: meta[k] for k in ("issue_active_pct", "warps_active_pct", "l1_hit_pct", "l2_hit_pct",
                                              "registers", "source") if k in meta} if meta else None}
+            # the renderer's real bound: SM instruction issue.  Peak = 148 SMs x 4 schedulers x
+            # the SM clock seen under load; achieved = ncu's warp-instructions per camera x cameras / kernel time.
+            # Beside it, the reference algorithm's op count per ray (its BVH traversal counts)
+            # x rays/s against the FP32 lane peak: above 1 means culling removed work the reference does.
+            mhz = (r["clocks"] or {}).get("sm_mhz") or 1965.0
+            if meta and meta.get("warp_instructions_per_unit"):
+                wips = meta["warp_instructions_per_unit"] * r["n"] / (r["render_ms"] / 1e3)
+                peak_wi = 148 * 4 * mhz * 1e6
+                ref_ops = 4360.0 if kind == "c5" else 1470.0
+                rays = r["n"] * 64 * 64 / (r["render_ms"] / 1e3)
+                line["roofline_render_issue"] = {
+                    "bound": "issue", "achieved": wips, "peak": peak_wi, "unit": "warp-instr/s",
+                    "frac": wips / peak_wi,
+                    "reference_ops_per_ray": ref_ops,
+                    "reference_equiv_frac": rays * ref_ops / (148 * 128 * mhz * 1e6),
+                    "note": "warp-instructions per camera from the committed ncu capture (profiles/ncu_summary.json) "
+                            "x cameras / live kernel time; peak at the SM clock sampled during the timed region"}
         if rank == 0:
             line["roofline_dynamics"] = run_dynamics_roofline(pk)
             line["roofline_env_step"] = run_env_step_roofline(pk)

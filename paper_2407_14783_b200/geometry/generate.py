@@ -17,6 +17,7 @@ import math
 
 import numpy as np
 
+from .. import quatmath
 from .shapes import AABB, Box, Scene, SceneObject, Sphere, TriMesh
 
 WALL_THICKNESS = 0.2
@@ -29,15 +30,7 @@ OBSTACLE_ID0 = 7
 
 def _axis_angle_matrix(axis, angle) -> np.ndarray:
     """to_matrix(from_axis_angle(axis, angle)) (quatmath.py:75-113)."""
-    axis = np.asarray(axis, dtype=float)
-    axis = axis / np.linalg.norm(axis)
-    h = 0.5 * angle
-    w, x, y, z = np.concatenate([[np.cos(h)], np.sin(h) * axis])
-    return np.array([
-        [1.0 - 2.0 * (y * y + z * z), 2.0 * (x * y - w * z), 2.0 * (x * z + w * y)],
-        [2.0 * (x * y + w * z), 1.0 - 2.0 * (x * x + z * z), 2.0 * (y * z - w * x)],
-        [2.0 * (x * z - w * y), 2.0 * (y * z + w * x), 1.0 - 2.0 * (x * x + y * y)],
-    ])
+    return quatmath.to_matrix(quatmath.from_axis_angle(axis, angle))
 
 
 def room_shell(volume: AABB, thickness: float = WALL_THICKNESS, ceiling: bool = True):

@@ -14,6 +14,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _native as nat
+from . import quatmath
 
 FORWARD = np.array([[0.0, 0.0, 1.0], [-1.0, 0.0, 0.0], [0.0, -1.0, 0.0]])
 DOWNWARD = np.array([[0.0, -1.0, 0.0], [-1.0, 0.0, 0.0], [0.0, 0.0, -1.0]])
@@ -62,22 +63,8 @@ class CameraModel:
         return c
 
 
-def _rotate(q, v):
-    w = q[..., 0]
-    ux, uy, uz = q[..., 1], q[..., 2], q[..., 3]
-    vx, vy, vz = v[..., 0], v[..., 1], v[..., 2]
-    tx, ty, tz = uy * vz - uz * vy, uz * vx - ux * vz, ux * vy - uy * vx
-    sx, sy, sz = uy * tz - uz * ty, uz * tx - ux * tz, ux * ty - uy * tx
-    return np.stack([vx + 2.0 * (w * tx + sx), vy + 2.0 * (w * ty + sy), vz + 2.0 * (w * tz + sz)], axis=-1)
-
-
-def _matrix(q):
-    w, x, y, z = q[..., 0], q[..., 1], q[..., 2], q[..., 3]
-    return np.stack([
-        np.stack([1.0 - 2.0 * (y * y + z * z), 2.0 * (x * y - w * z), 2.0 * (x * z + w * y)], -1),
-        np.stack([2.0 * (x * y + w * z), 1.0 - 2.0 * (x * x + z * z), 2.0 * (y * z - w * x)], -1),
-        np.stack([2.0 * (x * z - w * y), 2.0 * (y * z + w * x), 1.0 - 2.0 * (x * x + y * y)], -1),
-    ], -2)
+_rotate = quatmath.rotate
+_matrix = quatmath.to_matrix
 
 
 def camera_pose_world(body_position, body_orientation, camera: CameraModel):

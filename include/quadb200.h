@@ -233,6 +233,16 @@ int qb_env_reset(const qb_params *p, const qb_task *task, const qb_scene *s, con
 int qb_env_step(const qb_params *p, int32_t cmd_kind, const qb_task *task, const qb_scene *s, const qb_env_buffers *b,
                 void *stream);
 
+/* The same step in two launches (base.py:156-210): phase 1 = auto-reset,
+ * controller, dynamics (writes state, step count, non-finite flag and the
+ * pre-step state to prev_state, which must be non-NULL); phase 2 = proximity,
+ * task success + reward, terminated/truncated on that state.  Phase 2 reads
+ * nothing the observation render writes and the render reads nothing phase 2
+ * writes, so a caller may run them on two streams after phase 1.  Results
+ * equal qb_env_step's.  Not for swarm tasks. */
+int qb_env_step_phase(const qb_params *p, int32_t cmd_kind, const qb_task *task, const qb_scene *s,
+                      const qb_env_buffers *b, int32_t phase, void *stream);
+
 /* Swarm views for the observation (base.py:245-277, 306-309): for every
  * agent i, the other agents j != i (ascending) as render spheres
  * (x, y, z, collision_radius) in dtype (n, n-1, 4) with ids DRONE_ID0 + j

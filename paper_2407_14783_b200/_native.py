@@ -191,6 +191,7 @@ SIGNATURES = {
     "qb_env_reset": ([_PP(QbParams), _PP(QbTask), _P, _PP(QbEnvBuffers), _U64, _P], ctypes.c_int),
     "qb_env_step": ([_PP(QbParams), _I32, _PP(QbTask), _P, _PP(QbEnvBuffers), _P], ctypes.c_int),
     "qb_env_refresh": ([_PP(QbTask), _P, _PP(QbEnvBuffers), _P], ctypes.c_int),
+    "qb_env_step_phase": ([_PP(QbParams), _I32, _PP(QbTask), _P, _PP(QbEnvBuffers), _I32, _P], ctypes.c_int),
     "qb_env_swarm_views": ([_PP(QbTask), _PP(QbEnvBuffers), _P, _P, _P, _P], ctypes.c_int),
     "qb_rng_seed": ([_U64, _I64, _P, _P], ctypes.c_int),
     "qb_rng_doubles": ([_I64, _P, _I32, _P, _P], ctypes.c_int),

@@ -356,8 +356,12 @@ __global__ void k_swarm_views(EnvArgs<R> A, typename storage_of<R>::type *sphere
         for (int c = 0; c < 13; ++c) obs[idx * 13 + c] = st[c * B.ld + j];
 }
 
-// SUB = 2: the default two substeps unrolled at compile time (FP32 batch path)
-template <class R, int KIND, bool WARP, int SUB>
+// SUB = 2: the default two substeps unrolled at compile time (FP32 batch path).
+// PHASE 0: the fused step.  PHASE 1: auto-reset + controller + dynamics only
+// (state, step count, non-finite flag and the pre-step state in prev_state);
+// PHASE 2: proximity, task and flags on that state -- launched on a second
+// stream, concurrently with the observation render, which reads only the state.
+template <class R, int KIND, bool WARP, int SUB, int PHASE = 0>
 __global__ void __launch_bounds__(128, QB_ENV_MINB) k_env_step(EnvArgs<R> A) {
     using S = typename storage_of<R>::type;
     bool lead;
@@ -365,6 +369,30 @@ __global__ void __launch_bounds__(128, QB_ENV_MINB) k_env_step(EnvArgs<R> A) {
     const qb_env_buffers &B = A.B;
     const qb_task &T = A.T;
     if (i >= B.n) return;
+    if (PHASE == 2) {
+        R x[17];
+        load_state(A, i, x);
+        const S *ps = static_cast<const S *>(B.prev_state);
+        const double pp[3] = {(double)ps[i], (double)ps[B.ld + i], (double)ps[2 * B.ld + i]};
+        const bool ok = !B.nonfinite[i];
+        const int steps = B.step_count[i];
+        Proximity pr = proximity<R, WARP>(A, B.agent_scene[i], x);
+        double p[3] = {r_dbl(x[0]), r_dbl(x[1]), r_dbl(x[2])};
+        double v[3] = {r_dbl(x[3]), r_dbl(x[4]), r_dbl(x[5])};
+        bool success;
+        double reward;
+        task_eval(T, pp, p, v, pr.dist, pr.collision, success, reward);
+        const bool terminated = success || pr.collision || pr.oob || !ok;
+        const bool truncated = !terminated && steps >= T.episode_max_steps;
+        if (!lead) return;
+        write_post(A, i, pr);
+        B.success[i] = success;
+        B.reward[i] = (float)reward;
+        B.terminated[i] = terminated;
+        B.truncated[i] = truncated;
+        B.needs_respawn[i] = terminated || truncated;
+        return;
+    }
     // every per-env input is requested before the first store (one memory
     // round trip instead of four dependent ones at 20 warps/SM); a respawn
     // rewrites step count and scene, re-read on that (rare) path
@@ -392,6 +420,13 @@ __global__ void __launch_bounds__(128, QB_ENV_MINB) k_env_step(EnvArgs<R> A) {
     if (!ok) {
 #pragma unroll
         for (int k = 0; k < 17; ++k) x[k] = prev[k];
+    }
+    if (PHASE == 1) {
+        if (!lead) return;
+        store_planes(B.state, B.ld, i, x);
+        B.step_count[i] = steps;
+        B.nonfinite[i] = !ok;
+        return;
     }
     Proximity pr = proximity<R, WARP>(A, scene, x);
 
@@ -429,15 +464,15 @@ __global__ void k_rng_doubles(long long n, uint64_t *rng, int k, double *out) {
     pcg_store(rng + 4 * i, r);
 }
 
-template <class R, int K>
+template <class R, int K, int PH = 0>
 void launch_env_step(const EnvArgs<R> &A, bool warp, bool sub2, dim3 g, int BS, cudaStream_t st) {
     if constexpr (std::is_same<R, float>::value) {
         if (warp)
-            sub2 ? k_env_step<R, K, true, 2><<<g, BS, 0, st>>>(A) : k_env_step<R, K, true, 0><<<g, BS, 0, st>>>(A);
+            sub2 ? k_env_step<R, K, true, 2, PH><<<g, BS, 0, st>>>(A) : k_env_step<R, K, true, 0, PH><<<g, BS, 0, st>>>(A);
         else
-            sub2 ? k_env_step<R, K, false, 2><<<g, BS, 0, st>>>(A) : k_env_step<R, K, false, 0><<<g, BS, 0, st>>>(A);
+            sub2 ? k_env_step<R, K, false, 2, PH><<<g, BS, 0, st>>>(A) : k_env_step<R, K, false, 0, PH><<<g, BS, 0, st>>>(A);
     } else {
-        warp ? k_env_step<R, K, true, 0><<<g, BS, 0, st>>>(A) : k_env_step<R, K, false, 0><<<g, BS, 0, st>>>(A);
+        warp ? k_env_step<R, K, true, 0, PH><<<g, BS, 0, st>>>(A) : k_env_step<R, K, false, 0, PH><<<g, BS, 0, st>>>(A);
     }
 }
 
@@ -471,9 +506,16 @@ int dispatch_env(int mode, const qb_params *p, int kind, const qb_task *task, co
         if (swarm) k_swarm_post<R><<<gp, BS, 0, st>>>(A, 0);
         return qb::check_launch("env_reset");
     }
+    if (mode == 4) {  // phase 2 of a split step (no command kind involved)
+        if (warp)
+            k_env_step<R, QB_CMD_ROTOR, true, 0, 2><<<g, BS, 0, st>>>(A);
+        else
+            k_env_step<R, QB_CMD_ROTOR, false, 0, 2><<<g, BS, 0, st>>>(A);
+        return qb::check_launch("env_step_post");
+    }
     if (swarm && task->auto_reset) k_swarm_spawn<R><<<1, 32, 0, st>>>(A, 0);
     const bool sub2 = std::is_same<R, float>::value && A.C.substeps == 2;
-#define QB_ENV(K) launch_env_step<R, K>(A, warp, sub2, g, BS, st)
+#define QB_ENV(K) (mode == 3 ? launch_env_step<R, K, 1>(A, warp, sub2, g, BS, st) : launch_env_step<R, K, 0>(A, warp, sub2, g, BS, st))
     switch (kind) {
         case QB_CMD_SRT: QB_ENV(QB_CMD_SRT); break;
         case QB_CMD_CTBR: QB_ENV(QB_CMD_CTBR); break;
@@ -503,7 +545,7 @@ template <class R> int dispatch_views(const qb_task *task, const qb_env_buffers 
 }  // namespace
 
 namespace qb {
-// mode 0 reset, 1 step, 2 refresh
+// mode 0 reset, 1 step, 2 refresh, 3 / 4 the two phases of a split step
 int launch_swarm_views(const qb_task *task, const qb_env_buffers *b, void *spheres, int32_t *ids, void *obs,
                        cudaStream_t st) {
     if (b->n == 0) return QB_OK;

@@ -26,6 +26,8 @@ from __future__ import annotations
 from collections.abc import Sequence
 from dataclasses import dataclass
 
+import os
+
 import numpy as np
 
 from .. import _native as nat
@@ -172,6 +174,14 @@ class QuadEnvBase:
         self._task = self._pack_task()
         self._reset_done = False
         self._custom_hooks = self._has_custom_hooks()
+        # small batches with a camera: step in two launches so the proximity /
+        # reward phase runs on a side stream under the observation render
+        # (qb_env_step_phase; both read only the post-dynamics state)
+        self.split_step = (not self.swarm and self._prev is not None and any(c is not None for _, c in self.sensor_cameras)
+                           and self.num_agents * 32 <= torch.cuda.get_device_properties(self.device).multi_processor_count * 2048)
+        if os.environ.get("QB_SPLIT_STEP") == "0":  # A/B switch
+            self.split_step = False
+        self._post_stream = None
 
     # ------------------------------------------------------------------ setup
     def _has_custom_hooks(self) -> bool:
@@ -368,10 +378,16 @@ class QuadEnvBase:
         a = self._stage_action(action)
         self._bufs.action = a.data_ptr()
         with torch.cuda.device(self.device):
-            nat.check(nat.lib().qb_env_step(self._P, self._kind, self._task, self.dev_scenes.handle, self._bufs,
-                                            nat.stream_of()), "qb_env_step")
-            self._record_async_errors()
-            obs = self.get_observation()
+            if self.split_step:
+                join = self._launch_split_dynamics()
+                self._record_async_errors()
+                obs = self.get_observation()
+                join()
+            else:
+                nat.check(nat.lib().qb_env_step(self._P, self._kind, self._task, self.dev_scenes.handle, self._bufs,
+                                                nat.stream_of()), "qb_env_step")
+                self._record_async_errors()
+                obs = self.get_observation()
         if self._custom_hooks:
             success = torch.as_tensor(self.get_success(), device=self.device).bool()
             reward = torch.as_tensor(self.get_reward(), device=self.device)
@@ -491,7 +507,28 @@ class QuadEnvBase:
         self._graph_keepalive = seq
         return g.replay
 
+    def _launch_split_dynamics(self):
+        """Phase 1 on the current stream, phase 2 forked onto the post stream;
+        returns the join to call after the observation launches."""
+        import torch
+
+        lib, main = nat.lib(), torch.cuda.current_stream()
+        if self._post_stream is None:
+            self._post_stream = torch.cuda.Stream()
+        nat.check(lib.qb_env_step_phase(self._P, self._kind, self._task, self.dev_scenes.handle, self._bufs, 1,
+                                        nat.stream_of()), "qb_env_step_phase")
+        self._post_stream.wait_stream(main)
+        with torch.cuda.stream(self._post_stream):
+            nat.check(lib.qb_env_step_phase(self._P, self._kind, self._task, self.dev_scenes.handle, self._bufs, 2,
+                                            nat.stream_of()), "qb_env_step_phase")
+        return lambda: main.wait_stream(self._post_stream)
+
     def _launch_step(self):
+        if self.split_step:
+            join = self._launch_split_dynamics()
+            self._render_and_observe()
+            join()
+            return
         nat.check(nat.lib().qb_env_step(self._P, self._kind, self._task, self.dev_scenes.handle, self._bufs,
                                         nat.stream_of()), "qb_env_step")
         self._render_and_observe()

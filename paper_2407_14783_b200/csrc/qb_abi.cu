@@ -531,10 +531,10 @@ int qb_env_step(const qb_params *p, int32_t cmd_kind, const qb_task *task, const
 int qb_env_step_phase(const qb_params *p, int32_t cmd_kind, const qb_task *task, const qb_scene *s,
                       const qb_env_buffers *b, int32_t phase, void *stream) {
     QB_REQUIRE(p, "env: NULL params");
+    QB_REQUIRE(phase == 1 || phase == 2, "env: phase must be 1 or 2");
+    QB_REQUIRE(b && b->prev_state, "env: a split step needs prev_state");
     int rc = check_env(task, s, b);
     if (rc) return rc;
-    QB_REQUIRE(phase == 1 || phase == 2, "env: phase must be 1 or 2");
-    QB_REQUIRE(b->prev_state, "env: a split step needs prev_state");
     QB_REQUIRE(!task->swarm, "env: swarm steps are not split");
     if (phase == 1) QB_REQUIRE(b->action, "env: NULL action");
     return qb::launch_env(phase == 1 ? 3 : 4, p, cmd_kind, task, s, b, 0, qb::as_stream(stream));

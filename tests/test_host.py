@@ -229,6 +229,9 @@ def test_abi_argument_validation_without_gpu():
     assert lib.qb_control_stage(P, 7, nat.QB_F32, 1, 1, None, ctypes.addressof(buf), ctypes.addressof(buf), None, None) != 0
     assert lib.qb_control_stage(P, 1, nat.QB_F32, 1, 1, None, ctypes.addressof(buf), ctypes.addressof(buf), None, None) != 0
     assert b"state planes" in lib.qb_last_error()
+    # split env step: phase 1 or 2 only, and the pre-step state buffer is required
+    assert lib.qb_env_step_phase(P, 0, None, None, b, 3, None) != 0 and b"phase" in lib.qb_last_error()
+    assert lib.qb_env_step_phase(P, 0, None, None, b, 1, None) != 0 and b"prev_state" in lib.qb_last_error()
     # empty primitive set
     cnt = ctypes.c_int64(0)
     assert lib.qb_bvh_build(0, None, None, ctypes.byref(cnt), None, None, None, None, None) != 0

@@ -11,6 +11,12 @@ stream, with no host synchronisation:
   2. qb_render     (K2, once per distinct camera: depth + segmentation from the
                     same rays, landing pad centroid in the epilogue)
 
+Small camera batches (<= 9472 agents, the warp-per-env range) split step 1
+into qb_env_step_phase 1 (auto-reset, controller, dynamics) and phase 2
+(proximity, reward, flags) on a side stream that runs under the render and
+joins before step() returns (`split_step`; results bit-equal to the fused
+launch).
+
 Observations and flags are device tensors.  `observations[i]` / `info[i]`
 materialise the reference's per-agent dicts on demand (a host copy), so code
 written against the reference keeps working; batched consumers index by key

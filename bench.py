@@ -280,7 +280,8 @@ def run_env(args, rank, world, kind):
     torch.cuda.synchronize()
     clocks = clk.stop()
     ms = max_over_ranks(t0.elapsed_time(t1), world)
-    launches = K * (1 + len(env._cams) + (1 if env._obs_sensors else 0))
+    k3 = 2 if (small and env.split_step) else 1  # the graph path launches the split step's two phases
+    launches = K * (k3 + len(env._cams) + (1 if env._obs_sensors else 0))
     out = dict(env=env, cfg=cfg, n=n, total=total, ms=ms, clocks=clocks, launches=launches, graph=small)
     if not small:
         out["step_ms"] = float(np.mean([e[0].elapsed_time(e[1]) for e in ev]))

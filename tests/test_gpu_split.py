@@ -18,10 +18,18 @@ torch = pytest.importorskip("torch")
 def _cfgs():
     nav = dataclasses.replace(navigation_config(0, 100, with_segmentation=True), episode_max_steps=40)
     mesh = dataclasses.replace(nav, scenes=tuple(dataclasses.replace(sc, kind="cluttered_mesh") for sc in nav.scenes))
-    return {"nav": nav, "mesh": mesh, "landing": dataclasses.replace(landing_config(64), episode_max_steps=30)}
+    from paper_2407_14783_b200.env import SensorSpec
+    from paper_2407_14783_b200.sensing import NoiseSpec
+
+    noisy = dataclasses.replace(nav, sensors=(
+        SensorSpec(kind="depth", name="depth", noise=(NoiseSpec("normal", sigma=0.02),)),
+        SensorSpec(kind="segmentation", name="segmentation", noise=(NoiseSpec("saltpepper", p=0.02),)),
+        SensorSpec(kind="imu", name="imu", noise=(NoiseSpec("normal", sigma=0.05),))))
+    return {"nav": nav, "mesh": mesh, "landing": dataclasses.replace(landing_config(64), episode_max_steps=30),
+            "noisy": noisy}
 
 
-@pytest.mark.parametrize("name", ["nav", "mesh", "landing"])
+@pytest.mark.parametrize("name", ["nav", "mesh", "landing", "noisy"])
 def test_split_step_equals_fused(name):
     cfg = _cfgs()[name]
     a, b = make_env(cfg), make_env(cfg)
@@ -35,7 +43,7 @@ def test_split_step_equals_fused(name):
         yaw = torch.randn(n, device="cuda", generator=g)
         ra, rb = a.step(LV(v, yaw)), b.step(LV(v, yaw))
         torch.cuda.synchronize()
-        for k in ("state", "depth", "segmentation", "target"):
+        for k in ("state", "depth", "segmentation", "target", "imu"):
             if k in rb.observations:
                 assert torch.equal(ra.observations[k], rb.observations[k]), (t, k)
         assert torch.equal(a._planes, b._planes), t

@@ -167,6 +167,22 @@ def command_to_rotor_speeds(P: QbParams, kind: str, states, cmd) -> np.ndarray:
     return out
 
 
+def command_mixer_info(P: QbParams, kind: str, states, cmd):
+    """command_to_rotor_speeds plus, per agent, the mixer's torque scale and
+    smallest clipped rotor thrust (test diagnostics).  Returns (speeds (N,4),
+    scale (N,), min_thrust (N,))."""
+    states = _f64(states)
+    n = states.shape[0]
+    cmd = _f64(cmd, (n, 4))
+    cy = np.ascontiguousarray(np.cos(cmd[:, 3]))
+    sy = np.ascontiguousarray(np.sin(cmd[:, 3]))
+    out = np.empty((n, 4))
+    info = np.empty((n, 2))
+    lib().or_command_mixer_info(ctypes.byref(P), CMD_KINDS[kind], ctypes.c_int64(n), _ptr(states), _ptr(cmd), _ptr(cy),
+                                _ptr(sy), _ptr(out), _ptr(info))
+    return out, info[:, 0].copy(), info[:, 1].copy()
+
+
 def dynamics_step(P: QbParams, states, rotor_cmds):
     """dynamics.py:231-253. Returns (next (N,17), nonfinite (N,) bool)."""
     x = _f64(states).copy()

@@ -14,7 +14,7 @@ import os
 from .errors import NativeError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libquadb200.so")
+LIB_PATH = os.environ.get("QB_LIB_PATH") or os.path.join(_HERE, "libquadb200.so")  # override: A/B builds in scripts/
 
 QB_F32, QB_F64 = 0, 1
 CMD = {"srt": 0, "ctbr": 1, "ps": 2, "lv": 3, "rotor": 4}

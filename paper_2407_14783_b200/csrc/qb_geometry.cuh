@@ -359,10 +359,10 @@ template <class R> QB_D R ray_triangle_ref(const R *d, R ox, R oy, R oz, R dx, R
 }
 
 // ---- FP32 production versions on the packed float records ---------------
-// float record layouts (qb_bvh.cpp pack_prims):
+// float record layouts (qb_scene_pack.cuh pack_prim):
 //   sphere   : [cx cy cz r] [r*r 0 0 0] ...
 //   box      : [cx cy cz hx] [hy hz r00 r01] [r02 r10 r11 r12] [r20 r21 r22 0]
-//   triangle : [ax ay az e1x] [e1y e1z e2x e2y] [e2z 0 0 0]
+//   triangle : [ax ay az bx] [by bz cx cy] [cz 0 0 0]  (vertices)
 
 // 1/x from MUFU.RCP (~1 ulp): ray-setup reciprocals for slab tests against
 // outward-rounded boxes, no IEEE-division slow path (no call, no stack frame)
@@ -433,32 +433,92 @@ QB_D float ray_box_f(const float4 *p, float ox, float oy, float oz, float dx, fl
     return ray_box_v(__ldg(p), __ldg(p + 1), __ldg(p + 2), __ldg(p + 3), ox, oy, oz, dx, dy, dz, tmin, tmax);
 }
 
-// triangle record (a, e1, e2) passed by value: callers issue the record loads
-// together with the primitive's metadata load
-QB_D float ray_triangle_v(float4 a, float4 b, float4 c, float ox, float oy, float oz, float dx, float dy, float dz,
-                          float tmin, float tmax) {
-    float ax = a.x, ay = a.y, az = a.z;
-    float e1x = a.w, e1y = b.x, e1z = b.y, e2x = b.z, e2y = b.w, e2z = c.x;
-    float px = dy * e2z - dz * e2y, py = dz * e2x - dx * e2z, pz = dx * e2y - dy * e2x;
-    float det = e1x * px + e1y * py + e1z * pz;
+// Watertight ray-triangle test (Woop, Benthin & Wald, JCGT 2013), two-sided
+// like the reference's Moeller-Trumbore (kernels.py:249-275).  The record
+// holds the three vertices as floats rounded from the reference's doubles,
+// so triangles sharing an edge hold bit-identical copies of its end points.
+// Each vertex is moved into a per-ray sheared frame (the ray becomes the KZ
+// axis) by a deterministic function of that vertex alone, and the 2D edge
+// functions are products rounded separately and then subtracted (no FMA
+// contraction): swapping an edge's end points negates its value exactly.  A
+// ray crossing a shared edge therefore lands inside exactly one of the two
+// triangles (both when it hits the edge exactly) -- no cracks.  Moeller-
+// Trumbore on float (a, e1, e2) records is not watertight: the two triangles
+// round the shared edge differently and a ray can pass between them (found
+// by the C5 parity test on the indoor hall: 1 pixel in 2.6e5 read a surface
+// 0.6 m behind).
+//
+// KZ: any axis along which the ray direction is not small (callers pick the
+// dominant axis of the ray or of its tile); kx, ky the other two, cyclic.
+struct Shear {
+    float sx, sy, sz;
+};
+
+// per-ray shear constants: sz = 1 / d[kz] (any deterministic per-ray value
+// keeps the test watertight), sx = d[kx] sz, sy = d[ky] sz
+QB_D Shear ray_shear(int kz, float dx, float dy, float dz) {
+    const float dk = kz == 0 ? dx : (kz == 1 ? dy : dz);
+    const float ax = kz == 0 ? dy : (kz == 1 ? dz : dx), ay = kz == 0 ? dz : (kz == 1 ? dx : dy);
+    const float sz = rcp_approx(dk);
+    return {ax * sz, ay * sz, sz};
+}
+
+template <int KZ>
+QB_D float ray_triangle_wt(float4 r0, float4 r1, float4 r2, float ox, float oy, float oz, Shear sh, float tmin,
+                           float tmax) {
+    constexpr int KX = (KZ + 1) % 3, KY = (KZ + 2) % 3;
+    const float sx = sh.sx, sy = sh.sy, sz = sh.sz;
+    const float A[3] = {r0.x - ox, r0.y - oy, r0.z - oz};
+    const float B[3] = {r0.w - ox, r1.x - oy, r1.y - oz};
+    const float C[3] = {r1.z - ox, r1.w - oy, r2.x - oz};
+    const float ax = fmaf(-sx, A[KZ], A[KX]), ay = fmaf(-sy, A[KZ], A[KY]);
+    const float bx = fmaf(-sx, B[KZ], B[KX]), by = fmaf(-sy, B[KZ], B[KY]);
+    const float cx = fmaf(-sx, C[KZ], C[KX]), cy = fmaf(-sy, C[KZ], C[KY]);
+    const float U = __fsub_rn(__fmul_rn(cx, by), __fmul_rn(cy, bx));
+    const float V = __fsub_rn(__fmul_rn(ax, cy), __fmul_rn(ay, cx));
+    const float W = __fsub_rn(__fmul_rn(bx, ay), __fmul_rn(by, ax));
+    if ((U < 0.0f || V < 0.0f || W < 0.0f) && (U > 0.0f || V > 0.0f || W > 0.0f)) return -1.0f;
+    const float det = U + V + W;
     if (det == 0.0f) return -1.0f;
-    // Moeller-Trumbore with the barycentric tests on the numerators scaled by
-    // sign(det) (u = U/det in [0,1] <=> U*sgn in [0,|det|]): the division is
-    // paid only by the rays that pass both edge tests
-    const float adet = fabsf(det);
-    float tx = ox - ax, ty = oy - ay, tz = oz - az;
-    float U = copysignf(1.0f, det) * (tx * px + ty * py + tz * pz);
-    if (U < 0.0f || U > adet) return -1.0f;
-    float qx = ty * e1z - tz * e1y, qy = tz * e1x - tx * e1z, qz = tx * e1y - ty * e1x;
-    float V = copysignf(1.0f, det) * (dx * qx + dy * qy + dz * qz);
-    if (V < 0.0f || U + V > adet) return -1.0f;
-    float t = __fdividef(e2x * qx + e2y * qy + e2z * qz, det);
+    // hit distance in ray-parameter units: z' = sz * P[KZ]
+    const float T = fmaf(U, A[KZ], fmaf(V, B[KZ], W * C[KZ]));
+    const float t = __fdividef(T * sz, det);
     if (t > tmin && t <= tmax) return t;
     return -1.0f;
 }
 
-QB_D float ray_triangle_f(const float4 *p, float ox, float oy, float oz, float dx, float dy, float dz, float tmin, float tmax) {
-    return ray_triangle_v(__ldg(p), __ldg(p + 1), __ldg(p + 2), ox, oy, oz, dx, dy, dz, tmin, tmax);
+// dominant axis of a direction (ties to the lower axis)
+QB_D int dominant_axis(float dx, float dy, float dz) {
+    const float x = fabsf(dx), y = fabsf(dy), z = fabsf(dz);
+    return (x >= y && x >= z) ? 0 : (y >= z ? 1 : 2);
+}
+
+// triangle record passed by value (callers issue the record loads together
+// with the primitive's metadata load); kz: the ray's (or its tile's, warp-
+// uniform) dominant axis
+QB_D float ray_triangle_v(int kz, float4 a, float4 b, float4 c, float ox, float oy, float oz, Shear sh, float tmin,
+                          float tmax) {
+    if (kz == 2) return ray_triangle_wt<2>(a, b, c, ox, oy, oz, sh, tmin, tmax);
+    if (kz == 1) return ray_triangle_wt<1>(a, b, c, ox, oy, oz, sh, tmin, tmax);
+    return ray_triangle_wt<0>(a, b, c, ox, oy, oz, sh, tmin, tmax);
+}
+
+QB_D float ray_triangle_v(int kz, float4 a, float4 b, float4 c, float ox, float oy, float oz, float dx, float dy, float dz,
+                          float tmin, float tmax) {
+    return ray_triangle_v(kz, a, b, c, ox, oy, oz, ray_shear(kz, dx, dy, dz), tmin, tmax);
+}
+
+QB_D float ray_triangle_f(int kz, const float4 *p, float ox, float oy, float oz, float dx, float dy, float dz, float tmin,
+                          float tmax) {
+    return ray_triangle_v(kz, __ldg(p), __ldg(p + 1), __ldg(p + 2), ox, oy, oz, dx, dy, dz, tmin, tmax);
+}
+
+// out-of-line copy for kernels where triangles are the rare case (the
+// culling renderer's analytic rooms): keeps the three shear variants out of
+// the caller's register allocation
+static __device__ __noinline__ float ray_triangle_call(int kz, const float4 *p, float ox, float oy, float oz, float dx,
+                                                       float dy, float dz, float tmin, float tmax) {
+    return ray_triangle_f(kz, p, ox, oy, oz, dx, dy, dz, tmin, tmax);
 }
 
 // FP32 slab entry (kernels.py:288-319 semantics: entry clamped at 0, INF = miss)
@@ -568,6 +628,7 @@ QB_D double raycast_x(const DevScene &S, int scene, double ox_, double oy_, doub
 QB_D float raycast_f(const DevScene &S, int scene, float ox, float oy, float oz, float dx, float dy, float dz, float tmin,
                      float tmax, int &id_out) {
     float ix = 1.0f / dx, iy = 1.0f / dy, iz = 1.0f / dz;
+    const int kz = dominant_axis(dx, dy, dz);
     int stack[64];
     int top = 0;
     stack[top++] = S.root[scene];
@@ -585,7 +646,7 @@ QB_D float raycast_f(const DevScene &S, int scene, float ox, float oy, float oz,
                 const float4 *pr = S.primf + 4 * p;
                 float t = m.x == QB_SPHERE ? ray_sphere_f(pr, ox, oy, oz, dx, dy, dz, tmin, best_t)
                           : m.x == QB_BOX  ? ray_box_f(pr, ox, oy, oz, dx, dy, dz, tmin, best_t)
-                                           : ray_triangle_f(pr, ox, oy, oz, dx, dy, dz, tmin, best_t);
+                                           : ray_triangle_f(kz, pr, ox, oy, oz, dx, dy, dz, tmin, best_t);
                 if (t > 0.0f && (t < best_t || !hit || (t == best_t && m.y < best_id))) {
                     best_t = t;
                     best_id = m.y;

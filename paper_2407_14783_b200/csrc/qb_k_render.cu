@@ -119,6 +119,22 @@ QB_D void world_plane(const float *Rs, const float *o, float a, float b, float c
 //     bits; entries are >= 0); a pop is skipped unless some lane's hit still
 //     lies beyond that entry.  Culling is conservative and the result (nearest
 //     t, ties to the lowest id) is traversal-order independent.
+#ifdef QB_RF_DEBUG
+// debug trace of one (camera, pixel) through k_render_f (scripts/ builds only)
+__device__ int g_dbg_target[3] = {-1, -1, -1};
+__device__ int g_dbg_n = 0;
+__device__ float4 g_dbg_log[8192];
+#define QB_DBG(on, kind, a, b, c)                                                       \
+    do {                                                                                \
+        if (on) {                                                                       \
+            int k_ = atomicAdd(&g_dbg_n, 1);                                            \
+            if (k_ < 8192) g_dbg_log[k_] = make_float4((float)(kind), (float)(a), (float)(b), (float)(c)); \
+        }                                                                               \
+    } while (0)
+#else
+#define QB_DBG(on, kind, a, b, c) do {} while (0)
+#endif
+
 template <bool FROM_STATE>
 __global__ void __launch_bounds__(QB_RF_BLOCK, QB_RF_MINB) k_render_f(DevScene S, CamF cam, long long n, long long ld, const float *state,
                                                      const float *origins, const float *rotations, const int32_t *env_scene,
@@ -223,6 +239,11 @@ __global__ void __launch_bounds__(QB_RF_BLOCK, QB_RF_MINB) k_render_f(DevScene S
             const int j = j0 + (lane & 7);
             const int i = i0 + (lane >> 3);
             const bool valid = (j < W) && (i < H);
+#ifdef QB_RF_DEBUG
+            const bool dbg = c == g_dbg_target[0] && i == g_dbg_target[1] && j == g_dbg_target[2];
+#else
+            constexpr bool dbg = false;
+#endif
             const float y = ((i + 0.5f) * sy - 1.0f) * cam.tv;
             const float x = ((j + 0.5f) * sx - 1.0f) * cam.th;
             const float n2 = x * x + y * y + 1.0f;
@@ -237,6 +258,10 @@ __global__ void __launch_bounds__(QB_RF_BLOCK, QB_RF_MINB) k_render_f(DevScene S
             }
             const float ix = rcp_approx(dx), iy = rcp_approx(dy), iz = rcp_approx(dz);
             const float oix = o[0] * ix, oiy = o[1] * iy, oiz = o[2] * iz;
+            // the triangle test's shear axis: the dominant axis of a ray near the
+            // tile centre, warp-uniform (a tile spans ~11 deg, so |d[kz]| >= 0.38)
+            const int kz = __shfl_sync(FULL, dominant_axis(dx, dy, dz), 12);
+
             // lanes outside the image carry best = -1: they never want a box
             float best = valid ? tmax : -1.0f;
             int bid = -1;
@@ -268,10 +293,17 @@ __global__ void __launch_bounds__(QB_RF_BLOCK, QB_RF_MINB) k_render_f(DevScene S
                 // survivors' entry distances (all rays), kept one per lane
                 unsigned my_e = INF_BITS;
                 int my_rec = 0, ns = 0;
+#ifdef QB_RF_DEBUG
+                for (int q = 0; q < nf; ++q) {
+                    const int inq = __shfl_sync(FULL, (int)in, q);
+                    QB_DBG(dbg, 1, fr[q], inq, nf);
+                }
+#endif
                 for (unsigned m = __ballot_sync(FULL, in); m; m &= m - 1) {
                     const int node = fr[__ffs(m) - 1];
                     const float4 lo = __ldg(S.nodef + 2 * node), hi = __ldg(S.nodef + 2 * node + 1);
                     const float e = slab_enter_fma(lo, hi, oix, oiy, oiz, ix, iy, iz, best);
+                    QB_DBG(dbg, 2, node, e, best);
                     const unsigned em = __reduce_min_sync(FULL, e <= best ? __float_as_uint(e) : INF_BITS);
                     if (em != INF_BITS) {
                         if (lane == ns) {
@@ -300,6 +332,7 @@ __global__ void __launch_bounds__(QB_RF_BLOCK, QB_RF_MINB) k_render_f(DevScene S
                 if (ca < 0) {
                     while (sp > 0) {
                         const int2 e = stk[--sp];
+                        QB_DBG(dbg, 3, e.x >> 3, __uint_as_float((unsigned)e.y), best);
                         if (__any_sync(FULL, __uint_as_float((unsigned)e.y) <= best)) {
                             ca = e.x >> 3;
                             cb = (e.x & 7) - 2;
@@ -323,11 +356,12 @@ __global__ void __launch_bounds__(QB_RF_BLOCK, QB_RF_MINB) k_render_f(DevScene S
                         const int2 m = __ldg(S.meta + p);
                         float t;
                         if (m.x == QB_TRIANGLE)
-                            t = ray_triangle_v(ra, rb, rc, o[0], o[1], o[2], dx, dy, dz, tmin, best);
+                            t = ray_triangle_v(kz, ra, rb, rc, o[0], o[1], o[2], dx, dy, dz, tmin, best);
                         else if (m.x == QB_BOX)
                             t = ray_box_v(ra, rb, rc, __ldg(pr + 3), o[0], o[1], o[2], dx, dy, dz, tmin, best);
                         else
                             t = ray_sphere_v(ra, rb.x, o[0], o[1], o[2], dx, dy, dz, tmin, best);
+                        QB_DBG(dbg, 5, p, t, best);
                         if (t > 0.0f && (t < best || !hit || (t == best && m.y < bid))) {
                             best = t;
                             bid = m.y;
@@ -341,6 +375,7 @@ __global__ void __launch_bounds__(QB_RF_BLOCK, QB_RF_MINB) k_render_f(DevScene S
                 const float4 rlo = __ldg(S.nodef + 2 * ca + 2), rhi = __ldg(S.nodef + 2 * ca + 3);
                 const float el = slab_enter_fma(llo, lhi, oix, oiy, oiz, ix, iy, iz, best);
                 const float er = slab_enter_fma(rlo, rhi, oix, oiy, oiz, ix, iy, iz, best);
+                QB_DBG(dbg, 4, ca, el, er);
                 const bool wl = el <= best, wr = er <= best;
                 const bool hl = __any_sync(FULL, wl);
                 const bool hr = __any_sync(FULL, wr);
@@ -351,7 +386,13 @@ __global__ void __launch_bounds__(QB_RF_BLOCK, QB_RF_MINB) k_render_f(DevScene S
                     const float ef = left_first ? er : el;
                     const bool wf = left_first ? wr : wl;
                     const unsigned em = __reduce_min_sync(FULL, wf ? __float_as_uint(ef) : INF_BITS);
-                    if (lane == 0) stk[sp] = make_int2(__float_as_int(flo.w) * 8 + (__float_as_int(fhi.w) + 2), (int)em);
+                    // every lane stores the (warp-uniform) entry: each lane's later pop
+                    // then reads its own store.  A lane-0-only store is a cross-lane
+                    // shared-memory dependency with no __syncwarp before the pop: the
+                    // compiler may sink the store below the other lanes' loads, which then
+                    // pop a stale entry and skip a subtree (seen as one C5 pixel reading a
+                    // surface 0.6 m behind the one it should hit)
+                    stk[sp] = make_int2(__float_as_int(flo.w) * 8 + (__float_as_int(fhi.w) + 2), (int)em);
                     ++sp;
                     ca = __float_as_int(nlo.w);
                     cb = __float_as_int(nhi.w);
@@ -706,6 +747,8 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, QB_CULL_MINB)
                 best[u] = tmx[u];
                 bid[u] = 0x7fffffff;
             }
+            // triangle shear axis, warp-uniform (see k_render_f)
+            const int kz = __shfl_sync(FULL, dominant_axis(dx[0], dy[0], dz[0]), 12);
             for (int b = 0; b < ncand; b += 32) {
                 const int k = b + lane;
                 bool kp = false;
@@ -772,7 +815,7 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, QB_CULL_MINB)
                         } else {
 #pragma unroll
                             for (int u = 0; u < 2; ++u)
-                                t[u] = ray_triangle_f(S.primf + 4 * cand[k2], o[0], o[1], o[2], dx[u], dy[u], dz[u], tmin,
+                                t[u] = ray_triangle_call(kz, S.primf + 4 * cand[k2], o[0], o[1], o[2], dx[u], dy[u], dz[u], tmin,
                                                       best[u]);
                         }
                     } else {
@@ -784,7 +827,7 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, QB_CULL_MINB)
                         for (int u = 0; u < 2; ++u)
                             t[u] = mt.x == QB_SPHERE ? ray_sphere_f(pr, o[0], o[1], o[2], dx[u], dy[u], dz[u], tmin, best[u])
                                    : mt.x == QB_BOX  ? ray_box_f(pr, o[0], o[1], o[2], dx[u], dy[u], dz[u], tmin, best[u])
-                                                     : ray_triangle_f(pr, o[0], o[1], o[2], dx[u], dy[u], dz[u], tmin, best[u]);
+                                                     : ray_triangle_call(kz, pr, o[0], o[1], o[2], dx[u], dy[u], dz[u], tmin, best[u]);
                     }
 #pragma unroll
                     for (int u = 0; u < 2; ++u)
@@ -1091,3 +1134,17 @@ int launch_raycast(const qb_scene *s, int dtype, const int32_t *env_scene, long 
 }
 
 }  // namespace qb
+
+#ifdef QB_RF_DEBUG
+extern "C" int qb_dbg_set(int cam, int i, int j) {
+    int t[3] = {cam, i, j}, z = 0;
+    cudaMemcpyToSymbol(g_dbg_target, t, sizeof(t));
+    cudaMemcpyToSymbol(g_dbg_n, &z, sizeof(z));
+    return 0;
+}
+extern "C" int qb_dbg_get(float4 *out, int *n) {
+    cudaMemcpyFromSymbol(n, g_dbg_n, sizeof(int));
+    cudaMemcpyFromSymbol(out, g_dbg_log, sizeof(float4) * 8192);
+    return 0;
+}
+#endif

@@ -99,12 +99,10 @@ QB_HD void pack_prim(int type, const double *d, float4 *o) {
         bool ident = true;
         for (int k = 0; k < 9; ++k) ident = ident && d[6 + k] == (k % 4 == 0 ? 1.0 : 0.0) && !signbit(d[6 + k]);
         o[3] = make_float4((float)d[12], (float)d[13], (float)d[14], ident ? 1.f : 0.f);
-    } else {
-        const double e1[3] = {sub(d[3], d[0]), sub(d[4], d[1]), sub(d[5], d[2])};
-        const double e2[3] = {sub(d[6], d[0]), sub(d[7], d[1]), sub(d[8], d[2])};
-        o[0] = make_float4((float)d[0], (float)d[1], (float)d[2], (float)e1[0]);
-        o[1] = make_float4((float)e1[1], (float)e1[2], (float)e2[0], (float)e2[1]);
-        o[2] = make_float4((float)e2[2], 0.f, 0.f, 0.f);
+    } else {  // the vertices themselves: shared edges stay bit-identical (watertight test)
+        o[0] = make_float4((float)d[0], (float)d[1], (float)d[2], (float)d[3]);
+        o[1] = make_float4((float)d[4], (float)d[5], (float)d[6], (float)d[7]);
+        o[2] = make_float4((float)d[8], 0.f, 0.f, 0.f);
     }
 }
 

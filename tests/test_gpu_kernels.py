@@ -68,27 +68,81 @@ def test_k1_fp32_one_step(gdyn, kind):
     assert err.max() < 1e-5, summarize(err)
 
 
-@pytest.mark.parametrize("kind", ["ctbr", "srt", "ps", "lv"])
-def test_k1_fp32_100_steps(gdyn, kind):
-    """North star: FP32 states within 1e-5 (per-field floors) over 100 steps."""
-    traj, cmds = gdyn[f"traj_{kind}"], gdyn[f"traj_{kind}_cmds"]
+def _gpu_trajectory(kind, x0, cmds):
     p = native_params(QuadParams(), SimConfig(), ControllerGains())
-    pl = planes(traj[0], torch.float32)
+    pl = planes(x0, torch.float32)
     n = pl.shape[1]
-    worst = np.zeros(17)
+    out = [pl.T.double().cpu().numpy()]
     for t in range(cmds.shape[0]):
         a = torch.as_tensor(cmds[t], dtype=torch.float32, device=DEV).contiguous()
         nat.check(nat.lib().qb_dynamics_step(p, nat.CMD[kind], nat.QB_F32, n, n, nat.ptr(pl), nat.ptr(a), None, None,
                                              nat.stream_of()))
-        err = state_error(pl.T.double().cpu().numpy(), traj[t + 1])
-        worst = np.maximum(worst, err.max(axis=0))
-    print(kind, "worst per-field normalised error over 100 steps:", np.array2string(worst, precision=2))
-    # CTBR is well conditioned; random per-rotor SRT thrusts tumble the vehicle
-    # at O(100) rad/s and LV/PS close the loop through the saturating mixer, so
-    # FP32 rounding grows chaotically there (SURVEY.md 7.3-1).  Each one-step
-    # map stays < 1e-6 (test_k1_fp32_one_step); report the 100-step drift.
-    tol = 1e-5 if kind == "ctbr" else 5e-5
-    assert worst.max() < tol
+        out.append(pl.T.double().cpu().numpy())
+    return np.asarray(out)
+
+
+def _check_100_steps(kind, x0, cmds, ref, label):
+    """North star: FP32 states within 1e-5 (per-field floors) over 100 steps,
+    on every env the reference itself can hold there.
+
+    Closed loops through the saturating mixer (LV / PS) and tumbling open-loop
+    SRT are ill-conditioned at FP32 precision: the FP64 oracle
+    FED FP32-ROUNDED INPUTS (round to nearest, plus one-ulp perturbed replicas)
+    already spends more than half of the 1e-5 budget on some envs.  Those envs
+    are flagged by the oracle alone (oracle/parity.py fp32_conditioning) before
+    the GPU result is looked at; every other env must meet 1e-5 exactly as the
+    north star states.
+    Reported: per-field max and p99, count over 1e-5, flagged count, and how
+    many flagged envs start diverging at a mixer event (a rotor within 1e-3 N
+    of the thrust floor, where sqrt(f/k2) amplifies rounding, or a torque
+    scale s < 1)."""
+    from oracle.parity import fp32_conditioning
+
+    P = oracle.pack_params(QuadParams(), SimConfig(), ControllerGains())
+    cond = fp32_conditioning(P, kind, x0, cmds, ref=ref)
+    got = _gpu_trajectory(kind, x0, cmds)
+    err = state_error(got, ref)  # (T+1, N, 17)
+    env_err = err.max(axis=(0, 2))
+    field_max = err.max(axis=(0, 1))
+    field_p99 = np.percentile(err.max(axis=0), 99, axis=0)
+    over = env_err > 1e-5
+    fl = cond["flagged"]
+    print(f"{label} {kind}: envs {len(env_err)}, GPU over 1e-5: {int(over.sum())}, oracle-flagged (FP32-rounded inputs "
+          f"leave 1e-5): {int(fl.sum())}, flagged with a mixer event at onset: {int(cond['mixer_at_onset'].sum())}; "
+          f"unflagged worst {env_err[~fl].max() if (~fl).any() else 0:.2e}")
+    print("  per-field max", np.array2string(field_max, precision=1))
+    print("  per-field p99", np.array2string(field_p99, precision=1))
+    bad = over & ~fl
+    assert not bad.any(), (f"{int(bad.sum())} unflagged envs over 1e-5", env_err[bad], cond["dev"][bad])
+    if fl.any():  # flagged envs: the GPU drifts no further than a small multiple of the reference's own FP32-input drift
+        ratio = env_err[fl] / cond["dev"][fl]
+        print(f"  flagged: GPU err / oracle FP32-input drift: median {np.median(ratio):.2f}, max {ratio.max():.2f}")
+        assert ratio.max() < 4.0, ratio.max()
+    return over, fl
+
+
+@pytest.mark.parametrize("kind", ["ctbr", "srt", "ps", "lv"])
+def test_k1_fp32_100_steps(gdyn, kind):
+    """The reference's own 100-step closed loops (golden, 16 envs)."""
+    traj, cmds = gdyn[f"traj_{kind}"], gdyn[f"traj_{kind}_cmds"]
+    over, fl = _check_100_steps(kind, traj[0], cmds, traj, "golden")
+    if kind == "ctbr":  # well conditioned: every env within 1e-5
+        assert not over.any()
+
+
+@pytest.mark.parametrize("kind", ["ctbr", "srt", "ps", "lv"])
+def test_k1_fp32_100_steps_parity_set(kind):
+    """SURVEY 8-D parity set: 1024 seeded random envs x 100 steps with a fresh
+    command every step, reference = the oracle (pinned bit-exact to the
+    reference's goldens).  Fresh random commands every step make these loops
+    strongly chaotic: for SRT / PS nearly every env is flagged, and the claim
+    that carries is the ratio bound on flagged envs."""
+    from oracle.parity import oracle_trajectory, parity_set
+
+    P = oracle.pack_params(QuadParams(), SimConfig(), ControllerGains())
+    x0, cmds = parity_set(kind, 1024, 100, seed=11)
+    ref, _, _ = oracle_trajectory(P, kind, x0, cmds)
+    _check_100_steps(kind, x0, cmds, ref, "parity-set")
 
 
 def test_command_fp64_exact(gdyn):

@@ -237,7 +237,7 @@ def run_env(args, rank, world, kind):
         K = max(G, (K + G - 1) // G * G)
         args.steps = K
         acts = make_actions(kind, n, K + W, rank)
-        static_a = torch.empty((G, n, 4), device="cuda")
+        static_a = torch.zeros((G, n, 4), device="cuda")
         graph = env.make_step_graph(static_a)
 
     def launch(a, events=None):

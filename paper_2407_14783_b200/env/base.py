@@ -20,7 +20,12 @@ launch).
 Observations and flags are device tensors.  `observations[i]` / `info[i]`
 materialise the reference's per-agent dicts on demand (a host copy), so code
 written against the reference keeps working; batched consumers index by key
-(`observations["depth"]`) and never leave the GPU.
+(`observations["depth"]`) and never leave the GPU.  Like the reference's
+fresh per-step arrays, a StepResult does not change when the env steps on:
+reward / flags / info are a one-copy snapshot of the step's output block and
+the state observation a snapshot of the planes; rendered frames are
+double-buffered (valid through the next step, StaleObservations after that
+unless materialised or cloned).
 
 Sharding: an env built with `shard=(rank, world)` owns the contiguous global
 index range [rank*N/world, (rank+1)*N/world).  Streams are keyed by the
@@ -48,25 +53,44 @@ from ..sharding import shard_range
 DRONE_ID0 = 60000
 
 
+class StaleObservations(RuntimeError):
+    """Observations indexed after the env overwrote their buffers."""
+
+
 class Observations(Sequence):
     """Batched observation dict that also indexes like the reference list.
 
     obs["depth"] -> (N,H,W) CUDA tensor; obs[i] -> {"state": (13,), ...} numpy
     dict for agent i (reference layout, float64, segmentation cast to float).
-    The tensors are the env's persistent device buffers: the next step
-    overwrites them (clone, or index obs[i] before stepping, to keep them).
+
+    The reference returns fresh arrays every step (base.py:287-310).  Here the
+    state is a per-step snapshot and the rendered images live in one of two
+    buffer sets the env alternates between, so the observations of step k stay
+    valid through step k+1 (the usual act-then-step loop) without copying
+    2 GB of frames per step at config 3.  Step k+2 overwrites them: indexing
+    an Observations that old raises StaleObservations -- except obs[i] once it
+    was materialised (obs[i] / as_reference() copy everything to the host on
+    first use) -- and `clone()` gives a device copy that never goes stale.
     """
 
-    def __init__(self, data: dict, n: int, seg_keys=()):
+    def __init__(self, data: dict, n: int, seg_keys=(), env=None, gen: int = 0):
         self._data = data
         self._n = n
         self._seg_keys = set(seg_keys)
         self._host = None
+        self._env = env
+        self._gen = gen
+
+    def _check_fresh(self):
+        if self._env is not None and self._env._obs_gen - self._gen >= 2:
+            raise StaleObservations(f"observations of step {self._gen} were overwritten by step {self._env._obs_gen}: "
+                                    f"index or clone() them before stepping twice (the env double-buffers its frames)")
 
     def keys(self):
         return self._data.keys()
 
     def items(self):
+        self._check_fresh()
         return self._data.items()
 
     def __contains__(self, key):
@@ -75,13 +99,20 @@ class Observations(Sequence):
     def __len__(self):
         return self._n
 
+    def clone(self) -> "Observations":
+        """A device copy that the env never overwrites."""
+        self._check_fresh()
+        return Observations({k: v.clone() for k, v in self._data.items()}, self._n, self._seg_keys)
+
     def _materialize(self):
         if self._host is None:
+            self._check_fresh()
             self._host = {k: v.detach().cpu().numpy().astype(np.float64) for k, v in self._data.items()}
         return self._host
 
     def __getitem__(self, key):
-        if isinstance(key, str):
+        if isinstance(key, str):  # the device tensor itself: valid through the next step only
+            self._check_fresh()
             return self._data[key]
         if isinstance(key, slice):
             return [self[i] for i in range(*key.indices(self._n))]
@@ -97,7 +128,8 @@ class Observations(Sequence):
 
 
 class Info(Sequence):
-    """Per-agent info dicts (base.py:195-207), materialised lazily."""
+    """Per-agent info dicts (base.py:195-207), materialised lazily from the
+    step's own snapshot (later steps never change them)."""
 
     _KEYS = ("success", "collision", "out_of_bounds", "nonfinite", "nearest_distance", "scene", "step")
 
@@ -112,10 +144,14 @@ class Info(Sequence):
     def __getitem__(self, i):
         if isinstance(i, str):
             return self.data[i]
+        if isinstance(i, slice):
+            return [self[k] for k in range(*i.indices(self._n))]
         if self._host is None:
             self._host = {k: self.data[k].detach().cpu().numpy() for k in self._KEYS}
         h = self._host
         i = int(i)
+        if not -self._n <= i < self._n:
+            raise IndexError(i)
         return {
             "success": bool(h["success"][i]), "collision": bool(h["collision"][i]),
             "out_of_bounds": bool(h["out_of_bounds"][i]), "nonfinite": bool(h["nonfinite"][i]),
@@ -123,13 +159,27 @@ class Info(Sequence):
         }
 
 
+class _Snapshot:
+    """Holder of the typed views of one step's output snapshot."""
+
+
 @dataclass
 class StepResult:
+    """base.py:37-43.  reward / terminated / truncated / info are this step's
+    own device tensors (a snapshot: later steps do not change them);
+    as_reference() converts to the reference's numpy / list-of-dict form."""
+
     observations: Observations
     reward: object
     terminated: object
     truncated: object
     info: Info
+
+    def as_reference(self):
+        cpu = lambda t: t.detach().cpu().numpy() if hasattr(t, "detach") else np.asarray(t)  # noqa: E731
+        return StepResult(self.observations.as_reference(), cpu(self.reward).astype(np.float64),
+                          cpu(self.terminated).astype(bool), cpu(self.truncated).astype(bool),
+                          [self.info[i] for i in range(len(self.info))])
 
 
 def _dist(d, spec):
@@ -210,19 +260,15 @@ class QuadEnvBase:
         self._action_host = [torch.zeros((n, 4), dtype=dt, pin_memory=True) for _ in range(2)]
         self._action_host_ev = [None, None]
         self._action_host_i = 0
-        self.step_counts = z(n, dtype=torch.int32)
-        self.agent_scene = z(n, dtype=torch.int32)
+        # per-step outputs in ONE allocation: a StepResult snapshots them with one copy
+        self._outblk = z(self._outblk_bytes(n))
+        self._out_views(self._outblk, self)
         self._reset_counts = z(n, dtype=torch.int32)
-        self._flags = z(7, n)
-        (self._needs_respawn, self._terminated, self._truncated, self._success, self._collision, self._oob,
-         self._nonfinite) = self._flags.unbind(0)
-        self._reward = z(n, dtype=torch.float32)
-        self.nearest_dist = z(n, dtype=torch.float64)
-        self.nearest_pt = z(n, 3, dtype=torch.float64)
         self._rng = z(n, 4, dtype=torch.int64)
         self._errors = z(1, dtype=torch.int32)
         self._scene_perm = z(len(self.scenes), dtype=torch.int32)
-        # observation buffers: one render per distinct camera
+        # observation buffers: one render per distinct camera, two buffer sets
+        # (step k renders into set k % 2: the previous step's frames stay valid)
         self._cams, self._sensor_slot = {}, {}
         for spec, cam in self.sensor_cameras:
             if cam is None:
@@ -233,12 +279,18 @@ class QuadEnvBase:
             slot = self._cams[key]
             self._sensor_slot[spec.name] = slot
             if spec.kind == "depth" and slot["depth"] is None:
-                slot["depth"] = torch.zeros((n, cam.height, cam.width), dtype=dt, device=dev)
+                slot["depth_pair"] = [torch.zeros((n, cam.height, cam.width), dtype=dt, device=dev) for _ in range(2)]
             if spec.kind == "segmentation" and slot["seg"] is None:
-                slot["seg"] = torch.zeros((n, cam.height, cam.width), dtype=torch.int32, device=dev)
-            spec_slot = slot
+                slot["seg_pair"] = [torch.zeros((n, cam.height, cam.width), dtype=torch.int32, device=dev) for _ in range(2)]
+            for k in ("depth", "seg"):
+                if slot.get(k + "_pair"):
+                    slot[k] = slot[k + "_pair"][0]
             if not spec.noise:
-                spec_slot["names"].append((spec.name, spec.kind))
+                slot["names"].append((spec.name, spec.kind))
+        for slot in self._cams.values():
+            if self._centroid_id(slot):
+                slot["centroid_pair"] = [torch.zeros((n, 2), dtype=torch.float32, device=dev) for _ in range(2)]
+                slot["centroid"] = slot["centroid_pair"][0]
         # the observation pass (qb_env_observe): IMU readings and noisy camera
         # sensors, in config order -- the order their draws leave each env's
         # generator (base.py:287-305)
@@ -251,26 +303,35 @@ class QuadEnvBase:
                     check_noise(nz, spec.kind)
             except Exception as e:  # the reference raises on the first observation
                 self._noise_error = self._noise_error or e
-            if spec.kind == "imu":
-                out = torch.zeros((n, 6), dtype=dt, device=dev)
-                rec = sensor_obs("imu", spec.noise, out)
-            elif spec.noise:
-                slot = self._sensor_slot[spec.name]
-                out = torch.zeros((n, cam.height, cam.width), dtype=dt, device=dev)
-                src = slot["depth"] if spec.kind == "depth" else slot["seg"]
-                rec = sensor_obs(spec.kind, spec.noise, out, src=src, width=cam.width, height=cam.height)
-            else:
-                continue
-            self._obs_sensors.append({"name": spec.name, "kind": spec.kind, "out": out, "rec": rec})
+            outs, recs = [], []
+            for i in range(2):
+                if spec.kind == "imu":
+                    out = torch.zeros((n, 6), dtype=dt, device=dev)
+                    rec = sensor_obs("imu", spec.noise, out)
+                elif spec.noise:
+                    slot = self._sensor_slot[spec.name]
+                    out = torch.zeros((n, cam.height, cam.width), dtype=dt, device=dev)
+                    src = slot["depth_pair"][i] if spec.kind == "depth" else slot["seg_pair"][i]
+                    rec = sensor_obs(spec.kind, spec.noise, out, src=src, width=cam.width, height=cam.height)
+                else:
+                    break
+                outs.append(out)
+                recs.append(rec)
+            if outs:
+                self._obs_sensors.append({"name": spec.name, "kind": spec.kind, "out": outs[0], "outs": outs,
+                                          "recs": recs})
         if self._obs_sensors:
-            arr = (nat.QbSensorObs * len(self._obs_sensors))(*[o["rec"] for o in self._obs_sensors])
-            self._obs_array = arr
+            self._obs_arrays = [(nat.QbSensorObs * len(self._obs_sensors))(*[o["recs"][i] for o in self._obs_sensors])
+                                for i in range(2)]
+            self._obs_array = self._obs_arrays[0]
         # swarm mode: the other agents as render spheres + the swarm observation
         self._swarm_spheres = self._swarm_ids = self._swarm_obs = None
         if self.swarm and n > 1:
             self._swarm_spheres = torch.zeros((n, n - 1, 4), dtype=dt, device=dev)
             self._swarm_ids = torch.zeros((n, n - 1), dtype=torch.int32, device=dev)
-            self._swarm_obs = torch.zeros((n, n - 1, 13), dtype=dt, device=dev)
+            self._swarm_obs_pair = [torch.zeros((n, n - 1, 13), dtype=dt, device=dev) for _ in range(2)]
+            self._swarm_obs = self._swarm_obs_pair[0]
+        self._obs_i, self._obs_gen = 0, 0
         bufs = nat.QbEnvBuffers()
         bufs.n, bufs.ld, bufs.index_offset = n, n, self.index_offset
         bufs.dtype = nat.QB_F32 if dt == torch.float32 else nat.QB_F64
@@ -283,6 +344,55 @@ class QuadEnvBase:
                          ("error_count", self._errors)):
             setattr(bufs, field, None if t is None else t.data_ptr())
         self._bufs = bufs
+
+    # per-step output block: flags (7 x n u8) | reward f32 | step i32 | scene i32 | nearest dist f64 | point f64 x 3
+    @staticmethod
+    def _outblk_layout(n):
+        r8 = lambda x: (x + 7) // 8 * 8  # noqa: E731
+        off, lay = 0, {}
+        for name, nbytes in (("flags", 7 * n), ("reward", 4 * n), ("step", 4 * n), ("scene", 4 * n),
+                             ("dist", 8 * n), ("pt", 24 * n)):
+            lay[name] = (off, off + nbytes)
+            off = r8(off + nbytes)
+        return lay, off
+
+    @classmethod
+    def _outblk_bytes(cls, n):
+        return max(cls._outblk_layout(n)[1], 8)
+
+    def _out_views(self, blk, into):
+        """Typed views of a per-step output block (the env's own, or a snapshot)."""
+        import torch
+
+        n = self.num_agents
+        lay, _ = self._outblk_layout(n)
+        v = lambda k, dt: blk[lay[k][0]:lay[k][1]].view(dt)  # noqa: E731
+        flags = v("flags", torch.uint8).view(7, n)
+        (into._needs_respawn, into._terminated, into._truncated, into._success, into._collision, into._oob,
+         into._nonfinite) = flags.unbind(0)
+        into._flags = flags
+        into._reward = v("reward", torch.float32)
+        into.step_counts = v("step", torch.int32)
+        into.agent_scene = v("scene", torch.int32)
+        into.nearest_dist = v("dist", torch.float64)
+        into.nearest_pt = v("pt", torch.float64).view(n, 3)
+        return into
+
+    def _flip_observation_buffers(self):
+        """Step k renders into buffer set k % 2 (see Observations)."""
+        self._obs_i ^= 1
+        i = self._obs_i
+        for slot in self._cams.values():
+            for k in ("depth", "seg", "centroid"):
+                if slot.get(k + "_pair"):
+                    slot[k] = slot[k + "_pair"][i]
+        for o in self._obs_sensors:
+            o["out"] = o["outs"][i]
+        if self._obs_sensors:
+            self._obs_array = self._obs_arrays[i]
+        if self._swarm_obs is not None:
+            self._swarm_obs = self._swarm_obs_pair[i]
+        self._obs_gen += 1
 
     def _pack_task(self):
         c = self.config
@@ -380,15 +490,19 @@ class QuadEnvBase:
 
         if not self._reset_done:
             raise NotReset("call reset() before step()")
+        if self._noise_error is not None:  # before any launch (the reference raises on the first observation)
+            raise self._noise_error
         self._check_async_errors()
         a = self._stage_action(action)
         self._bufs.action = a.data_ptr()
         with torch.cuda.device(self.device):
             if self.split_step:
                 join = self._launch_split_dynamics()
-                self._record_async_errors()
-                obs = self.get_observation()
-                join()
+                try:
+                    self._record_async_errors()
+                    obs = self.get_observation()
+                finally:  # phase 2 always rejoins the main stream
+                    join()
             else:
                 nat.check(nat.lib().qb_env_step(self._P, self._kind, self._task, self.dev_scenes.handle, self._bufs,
                                                 nat.stream_of()), "qb_env_step")
@@ -400,12 +514,16 @@ class QuadEnvBase:
             terminated = success | self.collision | self.out_of_bounds | self.nonfinite
             truncated = ~terminated & (self.step_counts >= self.config.episode_max_steps)
             self._needs_respawn.copy_((terminated | truncated).to(torch.uint8))
-        else:
-            success, reward = self._success.bool(), self._reward
-            terminated, truncated = self._terminated.bool(), self._truncated.bool()
-        info = Info({"success": success, "collision": self.collision, "out_of_bounds": self.out_of_bounds,
-                     "nonfinite": self.nonfinite, "nearest_distance": self.nearest_dist, "scene": self.agent_scene,
-                     "step": self.step_counts}, self.num_agents)
+        # this step's outputs, snapshotted with one device copy: the reference
+        # returns fresh arrays per step (base.py:186-210)
+        snap = self._out_views(self._outblk.clone(), _Snapshot())
+        if not self._custom_hooks:
+            success, reward = snap._success.view(torch.bool), snap._reward
+            terminated, truncated = snap._terminated.view(torch.bool), snap._truncated.view(torch.bool)
+        info = Info({"success": success, "collision": snap._collision.view(torch.bool),
+                     "out_of_bounds": snap._oob.view(torch.bool), "nonfinite": snap._nonfinite.view(torch.bool),
+                     "nearest_distance": snap.nearest_dist, "scene": snap.agent_scene, "step": snap.step_counts},
+                    self.num_agents)
         return StepResult(obs, reward, terminated, truncated, info)
 
     def _record_async_errors(self):
@@ -425,8 +543,10 @@ class QuadEnvBase:
             raise SpawnFailure(f"{n} respawns found no spawn with clearance >= {self.config.min_spawn_clearance}")
 
     def _render_and_observe(self):
-        """Launch the observation kernels: K2 once per distinct camera, then
-        the sensor pass (IMU + noise chains) if any sensor needs it."""
+        """Launch the observation kernels into the next buffer set: K2 once per
+        distinct camera, then the sensor pass (IMU + noise chains) if any
+        sensor needs it."""
+        self._flip_observation_buffers()
         self._render()
         self._observe()
 
@@ -437,10 +557,6 @@ class QuadEnvBase:
                       "qb_env_swarm_views")
         for slot in self._cams.values():
             cid = self._centroid_id(slot)
-            if cid and slot["centroid"] is None:
-                import torch
-
-                slot["centroid"] = torch.zeros((self.num_agents, 2), dtype=torch.float32, device=self.device)
             render_state(self.dev_scenes, slot["camera"], self._planes, env_scene=self.agent_scene, depth=slot["depth"],
                          seg=slot["seg"], centroid_id=cid, centroid=slot["centroid"] if cid else None,
                          extra=self._swarm_spheres, extra_ids=self._swarm_ids)
@@ -459,7 +575,7 @@ class QuadEnvBase:
         if self._noise_error is not None:
             raise self._noise_error
         self._render_and_observe()
-        obs = {"state": self._planes[0:13].T}
+        obs = {"state": self._planes[0:13].clone().T}  # a snapshot: rows 0..12 of the planes are contiguous
         seg_keys = []
         for spec, cam in self.sensor_cameras:
             noisy = next((o for o in self._obs_sensors if o["name"] == spec.name), None)
@@ -473,7 +589,7 @@ class QuadEnvBase:
         if self._swarm_obs is not None:
             obs["swarm"] = self._swarm_obs
         self._extra_observations(obs)
-        return Observations(obs, self.num_agents, seg_keys)
+        return Observations(obs, self.num_agents, seg_keys, env=self, gen=self._obs_gen)
 
     def _centroid_id(self, slot) -> int:
         return 0
@@ -489,13 +605,24 @@ class QuadEnvBase:
         K consecutive steps, step k reading actions[k].  Returns a callable that
         replays the graph; refill `actions` in place between replays.  For
         latency-bound small batches (configs 1/2, N=100) this removes the
-        per-step host launch overhead."""
+        per-step host launch overhead.
+
+        Capture needs warm-up launches (2 K real steps with whatever `actions`
+        holds); the env's state, flags, counters and RNG streams are saved
+        before them and restored after, so making the graph does not advance
+        the env.  Each replay surfaces respawn failures of the previous one
+        (SpawnFailure), as step() does."""
         import torch
 
+        if not self._reset_done:
+            raise NotReset("call reset() before make_step_graph()")
         seq = actions if actions.dim() == 3 else actions.unsqueeze(0)
         if seq.shape[1:] != (self.num_agents, 4) or not seq.is_cuda or seq.dtype != self.dtype:
             raise ActionShapeMismatch(f"graph actions must be a ({self.num_agents},4) or (K,{self.num_agents},4) "
                                       f"{self.dtype} CUDA tensor")
+        keep = [t for t in (self._planes, self._prev, self._outblk, self._rng, self._reset_counts, self._errors)
+                if t is not None]
+        saved = [t.clone() for t in keep]
         stream = torch.cuda.Stream(device=self.device)
         stream.wait_stream(torch.cuda.current_stream(self.device))
         g = torch.cuda.CUDAGraph()
@@ -509,9 +636,21 @@ class QuadEnvBase:
                 for k in range(seq.shape[0]):
                     self._bufs.action = seq[k].data_ptr()
                     self._launch_step()
+            for t, v in zip(keep, saved):  # undo the warm-up
+                t.copy_(v)
         torch.cuda.current_stream(self.device).wait_stream(stream)
+        # replays write the observation buffer sets in the captured order, so
+        # after every replay the last captured step's set is the current one
         self._graph_keepalive = seq
-        return g.replay
+        k_steps = seq.shape[0]
+
+        def replay():
+            self._check_async_errors()
+            g.replay()
+            self._obs_gen += k_steps
+            self._record_async_errors()
+
+        return replay
 
     def _launch_split_dynamics(self):
         """Phase 1 on the current stream, phase 2 forked onto the post stream;

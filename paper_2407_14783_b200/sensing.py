@@ -100,20 +100,24 @@ def render_frames(scene, body_position, body_orientation, camera: CameraModel, e
     depth = torch.empty((n, camera.height, camera.width), dtype=dtype, device=dev.device)
     seg = torch.empty((n, camera.height, camera.width), dtype=torch.int32, device=dev.device)
     code = nat.QB_F32 if dtype == torch.float32 else nat.QB_F64
+    ex = ex_ids = None
+    k = 0
+    if extra_spheres is not None and (extra_spheres.numel() if isinstance(extra_spheres, torch.Tensor)
+                                      else np.asarray(extra_spheres).size):
+        # per-view spheres [x y z r] + their ids (kernels.py:438-445: swarm agents, ids 60000 + j)
+        ex = torch.as_tensor(extra_spheres, dtype=dtype, device=dev.device).reshape(n, -1, 4).contiguous()
+        k = ex.shape[1]
+        if extra_ids is None:
+            raise ValueError("extra_spheres needs extra_ids")
+        ex_ids = torch.as_tensor(extra_ids, device=dev.device).to(torch.int32).reshape(n, k).contiguous()
     with torch.cuda.device(dev.device):
-        if extra_spheres is not None and np.asarray(extra_spheres).size:
-            # swarm spheres need per-view poses inside the kernel: go through the state path
-            return _render_with_extra(dev, o, r, camera, extra_spheres, extra_ids, host, dtype)
         nat.check(nat.lib().qb_render_poses(dev.handle, camera.native(), code, n, nat.ptr(o), nat.ptr(r), nat.ptr(env_scene),
-                                            nat.ptr(depth), nat.ptr(seg), None, None, 0, nat.stream_of()),
+                                            nat.ptr(depth), nat.ptr(seg), nat.ptr(ex), nat.ptr(ex_ids), k,
+                                            nat.stream_of()),
                   "qb_render_poses")
     if host:
         return depth.double().cpu().numpy(), seg.long().cpu().numpy()
     return depth, seg
-
-
-def _render_with_extra(dev, o, r, camera, extra, extra_ids, host, dtype):
-    raise NotImplementedError("extra spheres through render_frames: use the env swarm path (F2)")
 
 
 def render_depth(scene, body_position, body_orientation, camera: CameraModel):

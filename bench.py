@@ -95,10 +95,11 @@ class ClockSampler:
         self._stop.set()
         if self._t:
             self._t.join(timeout=6)
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        good = [s for s in self.samples if len(s) >= 3]
+        sm = [float(s[0]) for s in good if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in good if s[1].replace(".", "").isdigit()]
         reasons = set()
-        for s in self.samples:
+        for s in good:
             try:
                 v = int(s[2], 16)
             except Exception:
@@ -111,17 +112,28 @@ class ClockSampler:
 # ---------------------------------------------------------------- distributed
 
 
+# plumbing test hook only (tests/test_gpu_sharding.py): QB_BENCH_SHARE_GPU=1 puts
+# every rank on cuda:0 with the gloo backend, to exercise the launcher and the
+# max-over-ranks timing on a one-GPU box; its numbers are not benchmark values
+SHARE_GPU = os.environ.get("QB_BENCH_SHARE_GPU") == "1"
+
+
 def dist_setup():
     import torch
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if SHARE_GPU:
+        local = 0
     torch.cuda.set_device(local if world > 1 else 0)
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if SHARE_GPU:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return rank, world, local
 
 
@@ -138,7 +150,7 @@ def max_over_ranks(x, world):
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device="cpu" if SHARE_GPU else "cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -266,7 +278,7 @@ def run_env(args, rank, world, kind):
     ev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(4)) for _ in range(K)]
     barrier(world)
     torch.cuda.synchronize()
-    clk = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))
+    clk = ClockSampler(0 if SHARE_GPU else int(os.environ.get("LOCAL_RANK", "0")))
     clk.start()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0.record()
@@ -446,7 +458,8 @@ def run_bptt(args, rank, world):
     from paper_2407_14783_b200.params import native_params
     from paper_2407_14783_b200.sharding import reduce_bptt
 
-    n, T = ENVS["c4"], 64
+    # weak scaling: 16384 envs per GPU; --strong: 16384 envs in total, split over the ranks
+    n, T = (ENVS["c4"] // world if args.strong else ENVS["c4"]), 64
     P = native_params()
     g = torch.Generator(device="cuda").manual_seed(7 + rank)
     init = torch.zeros((17, n), device="cuda")
@@ -456,7 +469,7 @@ def run_bptt(args, rank, world):
     acts = 900.0 + torch.randn((T, n, 4), device="cuda", generator=g) * 20.0
     target = torch.tensor([1.0, 0.0, 2.0], device="cuda")
     gsum = torch.zeros(T * 4, dtype=torch.float64, device="cuda")
-    red = torch.zeros(T * 4 + 1, dtype=torch.float64, device="cuda")
+    red = torch.zeros(T * 4 + 1, dtype=torch.float64, device="cpu" if SHARE_GPU else "cuda")
 
     def iteration():
         tape, _ = G.rollout_planes(P, "rotor", init, acts)
@@ -474,7 +487,7 @@ def run_bptt(args, rank, world):
     torch.cuda.synchronize()
     barrier(world)
     K = args.steps
-    clk = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))
+    clk = ClockSampler(0 if SHARE_GPU else int(os.environ.get("LOCAL_RANK", "0")))
     clk.start()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0.record()
@@ -555,12 +568,15 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
     ap.add_argument("--no-cpu", dest="cpu", action="store_false")
+    ap.add_argument("--strong", action="store_true", help="c4: fixed 16384 envs in total (strong scaling)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     kind = args.workload
 
     if args.impl == "reference":
         return reference_arm(args, kind)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args.gpus)
 
     import torch
 
@@ -572,6 +588,7 @@ def main():
     if kind == "c4":
         r = run_bptt(args, rank, world)
         steps_total = r["n"] * r["T"] * world * args.steps
+        line["scaling"] = "strong" if args.strong else "weak"
         line.update({"metric": "BPTT env-steps/sec (forward + adjoint), whole box", "value": steps_total / (r["ms"] / 1e3),
                      "ms_per_step": r["ms"] / args.steps, "clocks": r["clocks"], "gpu_launches": 2 * args.steps,
                      "config": {"workload": WORKLOADS[kind], "envs_per_gpu": r["n"], "horizon": r["T"],
@@ -654,6 +671,25 @@ def main():
         dist.destroy_process_group()
 
 
+def spawn_ranks(n):
+    """`bench.py --gpus N` without a launcher: re-run this script under
+    torch.distributed.run with one rank per GPU (rendezvous on 127.0.0.1);
+    rank 0 prints the JSON line."""
+    import socket
+
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < n and not SHARE_GPU:
+        raise SystemExit(f"--gpus {n}: only {have} CUDA device(s) visible")
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}", "--master-addr",
+           "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd, check=False).returncode
+
+
 def reference_arm(args, kind):
     """--impl reference: the reference's algorithm on the host cores (the C
     oracle restatement -- the Python reference cannot be compiled and does
@@ -681,4 +717,4 @@ def reference_arm(args, kind):
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main() or 0)

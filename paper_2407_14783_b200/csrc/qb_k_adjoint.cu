@@ -3,9 +3,9 @@
 // VJP.  One env per thread walks t = T-1 .. 0 keeping lambda (17) in
 // registers; per step it reads the saved pre-step state (17 planes) and the
 // action (16 B), and writes the action gradient (16 B): ~236 B/env-step of
-// HBM traffic, plus the optional in-kernel reduction of the action gradient
-// over envs (warp shuffle, one double atomic per warp) that feeds the
-// multi-GPU all-reduce of a shared open-loop action sequence.
+// HBM traffic, plus the optional deterministic env-sum of the action
+// gradient (k_env_sum) that feeds the multi-GPU all-reduce of a shared
+// open-loop action sequence.
 #include <type_traits>
 
 #include "qb_adjoint.cuh"
@@ -21,8 +21,7 @@ __global__ void __launch_bounds__(128) k_rollout_bwd(DynConsts<R> C, long long n
                                                      const typename storage_of<R>::type *actions,
                                                      const typename storage_of<R>::type *g_traj,
                                                      typename storage_of<R>::type *grad_actions,
-                                                     typename storage_of<R>::type *grad_init, uint8_t *boundary,
-                                                     double *action_grad_sum) {
+                                                     typename storage_of<R>::type *grad_init, uint8_t *boundary) {
     using S = typename storage_of<R>::type;
     // FP32 2-substep build: the first substep's stages go through shared
     // memory (one column of 52 floats per thread) instead of being recomputed
@@ -89,15 +88,6 @@ __global__ void __launch_bounds__(128) k_rollout_bwd(DynConsts<R> C, long long n
 #pragma unroll
             for (int k = 0; k < 4; ++k) gp[k] = to_store(ga[k]);
         }
-        if (action_grad_sum) {  // env-sum of the action gradient (shared parameters)
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                double v = live ? r_dbl(ga[k]) : 0.0;
-#pragma unroll
-                for (int s = 16; s > 0; s >>= 1) v += __shfl_xor_sync(FULL, v, s);
-                if ((threadIdx.x & 31) == 0) atomicAdd(action_grad_sum + 4 * t + k, v);
-            }
-        }
         if (!single) {
 #pragma unroll
             for (int k = 0; k < 17; ++k) lam[k] = lam[k] + R(gn[k]);
@@ -108,6 +98,33 @@ __global__ void __launch_bounds__(128) k_rollout_bwd(DynConsts<R> C, long long n
         for (int k = 0; k < 17; ++k) grad_init[k * ld + i] = to_store(lam[k]);
         if (boundary) boundary[i] = flag ? 1 : 0;
     }
+}
+
+// env-sum of the action gradient (shared open-loop parameters, config 4):
+// sum[4 t + k] += sum_i grad[t][i][k] in double, one block per step, a fixed
+// summation order (strided per-thread sums, then a shared-memory tree), so
+// the result is bitwise reproducible run to run -- unlike atomics
+template <class S>
+__global__ void __launch_bounds__(256) k_env_sum(long long n, const S *grad, double *sum) {
+    __shared__ double red[4][256];
+    const int t = blockIdx.x;
+    const S *g = grad + (long long)t * n * 4;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (long long i = threadIdx.x; i < n; i += blockDim.x) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) acc[k] += (double)g[4 * i + k];
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) red[k][threadIdx.x] = acc[k];
+    __syncthreads();
+    for (int s = 128; s > 0; s >>= 1) {
+        if ((int)threadIdx.x < s) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) red[k][threadIdx.x] += red[k][threadIdx.x + s];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x < 4) sum[4 * t + threadIdx.x] += red[threadIdx.x][0];
 }
 
 template <class R>
@@ -128,9 +145,9 @@ int dispatch(const qb_params *p, int kind, long long n, long long ld, int T, con
     auto *gI = static_cast<S *>(gi);
     // the default 2 substeps get a compile-time specialisation (FP32 only)
     const bool sub2 = std::is_same<R, float>::value && C.substeps == 2;
-#define QB_BWD(K)                                                                                         \
-    (sub2 ? (k_rollout_bwd<R, K, 2><<<g, B, 0, st>>>(C, n, ld, T, x, a, gt, gA, gI, boundary, sum), 0) \
-          : (k_rollout_bwd<R, K, 0><<<g, B, 0, st>>>(C, n, ld, T, x, a, gt, gA, gI, boundary, sum), 0))
+#define QB_BWD(K)                                                                                    \
+    (sub2 ? (k_rollout_bwd<R, K, 2><<<g, B, 0, st>>>(C, n, ld, T, x, a, gt, gA, gI, boundary), 0) \
+          : (k_rollout_bwd<R, K, 0><<<g, B, 0, st>>>(C, n, ld, T, x, a, gt, gA, gI, boundary), 0))
     switch (kind) {
         case QB_CMD_ROTOR: QB_BWD(QB_CMD_ROTOR); break;
         case QB_CMD_CTBR: QB_BWD(QB_CMD_CTBR); break;
@@ -138,7 +155,10 @@ int dispatch(const qb_params *p, int kind, long long n, long long ld, int T, con
         default: qb::set_error("command kind %d is not differentiable", kind); return QB_EINVAL;
     }
 #undef QB_BWD
-    return qb::check_launch("rollout_backward");
+    int rc = qb::check_launch("rollout_backward");
+    if (rc || !sum) return rc;
+    k_env_sum<S><<<T < 0 ? 1 : T, 256, 0, st>>>(n, gA, sum);
+    return qb::check_launch("action_grad_sum");
 }
 
 }  // namespace

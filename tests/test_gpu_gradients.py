@@ -68,10 +68,11 @@ def test_rollout_grad_batched_fp32(gjac):
     ga = ga.double().cpu().numpy().transpose(1, 0, 2)
     gi = gi.double().cpu().numpy()
     ref_a, ref_i = gjac["rg_grad_actions"], gjac["rg_grad_init"]
-    scale_a = np.maximum(np.abs(ref_a), np.abs(ref_a).max() * 1e-3)
-    assert (np.abs(ga - ref_a) / scale_a).max() < 1e-3
-    err_i = np.abs(gi - ref_i) / np.maximum(np.abs(ref_i), np.abs(ref_i).max(axis=1, keepdims=True) * 1e-3)
-    assert err_i.max() < 1e-3
+    # north star 1e-4, norm-wise per agent (max abs error / max abs gradient)
+    err_a = np.abs(ga - ref_a).max(axis=(1, 2)) / np.abs(ref_a).max(axis=(1, 2))
+    err_i = np.abs(gi - ref_i).max(axis=1) / np.abs(ref_i).max(axis=1)
+    print("golden rollout_grad FP32: action", err_a, "init", err_i)
+    assert err_a.max() < 1e-4 and err_i.max() < 1e-4
 
 
 def _fd_check(kind, acts_fn, n=6, T=5, seed=0):
@@ -154,3 +155,50 @@ def test_action_grad_sum_is_env_sum():
     s = torch.zeros(T * 4, dtype=torch.float64, device="cuda")
     ga, gi, _ = G.backward_planes(P, "rotor", tape, a, g, action_grad_sum=s)
     np.testing.assert_allclose(s.cpu().numpy().reshape(T, 4), ga.double().sum(1).cpu().numpy(), rtol=1e-5, atol=1e-8)
+
+
+def test_c4_fp32_gradients_h64_vs_reference():
+    """Config 4 shape: hover states + U(+-0.1) position,
+    rotor-speed actions 900 + N(0, 20^2), H = 64, loss = mean_envs
+    |p_T - (1,0,2)|^2 + 1e-6 sum |a - 900|^2.  The FP32 forward + adjoint
+    against the reference's rollout_grad (gradients.py:218-237, the oracle's
+    dense-Jacobian restatement pinned to the reference's goldens) on 64 envs:
+    north star 1e-4, norm-wise per env (max |g_gpu - g_ref| / max |g_ref|
+    over the env's (T, 4) action gradient, and over its 17-vector initial-state
+    gradient)."""
+    n, T = 64, 64
+    rng = np.random.default_rng(64)
+    x0 = np.zeros((n, 17))
+    x0[:, 0:3] = rng.uniform(-0.1, 0.1, (n, 3))
+    x0[:, 6] = 1.0
+    x0[:, 13:17] = QuadParams().hover_speed  # hover states (rotors at hover speed)
+    acts = 900.0 + rng.normal(scale=20.0, size=(T, n, 4))
+    x0 = x0.astype(np.float32).astype(np.float64)  # the FP32 run's exact inputs
+    acts = acts.astype(np.float32).astype(np.float64)
+    target = np.array([1.0, 0.0, 2.0])
+    P = native_params()
+    init = torch.as_tensor(x0.T.copy(), dtype=torch.float32, device="cuda")
+    a = torch.as_tensor(acts, dtype=torch.float32, device="cuda")
+    tape, _ = G.rollout_planes(P, "rotor", init, a)
+    gtraj = torch.zeros_like(tape)
+    gtraj[-1, 0:3] = 2.0 * (tape[-1, 0:3] - torch.as_tensor(target, dtype=torch.float32, device="cuda")[:, None]) / n
+    ga, gi, _ = G.backward_planes(P, "rotor", tape, a, gtraj)
+    ga = ga.double().cpu().numpy() + 2e-6 * (acts - 900.0)  # + d/da of the action penalty
+    gi = gi.double().cpu().numpy().T
+    Po = oracle.pack_params(QuadParams(), SimConfig(), ControllerGains())
+    err_a, err_i = [], []
+    for i in range(n):
+        def loss(tr):
+            g = np.zeros_like(tr)
+            g[-1, 0:3] = 2.0 * (tr[-1, 0:3] - target) / n
+            return 0.0, g
+
+        ra, ri, _, _ = oracle.rollout_grad(Po, x0[i], acts[:, i], loss)
+        ra = ra + 2e-6 * (acts[:, i] - 900.0)
+        err_a.append(np.abs(ga[:, i] - ra).max() / np.abs(ra).max())
+        err_i.append(np.abs(gi[i] - ri).max() / np.abs(ri).max())
+    err_a, err_i = np.array(err_a), np.array(err_i)
+    print(f"C4 FP32 H=64, {n} envs: action grad norm-wise rel err max {err_a.max():.2e} p99 "
+          f"{np.percentile(err_a, 99):.2e} median {np.median(err_a):.2e}; init grad max {err_i.max():.2e}")
+    assert err_a.max() < 1e-4
+    assert err_i.max() < 1e-4

@@ -300,68 +300,52 @@ def run_env(args, rank, world, kind):
         out["render_ms"] = float(np.mean([e[1].elapsed_time(e[2]) for e in ev]))
         if env._obs_sensors:
             out["observe_ms"] = float(np.mean([e[2].elapsed_time(e[3]) for e in ev]))
-    if args.e2e:
-        out["e2e"] = run_e2e(env, world, kind)
     return out
 
 
-def run_e2e(env, world, kind):
-    """Public API end to end: host (pinned) numpy actions in, observations +
-    reward/terminated/truncated back to pinned host memory, every step.  The
-    step's outputs are snapshotted on the device (D2D, ~3 TB/s) and read back
-    on a copy stream, so step k+1 computes while step k's results cross PCIe
-    (double-buffered snapshots and host buffers); the timed region ends when
-    the last step's results are in host memory."""
+def run_e2e(cfg, rank, world, kind):
+    """End to end through the reference-facing flat-array boundary
+    (bindings.step: SPEC.md:566-605 -> qb_env_step_io, one native call per
+    step): actions from pinned host memory, observations + reward / flags /
+    info back in pinned host memory before the call returns.  Host clock
+    around K steps (a host-to-host number), max over ranks."""
     import torch
 
-    from paper_2407_14783_b200.control import CTBR, LV
+    from paper_2407_14783_b200 import bindings
 
-    n = env.num_agents
-    K = 6 if n > 4096 else 50
-    rng = np.random.default_rng(0)
-    host = [np.ascontiguousarray(np.concatenate([rng.normal(size=(n, 3)), rng.uniform(-3, 3, (n, 1))], 1), np.float32)
-            for _ in range(K + 1)]
-    copy_stream = torch.cuda.Stream()
-    snap, outs, done = [{}, {}], [{}, {}], [None, None]
-
-    def one(k, a):
-        cmd = CTBR(a[:, 0] + 9.81, a[:, 1:]) if kind == "c1" else LV(a[:, :3], a[:, 3])
-        r = env.step(cmd)
-        b = k % 2
-        if done[b] is not None:  # buffers of step k-2 fully read back
-            torch.cuda.current_stream().wait_event(done[b])
-        d2h = 0
-        for name, t in list(r.observations.items()) + [("reward", r.reward), ("terminated", r.terminated),
-                                                         ("truncated", r.truncated)]:
-            if name not in snap[b]:
-                snap[b][name] = torch.empty(t.shape, dtype=t.dtype, device=t.device)
-                outs[b][name] = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
-            snap[b][name].copy_(t)
-            d2h += t.numel() * t.element_size()
-        ready = torch.cuda.Event()
-        ready.record()
-        copy_stream.wait_event(ready)
-        with torch.cuda.stream(copy_stream):
-            for name, t in snap[b].items():
-                outs[b][name].copy_(t, non_blocking=True)
-            ev = torch.cuda.Event()
-            ev.record()
-        done[b] = ev
-        return a.nbytes, d2h
-
-    one(0, host[0])  # allocate both buffer sets (pinned host allocation is slow) outside the timed region
-    one(1, host[1])
-    torch.cuda.synchronize()
+    h = bindings.make_env(cfg, shard=(rank, world))
+    n = h.num_agents
+    K = 6 if n > 4096 else 200
+    rng = np.random.default_rng(rank)
+    acts = []
+    for _ in range(K + 2):
+        a = torch.empty((n, 4), dtype=torch.float32, pin_memory=True).numpy()
+        if cfg.command_type == "ctbr":
+            a[:, 0] = 9.81
+            a[:, 1:] = rng.normal(scale=0.5, size=(n, 3))
+        else:
+            a[:, :3] = rng.normal(scale=1.5, size=(n, 3))
+            a[:, 0] += 1.0
+            a[:, 3] = rng.uniform(-math.pi, math.pi, n)
+        acts.append(a)
+    out = h.outputs(pinned=True)
+    bindings.reset(h, 0, out=out)
+    for k in range(2):
+        bindings.step(h, acts[k], out=out)
     barrier(world)
     t = time.perf_counter()
     for k in range(K):
-        h2d, d2h = one(k + 2, host[k + 1])
-    for ev in done:
-        ev.synchronize()
+        res = bindings.step(h, acts[k + 2], out=out)
     dt = max_over_ranks(time.perf_counter() - t, world)
+    d2h = sum(v.nbytes for k, v in out.items() if not k.startswith("_") and hasattr(v, "nbytes")) + out["_small"].nbytes
+    h2d = acts[0].nbytes
+    seg = {k: str(v.dtype) for k, v in res[0].arrays.items()}
+    bindings.close(h)
     return {"value": n * world * K / dt, "unit": "env-steps/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-            "steps": K, "path": "env.step(LV numpy) -> observations/reward/flags to pinned host memory "
-                                "(D2H of step k overlaps step k+1)"}
+            "steps": K, "ms_per_step": dt / K * 1e3, "dtypes": seg,
+            "path": "bindings.step(handle, pinned (N,4) actions) -> qb_env_step_io: action read in place, env step, "
+                    "render, state rows + flags/reward packed into pinned host memory, images D2H (segmentation as "
+                    "uint8 when every id < 256, lossless), stream synchronised before returning"}
 
 
 def run_env_step_roofline(pk):
@@ -558,6 +542,189 @@ def cpu_baseline_bptt(n_sample=8, T=64):
     return n_sample * T / dt, dt
 
 
+def render_rooflines(kind, r, pk, steps):
+    """K2's two roofline figures.  Primary: SM instruction issue, the bound
+    the renderer actually has: warp-instructions per camera from
+    the committed ncu capture x cameras / live kernel time, against 148 SMs x
+    4 schedulers x the SM clock sampled under load.  Secondary: HBM, the
+    algorithmic bytes (depth + seg writes, pose reads) / kernel time."""
+    px = r["n"] * 64 * 64
+    nbytes = px * sum(4 for s in r["cfg"].sensors) + r["n"] * 40
+    gbs = nbytes / (r["render_ms"] / 1e3) / 1e9
+    traffic, meta = profile_traffic("k_render_cull" if kind != "c5" else "k_render_f")
+    hbm = {"bound": "hbm", "achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": gbs / pk["hbm_gbs"],
+           "traffic": traffic * r["n"] if traffic else None,
+           "note": "K2 render: algorithmic bytes = depth+seg writes + pose reads; far below HBM by design"}
+    mhz = (r["clocks"] or {}).get("sm_mhz") or 1965.0
+    rays = px / (r["render_ms"] / 1e3)
+    issue = None
+    if meta and meta.get("warp_instructions_per_unit"):
+        wips = meta["warp_instructions_per_unit"] * r["n"] / (r["render_ms"] / 1e3)
+        peak_wi = 148 * 4 * mhz * 1e6
+        ref_ops = 4360.0 if kind == "c5" else 1470.0
+        issue = {"bound": "issue", "achieved": wips, "peak": peak_wi, "unit": "warp-instr/s", "frac": wips / peak_wi,
+                 "traffic": traffic * r["n"] if traffic else None,
+                 "kernel": "k_render_cull" if kind != "c5" else "k_render_f",
+                 "kernel_ms": r["render_ms"], "step_ms": r["ms"] / steps, "rays_per_s": rays,
+                 "warp_instr_per_camera": meta["warp_instructions_per_unit"],
+                 "reference_ops_per_ray": ref_ops,
+                 "reference_equiv_frac": rays * ref_ops / (148 * 128 * mhz * 1e6),
+                 "ncu": {k: meta[k] for k in ("issue_active_pct", "warps_active_pct", "l1_hit_pct", "l2_hit_pct",
+                                              "registers", "source") if k in meta},
+                 "note": f"dominant kernel of the step ({r['render_ms']:.3f} of {r['ms'] / steps:.3f} ms); "
+                         "peak = 148 SMs x 4 issue slots x the SM clock sampled in the timed region"}
+    return issue, hbm
+
+
+def env_line(kind, args, rank, world, pk, cpu=True, e2e=True):
+    """Bench line body of one env workload (configs 1, 2, 3, 5, ...)."""
+    r = run_env(args, rank, world, kind)
+    value = r["total"] * args.steps / (r["ms"] / 1e3)
+    line = {"value": value, "ms_per_step": r["ms"] / args.steps, "steps": args.steps, "clocks": r["clocks"],
+            "gpu_launches": r["launches"],
+            "config": {"workload": WORKLOADS[kind], "envs_per_gpu": r["n"], "global_envs": r["total"],
+                       "resolution": "64x64", "integrator": "rk4, 2 substeps",
+                       "sensors": ",".join(f"{s.name}:{s.kind}" for s in r["cfg"].sensors) or "none",
+                       "l2": "per-step output (depth+seg, 2.1 GB at c3) >> 126 MB L2; no flush needed"
+                       if not r["graph"] else "100 envs: latency-bound; 10 env steps per CUDA-graph replay "
+                                              "(actions staged by device copies inside the timed region)",
+                       "parallelism": f"env shards x{world}, no per-step collective"}}
+    if "render_ms" in r:
+        line["kernel_ms"] = {"env_step_k1k3": r["step_ms"], "render_k2": r["render_ms"]}
+        if "observe_ms" in r:
+            line["kernel_ms"]["observe_imu_noise"] = r["observe_ms"]
+        issue, hbm = render_rooflines(kind, r, pk, args.steps)
+        line["roofline"] = issue or hbm
+        line["roofline_render_hbm"] = hbm
+    elif r["graph"]:
+        # latency-bound small batch: per-step device time of the whole graph-replayed step
+        line["roofline"] = {"bound": "latency", "achieved": r["ms"] / args.steps * 1e3, "unit": "us/step",
+                            "peak": None, "frac": None, "traffic": None,
+                            "note": "100 envs = 100 warps on 148 SMs: one dependent chain of ~2.6k instructions "
+                                    "per env-step; no throughput roofline applies (see roofline_env_step for K1+K3 "
+                                    "at 4M envs)"}
+    if e2e:
+        line["e2e"] = run_e2e(r["cfg"], rank, world, kind)
+    if rank == 0 and cpu:
+        ns = {"c5": 64, "c3n": 256, "swarm": 256}.get(kind, min(1024, ENVS[kind]))
+        steps = {"c5": 2, "swarm": 4}.get(kind, 12 if ns > 100 else 400)
+        v, dt = cpu_baseline_env(kind, n_sample=ns, steps=steps)
+        line["cpu_baseline"] = {"value": v, "unit": "env-steps/s", "cores": os.cpu_count(), "kind": "port",
+                                "sample": f"{ns} envs x {steps} steps of the same env step on the C oracle "
+                                          f"(OpenMP), {dt:.1f} s"}
+    line["_r"] = r
+    return line
+
+
+def bptt_line(args, rank, world, pk, cpu=True):
+    r = run_bptt(args, rank, world)
+    steps_total = r["n"] * r["T"] * world * args.steps
+    line = {"metric": "BPTT env-steps/sec (forward + adjoint), whole box", "value": steps_total / (r["ms"] / 1e3),
+            "ms_per_step": r["ms"] / args.steps, "steps": args.steps, "clocks": r["clocks"],
+            "scaling": "strong" if args.strong else "weak", "gpu_launches": 3 * args.steps,
+            "config": {"workload": WORKLOADS["c4"], "envs_per_gpu": r["n"], "horizon": r["T"],
+                       "parallelism": f"env shards x{world}, all_reduce(SUM) of loss + shared action grad"},
+            "kernel_ms": {"rollout_forward": r["fwd_ms"], "rollout_backward": r["bwd_ms"]}}
+    fwd_b, bwd_b = 152 + 68, 236  # algorithmic B/env-step (tape write, tape/action read, grad write)
+    gbs = r["n"] * r["T"] * (fwd_b + bwd_b) / ((r["fwd_ms"] + r["bwd_ms"]) / 1e3) / 1e9
+    hbm = {"bound": "hbm", "achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": gbs / pk["hbm_gbs"],
+           "traffic": None, "note": "forward+adjoint, (220+236) algorithmic B/env-step"}
+    line["roofline"] = hbm
+    _, meta = profile_traffic("k_rollout_bwd")
+    if meta and meta.get("warp_instructions_per_unit"):
+        mhz = (r["clocks"] or {}).get("sm_mhz") or 1965.0
+        wips = meta["warp_instructions_per_unit"] * r["n"] * r["T"] / (r["bwd_ms"] / 1e3)
+        line["roofline_adjoint_issue"] = {
+            "bound": "issue", "achieved": wips, "peak": 148 * 4 * mhz * 1e6, "unit": "warp-instr/s",
+            "frac": wips / (148 * 4 * mhz * 1e6), "kernel": "k_rollout_bwd",
+            "note": "the adjoint recomputes each step's RK4 stages and runs the hand-derived VJP: "
+                    f"{meta['warp_instructions_per_unit']:.0f} warp-instr/env-step (ncu) -- issue, not HBM, bounds it"}
+    if rank == 0 and cpu:
+        v, dt = cpu_baseline_bptt()
+        line["cpu_baseline"] = {"value": v, "unit": "env-steps/s", "cores": 1, "kind": "port",
+                                "sample": f"8 agents x H=64 oracle rollout_grad ({dt:.1f} s)"}
+    return line
+
+
+def parity_leg(line, kind):
+    """Checker run after the timed region (never inside it): one more env
+    step of the benchmark env through env.step, re-evaluated by the CPU
+    oracle on the GPU's own pre/post-step states (oracle/parity.py): flags /
+    nearest point / reward bit-exact, dynamics per north-star tolerance, a
+    seeded 512-camera sample re-rendered (mismatch and grazing fractions)."""
+    import torch
+
+    from oracle.parity import env_step_parity, oracle_scenes
+    from paper_2407_14783_b200.control import CTBR, LV
+    from paper_2407_14783_b200.params import ControllerGains, QuadParams, SimConfig
+
+    r = line["_r"]
+    env, cfg = r["env"], r["cfg"]
+    n = env.num_agents
+    rng = np.random.default_rng(99)
+    a = np.concatenate([rng.normal(scale=1.5, size=(n, 3)) + [1.0, 0, 0], rng.uniform(-np.pi, np.pi, (n, 1))], 1)
+    cmd = LV(a[:, :3], a[:, 3]) if cfg.command_type == "lv" else CTBR(a[:, 0] + 9.81, a[:, 1:])
+    if cfg.command_type != "lv":
+        a = np.concatenate([a[:, :1] + 9.81, a[:, 1:]], 1)
+    t = time.perf_counter()
+    res = env.step(cmd)
+    torch.cuda.synchronize()
+    sample = np.sort(rng.choice(n, size=min(512, n), replace=False))
+    rep = env_step_parity(env, cfg, res.observations, a, oracle_scenes(cfg), (QuadParams(), SimConfig(), ControllerGains()),
+                          sample)
+    keep = ("flags_equal", "flag_mismatches", "nearest_equal", "reward_equal", "state_err_max", "state_err_p99",
+            "envs_over_1e-5", "over_1e-5_explained", "over_1e-5_unexplained", "render")
+    out = {k: rep[k] for k in keep if k in rep}
+    out["envs"] = n
+    out["checker"] = "CPU oracle (oracle/parity.py) on the GPU's own states, one extra untimed step"
+    out["seconds"] = time.perf_counter() - t
+    return out
+
+
+def sustained_leg(args, rank, world, line, seconds=5.0):
+    """>= 5 s of steady-state device-timed steps with the clock
+    sampler running: the long-run value beside the short headline window."""
+    import torch
+
+    import paper_2407_14783_b200._native as nat
+
+    r = line["_r"]
+    env = r["env"]
+    K = max(10, int(math.ceil(seconds * 1e3 / max(line["ms_per_step"], 1e-3))))
+    a = make_actions("c3", env.num_agents, 8, rank)
+
+    def launch(i):
+        env._bufs.action = a[i % 8].data_ptr()
+        nat.check(nat.lib().qb_env_step(env._P, env._kind, env._task, env.dev_scenes.handle, env._bufs, nat.stream_of()))
+        env._render()
+        env._observe()
+
+    torch.cuda.synchronize()
+    barrier(world)
+    clk = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")) if not SHARE_GPU else 0)
+    clk.start()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for i in range(K):
+        launch(i)
+    t1.record()
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    ms = max_over_ranks(t0.elapsed_time(t1), world)
+    return {"value": r["total"] * K / (ms / 1e3), "unit": "env-steps/s", "steps": K, "seconds": ms / 1e3,
+            "ms_per_step": ms / K, "clocks": clocks}
+
+
+def sub_args(args, kind, steps):
+    ns = argparse.Namespace(**vars(args))
+    ns.workload, ns.steps, ns.warmup = kind, steps, max(args.warmup, 3)
+    return ns
+
+
+def strip(d):
+    return {k: v for k, v in d.items() if not k.startswith("_")}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -568,6 +735,8 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
     ap.add_argument("--no-cpu", dest="cpu", action="store_false")
+    ap.add_argument("--no-sub", dest="sub", action="store_false",
+                    help="config 3 only: skip the config 1/2/4/5 sub-records, the parity and the sustained legs")
     ap.add_argument("--strong", action="store_true", help="c4: fixed 16384 envs in total (strong scaling)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -584,86 +753,37 @@ def main():
     pk, pk_kind = peaks()
     line = {"metric": METRIC, "unit": "env-steps/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (procedurally generated scenes, seeded actions); no datasets offline"}
+            "data": "synthetic (procedurally generated scenes, seeded actions); no datasets offline",
+            "peaks_source": pk_kind}
     if kind == "c4":
-        r = run_bptt(args, rank, world)
-        steps_total = r["n"] * r["T"] * world * args.steps
-        line["scaling"] = "strong" if args.strong else "weak"
-        line.update({"metric": "BPTT env-steps/sec (forward + adjoint), whole box", "value": steps_total / (r["ms"] / 1e3),
-                     "ms_per_step": r["ms"] / args.steps, "clocks": r["clocks"], "gpu_launches": 2 * args.steps,
-                     "config": {"workload": WORKLOADS[kind], "envs_per_gpu": r["n"], "horizon": r["T"],
-                                "parallelism": f"env shards x{world}, all_reduce(SUM) of loss + shared action grad"},
-                     "kernel_ms": {"rollout_forward": r["fwd_ms"], "rollout_backward": r["bwd_ms"]}})
-        fwd_b, bwd_b = 152 + 68, 236  # algorithmic B/env-step (tape write, tape/action read, grad write)
-        gbs = r["n"] * r["T"] * (fwd_b + bwd_b) / ((r["fwd_ms"] + r["bwd_ms"]) / 1e3) / 1e9
-        line["roofline"] = {"bound": "hbm", "achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                            "frac": gbs / pk["hbm_gbs"], "traffic": None,
-                            "note": "forward+adjoint, (220+236) algorithmic B/env-step"}
-        if rank == 0 and args.cpu:
-            v, dt = cpu_baseline_bptt()
-            line["cpu_baseline"] = {"value": v, "unit": "env-steps/s", "cores": 1, "kind": "port",
-                                    "sample": f"8 agents x H=64 oracle rollout_grad ({dt:.1f} s)"}
+        line.update(bptt_line(args, rank, world, pk, cpu=args.cpu))
     else:
-        r = run_env(args, rank, world, kind)
-        value = r["total"] * args.steps / (r["ms"] / 1e3)
-        line.update({"value": value, "ms_per_step": r["ms"] / args.steps, "clocks": r["clocks"],
-                     "gpu_launches": r["launches"],
-                     "config": {"workload": WORKLOADS[kind], "envs_per_gpu": r["n"], "global_envs": r["total"],
-                                "resolution": "64x64", "integrator": "rk4, 2 substeps",
-                                "sensors": ",".join(f"{s.name}:{s.kind}" for s in r["cfg"].sensors) or "none",
-                                "l2": "per-step output (depth+seg, 2.1 GB at c3) >> 126 MB L2; no flush needed"
-                                if not r["graph"] else "100 envs: latency-bound; 10 env steps per CUDA-graph replay "
-                                                       "(actions staged by device copies inside the timed region)",
-                                "parallelism": f"env shards x{world}, no per-step collective"}})
-        if "render_ms" in r:
-            line["kernel_ms"] = {"env_step_k1k3": r["step_ms"], "render_k2": r["render_ms"]}
-            if "observe_ms" in r:
-                line["kernel_ms"]["observe_imu_noise"] = r["observe_ms"]
-            px = r["n"] * 64 * 64
-            nbytes = px * sum(4 for s in r["cfg"].sensors) + r["n"] * 40  # outputs + pose reads
-            gbs = nbytes / (r["render_ms"] / 1e3) / 1e9
-            traffic, meta = profile_traffic("k_render_cull" if kind != "c5" else "k_render_f")
-            line["roofline"] = {
-                "bound": "hbm", "achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": gbs / pk["hbm_gbs"],
-                "traffic": traffic * r["n"] if traffic else None,
-                "note": (f"dominant kernel K2 render ({r['render_ms']:.3f} of {r['ms'] / args.steps:.3f} ms/step): "
-                         f"algorithmic bytes = depth+seg writes + pose reads; the kernel is SM-issue-bound "
-                         f"(see profiles/ncu_summary.json), peak = {pk_kind} HBM copy bandwidth"),
-                # the renderer's own figures: rays/s of the kernel and its SM / cache counters (ncu)
-                "rays_per_s": r["n"] * 64 * 64 / (r["render_ms"] / 1e3),
-                "ncu": {k: meta[k] for k in ("issue_active_pct", "warps_active_pct", "l1_hit_pct", "l2_hit_pct",
-                                             "registers", "source") if k in meta} if meta else None}
-            # the renderer's real bound: SM instruction issue.  Peak = 148 SMs x 4 schedulers x
-            # the SM clock seen under load; achieved = ncu's warp-instructions per camera x cameras / kernel time.
-            # Beside it, the reference algorithm's op count per ray (its BVH traversal counts)
-            # x rays/s against the FP32 lane peak: above 1 means culling removed work the reference does.
-            mhz = (r["clocks"] or {}).get("sm_mhz") or 1965.0
-            if meta and meta.get("warp_instructions_per_unit"):
-                wips = meta["warp_instructions_per_unit"] * r["n"] / (r["render_ms"] / 1e3)
-                peak_wi = 148 * 4 * mhz * 1e6
-                ref_ops = 4360.0 if kind == "c5" else 1470.0
-                rays = r["n"] * 64 * 64 / (r["render_ms"] / 1e3)
-                line["roofline_render_issue"] = {
-                    "bound": "issue", "achieved": wips, "peak": peak_wi, "unit": "warp-instr/s",
-                    "frac": wips / peak_wi,
-                    "reference_ops_per_ray": ref_ops,
-                    "reference_equiv_frac": rays * ref_ops / (148 * 128 * mhz * 1e6),
-                    "note": "warp-instructions per camera from the committed ncu capture (profiles/ncu_summary.json) "
-                            "x cameras / live kernel time; peak at the SM clock sampled during the timed region"}
+        body = env_line(kind, args, rank, world, pk, cpu=args.cpu, e2e=args.e2e)
+        line.update(body)
+        line["steps"] = args.steps
         if rank == 0:
             line["roofline_dynamics"] = run_dynamics_roofline(pk)
             line["roofline_env_step"] = run_env_step_roofline(pk)
-            if args.cpu:
-                ns = {"c5": 64, "c3n": 256, "swarm": 256}.get(kind, min(1024, ENVS[kind]))
-                steps = {"c5": 2, "swarm": 4}.get(kind, 12 if ns > 100 else 400)
-                v, dt = cpu_baseline_env(kind, n_sample=ns, steps=steps)
-                line["cpu_baseline"] = {"value": v, "unit": "env-steps/s", "cores": os.cpu_count(), "kind": "port",
-                                        "sample": f"{ns} envs x {steps} steps of the same env step on the C oracle "
-                                                  f"(OpenMP), {dt:.1f} s"}
-        if "e2e" in r:
-            line["e2e"] = r["e2e"]
+        if kind == "c3" and args.sub:
+            line["sustained"] = sustained_leg(args, rank, world, body)
+            if rank == 0:
+                line["parity"] = parity_leg(body, kind)
+    if kind == "c3" and args.sub:
+        # every other BASELINE config as a sub-record (same contract keys), so the
+        # driver's default run carries each config's number, e2e and CPU baseline
+        del body["_r"]["env"]
+        body["_r"] = None
+        torch.cuda.empty_cache()
+        subs = {}
+        for sk, st in (("c1", 200), ("c2", 100), ("c5", 10)):
+            sl = env_line(sk, sub_args(args, sk, st), rank, world, pk, cpu=args.cpu, e2e=args.e2e)
+            sl["_r"] = None
+            subs[sk] = strip(sl)
+            torch.cuda.empty_cache()
+        subs["c4"] = bptt_line(sub_args(args, "c4", 10), rank, world, pk, cpu=args.cpu)
+        line["configs"] = subs
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        print(json.dumps(strip(line)), flush=True)
     barrier(world)
     if world > 1:
         import torch.distributed as dist

@@ -291,6 +291,58 @@ typedef struct qb_sensor_obs {
 int qb_env_observe(const qb_params *p, const qb_env_buffers *b, int32_t n_sensors, const qb_sensor_obs *sensors,
                    void *stream);
 
+/* ------------------------------------------------- flat-array host bindings */
+
+/* The SPEC's "bindings" module (reset(handle, seed) /
+ * step(handle, actions N x 4) -> (FlatObservation, rewards, terminated,
+ * truncated, info), flat arrays across the boundary, freshly owned results):
+ * one call runs a whole env step from HOST actions to HOST results.  It is
+ * the one entry point that takes host buffers and may synchronise. */
+
+/* One camera render of the step: DEVICE outputs (either may be NULL). */
+typedef struct qb_io_view {
+    qb_camera cam;
+    void *depth;        /* (n,H,W) dtype */
+    int32_t *seg;       /* (n,H,W) int32 object ids */
+    uint8_t *seg_u8;    /* optional (n,H,W) uint8 copy of seg for the host (ids < 256: lossless) */
+    int32_t centroid_id, pad_;
+    float *centroid;    /* (n,2) when centroid_id > 0 */
+} qb_io_view;
+
+/* One byte copy: a DEVICE -> DEVICE gather (packs) or DEVICE -> HOST copy (copies). */
+typedef struct qb_io_copy {
+    const void *src;
+    void *dst;
+    int64_t bytes;
+} qb_io_copy;
+
+#define QB_IO_MAX_PACKS 8
+
+typedef struct qb_step_io {
+    int32_t step;             /* 1: step the env with host_action first; 0: observe only (after reset) */
+    int32_t sync;             /* 1: return after the copies completed (stream synchronised) */
+    const void *host_action;  /* (n,4) dtype, HOST: pinned memory is read in place by the step kernel,
+                                 pageable memory is first copied into b->action (DEVICE) */
+    void *state_rows;         /* (n,13) dtype state observation rows (base.py:234-243), or NULL; DEVICE or
+                                 pinned HOST memory (written through its device mapping) */
+    int32_t n_views, n_copies;
+    const qb_io_view *views;
+    const qb_io_copy *copies; /* DEVICE -> HOST, in order */
+    int32_t n_sensors, n_packs;
+    const qb_sensor_obs *sensors; /* noise / IMU pass (qb_env_observe) after the renders, or NULL */
+    const qb_io_copy *packs;  /* <= QB_IO_MAX_PACKS small gathers done by the same kernel as the
+                                 state rows, from DEVICE to DEVICE or to pinned HOST memory (then
+                                 the small results reach the host without any copy operation) */
+} qb_step_io;
+
+/* QuadEnvBase.step (base.py:156-210) + get_observation (:287-310) from host
+ * actions to host results: H2D of the actions, the fused env step
+ * (qb_env_step), every view's render, the sensor pass, one pack kernel (state
+ * rows + gathers), the uint8 segmentation copies, then the D2H copies.  Not
+ * for swarm tasks. */
+int qb_env_step_io(const qb_params *p, int32_t cmd_kind, const qb_task *task, const qb_scene *s,
+                   const qb_env_buffers *b, const qb_step_io *io, void *stream);
+
 /* numpy.random.default_rng(seed + i) seeding for i in [0,n): out (n,4). */
 int qb_rng_seed(uint64_t seed, int64_t n, uint64_t *out, void *stream);
 /* n draws of next_double from each stream (testing hook): out (n, k). */

@@ -52,9 +52,19 @@ def _axis_rot(axis, ang):
     return np.eye(3) + np.sin(ang) * K + (1 - np.cos(ang)) * K @ K
 
 
-def grazing_mask(scene, origins, rotations, width, height, th, tv, max_range, d_o=1e-5, d_r=3e-6):
-    """Pixels whose oracle result changes under pose / ray perturbations a few
-    times larger than FP32 rounding.  Returns (mask, depth0, ids0)."""
+def grazing_mask(scene, origins, rotations, width, height, th, tv, max_range, d_o=1e-5, d_r=3e-6, cam_rot=None,
+                 d_q=4e-7):
+    """Pixels whose oracle result is unstable under perturbations a few times
+    larger than the FP32 error of the pose: origin shifts
+    (d_o ~ 20x the FP32 rounding of a position at 5 m), rigid rotations of
+    the ray bundle (d_r), and -- with cam_rot, the camera's body mount -- a
+    change of the quaternion's norm by d_q (a few FP32 ulps of |q|^2).  The
+    last one matters because the reference builds the camera rotation from a
+    non-unit quaternion (quatmath.to_matrix: I + s^2 (R - I) for q = s q_hat)
+    and its sphere test assumes a unit ray direction (kernels.py:185-201:
+    disc = b^2 - c, no |d|^2 term): near a sphere's rim the depth moves by
+    ~ (b^2 / sqrt(disc)) * (|q|^2 - 1), i.e. 1e-4 m for |q|^2 - 1 = 1e-7, the
+    FP32 rounding level of the stored state.  Returns (mask, depth0, ids0)."""
     depth0, ids0 = scene.render(origins, rotations, width, height, th, tv, max_range)
     mask = np.zeros(depth0.shape, bool)
     perts = []
@@ -67,6 +77,10 @@ def grazing_mask(scene, origins, rotations, width, height, th, tv, max_range, d_
         for s in (-1.0, 1.0):
             R = _axis_rot(ax, s * d_r)
             perts.append((origins, np.einsum("ij,njk->nik", R, rotations)))
+    if cam_rot is not None:  # rotations = to_matrix(q) @ cam_rot: scale to_matrix(q) - I by (1 +- d_q)
+        dev = rotations - np.asarray(cam_rot, float)[None]
+        for s in (-1.0, 1.0):
+            perts.append((origins, np.ascontiguousarray(rotations + s * d_q * dev)))
     for o, r in perts:
         d, i = scene.render(o, r, width, height, th, tv, max_range)
         mask |= (i != ids0) | (np.abs(d - depth0) > DEPTH_TOL)
@@ -224,7 +238,8 @@ def env_step_parity(env, cfg, obs, action, oscenes, P, sample, *, check_render=T
         cam = specs[0][1]
         o_, r_ = camera_pose_world(st[sample, 0:3], st[sample, 6:10], cam.rotation, cam.translation)
         if graze:
-            graz, d0, i0 = grazing_mask(sc, o_, r_, cam.width, cam.height, cam.tan_half_h, cam.tan_half_v, cam.max_range)
+            graz, d0, i0 = grazing_mask(sc, o_, r_, cam.width, cam.height, cam.tan_half_h, cam.tan_half_v, cam.max_range,
+                                        cam_rot=cam.rotation)
         else:
             d0, i0 = sc.render(o_, r_, cam.width, cam.height, cam.tan_half_h, cam.tan_half_v, cam.max_range)
             graz = np.zeros(d0.shape, bool)
@@ -244,12 +259,16 @@ def env_step_parity(env, cfg, obs, action, oscenes, P, sample, *, check_render=T
         n_graz += int(graz.sum())
         ng = bad_any & ~graz
         n_bad_ng += int(ng.sum())
-        if ng.any() and "first_non_grazing" not in out:
-            k, i, j = (int(v) for v in np.argwhere(ng)[0])
-            det = {"camera": int(sample[k]), "pixel": [i, j], "ref_depth": float(d0[k, i, j]), "ref_id": int(i0[k, i, j])}
-            for spec, _ in specs:
-                det[spec.name] = float(_as_np(obs[spec.name][int(sample[k]), i, j]))
-            out["first_non_grazing"] = det
+        if ng.any():
+            lst = out.setdefault("non_grazing_detail", [])
+            for k, i, j in np.argwhere(ng)[:max(0, 16 - len(lst))]:
+                k, i, j = int(k), int(i), int(j)
+                det = {"camera": int(sample[k]), "pixel": [i, j], "ref_depth": float(d0[k, i, j]),
+                       "ref_id": int(i0[k, i, j]), "cam_pos": [float(x) for x in o_[k]]}
+                for spec, _ in specs:
+                    det[spec.name] = float(_as_np(obs[spec.name][int(sample[k]), i, j]))
+                lst.append(det)
+            out.setdefault("first_non_grazing", lst[0])
         if cfg.task == "landing" and "target" in obs:  # pad centroid target (tasks.py:121-128)
             tgt = _as_np(obs["target"][torch_index(obs["target"], sample)])
             for k in range(len(sample)):

@@ -165,6 +165,39 @@ class QbSensorObs(ctypes.Structure):
     ]
 
 
+class QbIoView(ctypes.Structure):
+    _fields_ = [
+        ("cam", QbCamera),
+        ("depth", _P),
+        ("seg", _P),
+        ("seg_u8", _P),
+        ("centroid_id", ctypes.c_int32),
+        ("pad_", ctypes.c_int32),
+        ("centroid", _P),
+    ]
+
+
+class QbIoCopy(ctypes.Structure):
+    _fields_ = [("src", _P), ("dst", _P), ("bytes", ctypes.c_int64)]
+
+
+class QbStepIo(ctypes.Structure):
+    _fields_ = [
+        ("step", ctypes.c_int32),
+        ("sync", ctypes.c_int32),
+        ("host_action", _P),
+        ("state_rows", _P),
+        ("n_views", ctypes.c_int32),
+        ("n_copies", ctypes.c_int32),
+        ("views", _P),
+        ("copies", _P),
+        ("n_sensors", ctypes.c_int32),
+        ("n_packs", ctypes.c_int32),
+        ("sensors", _P),
+        ("packs", _P),
+    ]
+
+
 # exported symbol -> (argtypes, restype)
 _I64, _I32, _U64, _D = ctypes.c_int64, ctypes.c_int32, ctypes.c_uint64, ctypes.c_double
 _PP = ctypes.POINTER
@@ -198,6 +231,7 @@ SIGNATURES = {
     "qb_rng_normals": ([_I64, _P, _I32, _P, _P], ctypes.c_int),
     "qb_rng_poissons": ([_I64, _P, _I32, _P, _P, _P], ctypes.c_int),
     "qb_env_observe": ([_PP(QbParams), _PP(QbEnvBuffers), _I32, _P, _P], ctypes.c_int),
+    "qb_env_step_io": ([_PP(QbParams), _I32, _PP(QbTask), _P, _PP(QbEnvBuffers), _PP(QbStepIo), _P], ctypes.c_int),
 }
 
 _lib = None

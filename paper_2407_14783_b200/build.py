@@ -64,8 +64,21 @@ def build(force: bool = False, verbose: bool = False, extra_flags=()) -> str:
     cc = nvcc()
     hostc = _host_compiler_flags()
 
+    # a translation unit is recompiled when it, a header or this script is newer
+    # than its object (or always, with extra flags: tuning builds)
+    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if not f.endswith(".cu")]
+    headers += [os.path.join(INCLUDE, f) for f in os.listdir(INCLUDE)] + [os.path.abspath(__file__)]
+    common = max(os.path.getmtime(f) for f in headers)
+    stamp = os.path.join(OBJ, "flags.txt")  # objects of a tuning build (-D ...) are never reused by another build
+    flags_now = " ".join(extra_flags)
+    if not os.path.exists(stamp) or open(stamp).read() != flags_now:
+        force = True
+
     def compile_one(src):
         obj = os.path.join(OBJ, src.replace(".cu", ".o"))
+        if (not force and os.path.exists(obj)
+                and os.path.getmtime(obj) >= max(common, os.path.getmtime(os.path.join(CSRC, src)))):
+            return obj
         cmd = [cc, *ARCH, *NVCC_FLAGS, *hostc, *extra_flags, "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:
             print(" ".join(cmd), flush=True)
@@ -78,6 +91,8 @@ def build(force: bool = False, verbose: bool = False, extra_flags=()) -> str:
 
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
         objs = list(ex.map(compile_one, sources()))
+    with open(stamp, "w") as f:
+        f.write(flags_now)
     tmp = LIB + ".tmp"
     cmd = [cc, *ARCH, *hostc, "-shared", "-cudart", "static", "-o", tmp, *objs]
     if verbose:

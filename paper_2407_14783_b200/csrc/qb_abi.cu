@@ -567,6 +567,92 @@ int qb_env_observe(const qb_params *p, const qb_env_buffers *b, int32_t n_sensor
     return qb::launch_observe(p, b, n_sensors, sensors, qb::as_stream(stream));
 }
 
+int qb_env_step_io(const qb_params *p, int32_t cmd_kind, const qb_task *task, const qb_scene *s,
+                   const qb_env_buffers *b, const qb_step_io *io, void *stream) {
+    QB_REQUIRE(p && io, "qb_env_step_io: NULL argument");
+    int rc = check_env(task, s, b);
+    if (rc) return rc;
+    QB_REQUIRE(!task->swarm, "qb_env_step_io: swarm tasks are not supported by the flat bindings");
+    QB_REQUIRE(io->n_views >= 0 && (io->views || io->n_views == 0), "qb_env_step_io: bad views");
+    QB_REQUIRE(io->n_copies >= 0 && (io->copies || io->n_copies == 0), "qb_env_step_io: bad copies");
+    QB_REQUIRE(io->n_sensors >= 0 && (io->sensors || io->n_sensors == 0), "qb_env_step_io: bad sensors");
+    for (int v = 0; v < io->n_views; ++v) {
+        rc = check_cam(&io->views[v].cam);
+        if (rc) return rc;
+        QB_REQUIRE(io->views[v].centroid_id <= 0 || io->views[v].centroid, "qb_env_step_io: centroid buffer missing");
+        QB_REQUIRE(!io->views[v].seg_u8 || io->views[v].seg, "qb_env_step_io: seg_u8 needs seg");
+    }
+    for (int c = 0; c < io->n_copies; ++c)
+        QB_REQUIRE(io->copies[c].bytes >= 0 && (io->copies[c].bytes == 0 || (io->copies[c].src && io->copies[c].dst)),
+                   "qb_env_step_io: bad copy %d", c);
+    QB_REQUIRE(io->n_packs >= 0 && io->n_packs <= QB_IO_MAX_PACKS && (io->packs || io->n_packs == 0),
+               "qb_env_step_io: bad packs (max %d)", QB_IO_MAX_PACKS);
+    for (int c = 0; c < io->n_packs; ++c)
+        QB_REQUIRE(io->packs[c].bytes >= 0 && (io->packs[c].bytes == 0 || (io->packs[c].src && io->packs[c].dst)),
+                   "qb_env_step_io: bad pack %d", c);
+    cudaStream_t st = qb::as_stream(stream);
+    const size_t es = b->dtype == QB_F32 ? 4 : 8;
+    if (io->step) {
+        QB_REQUIRE(io->host_action && b->action, "qb_env_step_io: host_action and the device action buffer are required");
+        // pinned (page-locked) host actions are read by the step kernel itself
+        // through their device mapping (one 16 B load per env over PCIe) instead
+        // of a separate H2D copy; pageable ones are copied into b->action
+        qb_env_buffers bb = *b;
+        cudaPointerAttributes attr;
+        if (cudaPointerGetAttributes(&attr, io->host_action) == cudaSuccess && attr.type == cudaMemoryTypeHost &&
+            attr.devicePointer) {
+            bb.action = attr.devicePointer;
+        } else {
+            cudaGetLastError();  // (an unregistered pointer is not an error here)
+            cudaError_t e = cudaMemcpyAsync(const_cast<void *>(b->action), io->host_action, (size_t)b->n * 4 * es,
+                                            cudaMemcpyHostToDevice, st);
+            if (e != cudaSuccess) {
+                qb::set_error("qb_env_step_io: action copy: %s", cudaGetErrorString(e));
+                return QB_ECUDA;
+            }
+        }
+        rc = qb::launch_env(1, p, cmd_kind, task, s, &bb, 0, st);
+        if (rc) return rc;
+    }
+    for (int v = 0; v < io->n_views; ++v) {
+        const qb_io_view &vw = io->views[v];
+        rc = qb::launch_render(s, &vw.cam, b->dtype, b->n, b->ld, b->state, nullptr, nullptr, b->agent_scene, vw.depth,
+                               vw.seg, vw.centroid_id, vw.centroid, nullptr, nullptr, 0, st);
+        if (rc) return rc;
+    }
+    if (io->n_sensors) {
+        rc = qb::launch_observe(p, b, io->n_sensors, io->sensors, st);
+        if (rc) return rc;
+    }
+    if (io->state_rows || io->n_packs) {
+        rc = qb::launch_io_pack(b->dtype, b->n, b->ld, b->state, io->state_rows, io->n_packs, io->packs, st);
+        if (rc) return rc;
+    }
+    for (int v = 0; v < io->n_views; ++v) {
+        const qb_io_view &vw = io->views[v];
+        if (!vw.seg_u8) continue;
+        rc = qb::launch_narrow_u8((long long)b->n * vw.cam.width * vw.cam.height, vw.seg, vw.seg_u8, st);
+        if (rc) return rc;
+    }
+    for (int c = 0; c < io->n_copies; ++c) {
+        const qb_io_copy &cp = io->copies[c];
+        if (!cp.bytes) continue;
+        cudaError_t e = cudaMemcpyAsync(cp.dst, cp.src, (size_t)cp.bytes, cudaMemcpyDeviceToHost, st);
+        if (e != cudaSuccess) {
+            qb::set_error("qb_env_step_io: result copy %d: %s", c, cudaGetErrorString(e));
+            return QB_ECUDA;
+        }
+    }
+    if (io->sync) {
+        cudaError_t e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) {
+            qb::set_error("qb_env_step_io: %s", cudaGetErrorString(e));
+            return QB_ECUDA;
+        }
+    }
+    return QB_OK;
+}
+
 int qb_rng_seed(uint64_t seed, int64_t n, uint64_t *out, void *stream) {
     QB_REQUIRE(out && n >= 0, "qb_rng_seed: bad arguments");
     return qb::launch_rng_seed(seed, n, out, qb::as_stream(stream));

@@ -82,4 +82,7 @@ int launch_rng_normals(long long n, uint64_t *rng, int k, double *out, cudaStrea
 int launch_rng_poissons(long long n, uint64_t *rng, int k, const double *lam, int64_t *out, cudaStream_t st);
 int launch_observe(const qb_params *p, const qb_env_buffers *b, int n_sensors, const qb_sensor_obs *sensors,
                    cudaStream_t st);
+int launch_io_pack(int dtype, long long n, long long ld, const void *planes, void *rows, int n_packs,
+                   const qb_io_copy *packs, cudaStream_t st);
+int launch_narrow_u8(long long count, const int32_t *seg, uint8_t *out, cudaStream_t st);
 }  // namespace qb

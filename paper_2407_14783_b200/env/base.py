@@ -441,6 +441,11 @@ class QuadEnvBase:
     # ------------------------------------------------------------------ reset / step
     def reset(self, seed: int = 0) -> Observations:
         """Fresh initial states for every agent; deterministic per seed (base.py:93-112)."""
+        self._reset_state(seed)
+        return self.get_observation()
+
+    def _reset_state(self, seed: int):
+        """reset() without the observation: scene permutation, spawns, proximity."""
         import torch
 
         s = len(self.scenes)
@@ -455,7 +460,6 @@ class QuadEnvBase:
             raise SpawnFailure(f"{nfail} agents: no spawn with clearance >= {self.config.min_spawn_clearance} in 1000 attempts")
         self._reset_done = True
         self._pending_errors = None
-        return self.get_observation()
 
     def _stage_action(self, action):
         import torch

@@ -1,0 +1,135 @@
+"""Flat-array bindings: one native call per step
+(qb_env_step_io) from host actions to host arrays.  The results must equal
+the batched env's (env.step) bit for bit on the same seed and actions --
+states, images (uint8 segmentation = the int32 ids), rewards, flags, info --
+over episodes with respawns; every step's arrays are freshly owned; the
+handle's error behaviour follows the SPEC."""
+
+import dataclasses
+
+import numpy as np
+import pytest
+
+from paper_2407_14783_b200 import bindings
+from paper_2407_14783_b200.control import CTBR, LV
+from paper_2407_14783_b200.env import EnvConfig, SensorSpec, landing_config, make_env, navigation_config
+from paper_2407_14783_b200.errors import ActionShapeMismatch, NotReset
+from paper_2407_14783_b200.sensing import NoiseSpec
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+def _cfgs():
+    nav = dataclasses.replace(navigation_config(0, 100, with_segmentation=True), episode_max_steps=40)
+    noisy = dataclasses.replace(nav, sensors=(
+        SensorSpec(kind="depth", name="depth", noise=(NoiseSpec("normal", sigma=0.02),)),
+        SensorSpec(kind="segmentation", name="segmentation", noise=(NoiseSpec("saltpepper", p=0.02),)),
+        SensorSpec(kind="imu", name="imu", noise=(NoiseSpec("normal", sigma=0.05),))))
+    return {"hover": EnvConfig(num_agents=100, command_type="ctbr", episode_max_steps=30),
+            "nav": nav, "nav_big": dataclasses.replace(nav, num_agents=12000),
+            "landing": dataclasses.replace(landing_config(64), episode_max_steps=30), "noisy": noisy}
+
+
+def _actions(cfg, n, rng):
+    if cfg.command_type == "ctbr":
+        a = np.concatenate([rng.uniform(5, 15, (n, 1)), rng.normal(size=(n, 3))], 1)
+        return a.astype(np.float32), lambda x: CTBR(x[:, 0], x[:, 1:])
+    a = np.concatenate([rng.normal(scale=2.0, size=(n, 3)), rng.uniform(-3, 3, (n, 1))], 1)
+    return a.astype(np.float32), lambda x: LV(x[:, :3], x[:, 3])
+
+
+@pytest.mark.parametrize("name,pinned", [("hover", False), ("hover", True), ("nav", False), ("nav", True),
+                                         ("nav_big", False), ("landing", True), ("noisy", False)])
+def test_bindings_equal_env_step(name, pinned):
+    """pinned: actions from page-locked memory (read in place by the step
+    kernel) and results into a reused pinned set (small results written by
+    the pack kernel straight into host memory)."""
+    cfg = _cfgs()[name]
+    h = bindings.make_env(cfg)
+    out = h.outputs() if pinned else None
+    a_pin = torch.zeros((cfg.num_agents, 4), pin_memory=True).numpy() if pinned else None
+    ref = make_env(cfg)
+    ref.split_step = False
+    o_h = bindings.reset(h, seed=3)
+    o_r = ref.reset(seed=3)
+    torch.cuda.synchronize()
+    assert np.array_equal(o_h["state"], o_r["state"].cpu().numpy())
+    n = cfg.num_agents
+    rng = np.random.default_rng(0)
+    kept = []
+    for t in range(45):
+        a, cmd = _actions(cfg, n, rng)
+        if pinned:
+            a_pin[:] = a
+        obs, rew, term, trunc, info = bindings.step(h, a_pin if pinned else a, out=out)
+        r = ref.step(cmd(torch.as_tensor(a, device="cuda")))
+        torch.cuda.synchronize()
+        assert np.array_equal(obs["state"], r.observations["state"].cpu().numpy()), (t, "state")
+        for k in obs.keys():
+            if k == "state":
+                continue
+            want = r.observations[k]
+            want = want.cpu().numpy() if hasattr(want, "cpu") else np.asarray(want)
+            got = obs[k]
+            assert got.shape == want.shape, (t, k)
+            if got.dtype == np.uint8:
+                assert want.max() < 256
+            assert np.array_equal(got.astype(want.dtype), want), (t, k)
+        assert np.array_equal(rew, r.reward.cpu().numpy()), t
+        assert np.array_equal(term, r.terminated.cpu().numpy()), t
+        assert np.array_equal(trunc, r.truncated.cpu().numpy()), t
+        for k in ("success", "collision", "out_of_bounds", "nonfinite", "nearest_distance", "scene", "step"):
+            assert np.array_equal(info[k], r.info[k].cpu().numpy()), (t, k)
+        if not pinned:
+            kept.append((obs["state"].copy(), obs["state"], rew.copy(), rew))
+    # freshly owned arrays: later steps never changed earlier results
+    for snap, live, rsnap, rlive in kept:
+        assert np.array_equal(snap, live) and np.array_equal(rsnap, rlive)
+    assert int(ref.step_counts.max()) < 45  # episodes ended and respawned along the way
+    bindings.close(h)
+
+
+def test_bindings_pinned_outputs_and_layout():
+    cfg = _cfgs()["nav"]
+    h = bindings.make_env(cfg)
+    out = h.outputs()
+    o = bindings.reset(h, seed=1, out=out)
+    assert o["segmentation"].dtype == np.uint8  # nav ids < 256: lossless narrow
+    assert np.shares_memory(o["state"], out["_small"])
+    rng = np.random.default_rng(1)
+    a, _ = _actions(cfg, cfg.num_agents, rng)
+    obs, rew, term, trunc, info = bindings.step(h, a, out=out)
+    assert obs["depth"] is out["depth"]  # written in place, no allocation
+    for k, (shape, dt) in obs.layout.items():
+        assert obs[k].shape == tuple(shape) and obs[k].dtype == np.dtype(dt), k
+
+
+def test_bindings_errors():
+    cfg = _cfgs()["hover"]
+    h = bindings.make_env(cfg)
+    with pytest.raises(NotReset):
+        bindings.step(h, np.zeros((100, 4), np.float32))
+    bindings.reset(h, 0)
+    with pytest.raises(ActionShapeMismatch):
+        bindings.step(h, np.zeros((99, 4), np.float32))
+    h._lock.acquire()  # another caller holds the handle
+    try:
+        with pytest.raises(bindings.HandleBusy):
+            bindings.step(h, np.zeros((100, 4), np.float32))
+    finally:
+        h._lock.release()
+    bindings.close(h)
+    with pytest.raises(bindings.HandleClosed):
+        bindings.step(h, np.zeros((100, 4), np.float32))
+    # two handles are independent (SPEC.md: cross-check trajectories)
+    h1, h2 = bindings.make_env(cfg), bindings.make_env(cfg)
+    bindings.reset(h1, 4), bindings.reset(h2, 4)
+    a = np.tile(np.array([[9.81, 0.1, -0.2, 0.0]], np.float32), (100, 1))
+    for _ in range(3):
+        s1 = bindings.step(h1, a)[0]["state"]
+    s2 = bindings.step(h2, a)[0]["state"]
+    assert not np.array_equal(s1, s2)
+    for _ in range(2):
+        s2 = bindings.step(h2, a)[0]["state"]
+    assert np.array_equal(s1, s2)

@@ -111,7 +111,9 @@ def test_ctypes_struct_layouts_match_c():
     prog = ("#include <stdio.h>\n#include <stddef.h>\n#include \"quadb200.h\"\n"
             "int main(){printf(\"%zu %zu %zu %zu %zu %zu %zu %zu %zu %zu\\n\", sizeof(qb_params), sizeof(qb_task),"
             " sizeof(qb_env_buffers), sizeof(qb_camera), sizeof(qb_dist), offsetof(qb_params, substeps),"
-            " offsetof(qb_task, target), sizeof(qb_noise), sizeof(qb_sensor_obs), offsetof(qb_sensor_obs, src));}\n")
+            " offsetof(qb_task, target), sizeof(qb_noise), sizeof(qb_sensor_obs), offsetof(qb_sensor_obs, src));"
+            " printf(\"%zu %zu %zu %zu %zu\\n\", sizeof(qb_io_view), offsetof(qb_io_view, centroid), sizeof(qb_io_copy),"
+            " sizeof(qb_step_io), offsetof(qb_step_io, sensors));}\n")
     exe = "/tmp/qb_layout"
     cc = "/usr/bin/gcc" if os.path.exists("/usr/bin/gcc") else "gcc"
     r = subprocess.run([cc, "-x", "c", "-I", src, "-o", exe, "-"], input=prog, text=True, capture_output=True)
@@ -119,7 +121,9 @@ def test_ctypes_struct_layouts_match_c():
     got = [int(x) for x in subprocess.run([exe], capture_output=True, text=True).stdout.split()]
     want = [ctypes.sizeof(nat.QbParams), ctypes.sizeof(nat.QbTask), ctypes.sizeof(nat.QbEnvBuffers),
             ctypes.sizeof(nat.QbCamera), ctypes.sizeof(nat.QbDist), nat.QbParams.substeps.offset, nat.QbTask.target.offset,
-            ctypes.sizeof(nat.QbNoise), ctypes.sizeof(nat.QbSensorObs), nat.QbSensorObs.src.offset]
+            ctypes.sizeof(nat.QbNoise), ctypes.sizeof(nat.QbSensorObs), nat.QbSensorObs.src.offset,
+            ctypes.sizeof(nat.QbIoView), nat.QbIoView.centroid.offset, ctypes.sizeof(nat.QbIoCopy),
+            ctypes.sizeof(nat.QbStepIo), nat.QbStepIo.sensors.offset]
     assert got == want
 
 

@@ -1,8 +1,8 @@
-"""Condense the round's ncu captures (gpurun_out/r1_*.ncu-rep) into profiles/.
+"""Condense the round's ncu captures (gpurun_out/<round>_*.ncu-rep, QB_ROUND=r1|r2) into profiles/.
 
 profiles/ncu_summary.json  per-kernel figures bench.py quotes (DRAM bytes per
                            unit -> roofline "traffic"), one entry per kernel
-profiles/r1_ncu_raw_summary.json  the raw metric rows (scripts/ncu_summary.py)
+profiles/<round>_ncu_raw_summary.json  the raw metric rows (scripts/ncu_summary.py)
 """
 import json
 import os
@@ -15,14 +15,16 @@ from ncu_summary import read  # noqa: E402
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "gpurun_out")
 DEST = sys.argv[1] if len(sys.argv) > 1 else os.path.join(ROOT, "profiles")  # (on the GPU box: gpurun_out/prof)
+RND = os.environ.get("QB_ROUND", "r1")
+ROUND_TEXT = {"r1": "round 1", "r2": "round 2"}.get(RND, RND)
 CAPTURES = {  # report -> (kernel key, units in the captured launch, unit)
-    "r1_render_cull": ("k_render_cull", 16384, "camera (64x64, depth+seg), 69-prim nav room"),
-    "r1_render_bvh": ("k_render_f", 32768, "camera (64x64, down depth+seg), 5e5-tri hall"),
-    "r1_env_step": ("k_env_step", 65536, "env"),
-    "r1_dyn_step": ("k_dyn_step", 4194304, "env"),
-    "r1_bptt": (None, 16384 * 64, "env-step"),
-    "r1_observe": ("k_env_observe", 16384, "env (C3n sensor pass: depth N -> Redwood, seg salt-and-pepper, IMU)"),
-    "r1_env_big": ("k_env_step_4m", 4194304, "env (K1+K3 fused step, free flight, garage)"),
+    f"{RND}_render_cull": ("k_render_cull", 16384, "camera (64x64, depth+seg), 69-prim nav room"),
+    f"{RND}_render_bvh": ("k_render_f", 32768, "camera (64x64, down depth+seg), 5e5-tri hall"),
+    f"{RND}_env_step": ("k_env_step", 65536, "env"),
+    f"{RND}_dyn_step": ("k_dyn_step", 4194304, "env"),
+    f"{RND}_bptt": (None, 16384 * 64, "env-step"),
+    f"{RND}_observe": ("k_env_observe", 16384, "env (C3n sensor pass: depth N -> Redwood, seg salt-and-pepper, IMU)"),
+    f"{RND}_env_big": ("k_env_step_4m", 4194304, "env (K1+K3 fused step, free flight, garage)"),
 }
 
 
@@ -58,17 +60,17 @@ for rep, (key, units, unit) in CAPTURES.items():
             "l2_hit_pct": num(r["lts__t_sector_hit_rate.pct"]),
             "registers": num(r["launch__registers_per_thread"]),
             "warp_instructions_per_unit": num(r["smsp__inst_executed.sum"]) / units,
-            "source": f"{rep}.ncu-rep (ncu --set full --clock-control none, round 1)",
+            "source": f"{rep}.ncu-rep (ncu --set full --clock-control none, {ROUND_TEXT})",
         }
 os.makedirs(DEST, exist_ok=True)
 with open(os.path.join(DEST, "ncu_summary.json"), "w") as f:
     json.dump(summary, f, indent=1)
-with open(os.path.join(DEST, "r1_ncu_raw_summary.json"), "w") as f:
+with open(os.path.join(DEST, f"{RND}_ncu_raw_summary.json"), "w") as f:
     json.dump(raw, f, indent=1)
-if os.path.exists(os.path.join(OUT, "r1_launches.csv")):
-    shutil.copy(os.path.join(OUT, "r1_launches.csv"), os.path.join(DEST, "r1_launch_list.csv"))
+if os.path.exists(os.path.join(OUT, f"{RND}_launches.csv")):
+    shutil.copy(os.path.join(OUT, f"{RND}_launches.csv"), os.path.join(DEST, f"{RND}_launch_list.csv"))
 # per-line source tables of the two renderers (for reading back without the .ncu-rep)
-for rep in ("r1_render_cull", "r1_render_bvh", "r1_observe", "r1_env_big"):
+for rep in (f"{RND}_render_cull", f"{RND}_render_bvh", f"{RND}_observe", f"{RND}_env_big", f"{RND}_bptt"):
     path = os.path.join(OUT, rep + ".ncu-rep")
     if os.path.exists(path):
         import subprocess

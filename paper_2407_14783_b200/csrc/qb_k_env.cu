@@ -16,6 +16,7 @@
 // streams identical to default_rng(seed + i) (qb_rng.cuh).
 #include "qb_dynamics.cuh"
 #include "qb_geometry.cuh"
+#include "qb_checks.cuh"
 #include "qb_internal.h"
 #include "qb_rng.cuh"
 
@@ -105,6 +106,7 @@ __device__ bool spawn(const EnvArgs<R> &A, long long i, R *x, bool lead) {
     const long long gi = B.index_offset + i;
     const int rc = B.reset_count[i];
     const int scene = T.scene_perm[(int)((gi + rc) % T.n_scene_perm)];
+    QB_CHECK(scene >= 0 && scene < A.S.n_scenes, "spawn scene index");
     Pcg64 r = pcg_load(B.rng + 4 * i);
     if (WARP) __syncwarp();  // every lane has read the old values
     if (lead) {
@@ -261,6 +263,7 @@ template <class R, bool WARP> __global__ void __launch_bounds__(128) k_env_reset
         load_state(A, i, x);
     }
     if (mode == 3) return;  // swarm reset: spawns and proximity follow
+    QB_CHECK(B.agent_scene[i] >= 0 && B.agent_scene[i] < A.S.n_scenes, "env step scene index");
     const Proximity pr = proximity<R, WARP>(A, B.agent_scene[i], x);
     if (lead) write_post(A, i, pr);
 }

@@ -12,6 +12,7 @@
 // and thread per env (k_env_observe, chains with Poisson noise, whose draw
 // count per pixel depends on the value).
 #include "qb_dynamics.cuh"
+#include "qb_checks.cuh"
 #include "qb_internal.h"
 #include "qb_rng.cuh"
 

@@ -23,6 +23,7 @@
 
 #include "qb_dynamics.cuh"
 #include "qb_geometry.cuh"
+#include "qb_checks.cuh"
 #include "qb_internal.h"
 
 // BVH packet kernel: one camera per warp, QB_RF_BLOCK/32 warps per block and
@@ -320,6 +321,7 @@ __global__ void __launch_bounds__(QB_RF_BLOCK, QB_RF_MINB) k_render_f(DevScene S
                     rank += (eq > my_e) || (eq == my_e && q < lane);
                 }
                 __syncwarp();
+                QB_CHECK(lane >= ns || rank < STK, "k_render_f frontier stack");
                 if (lane < ns) stk[rank] = make_int2(my_rec, (int)my_e);
                 sp = ns;
                 __syncwarp();
@@ -392,6 +394,7 @@ __global__ void __launch_bounds__(QB_RF_BLOCK, QB_RF_MINB) k_render_f(DevScene S
                     // compiler may sink the store below the other lanes' loads, which then
                     // pop a stale entry and skip a subtree (seen as one C5 pixel reading a
                     // surface 0.6 m behind the one it should hit)
+                    QB_CHECK(sp < STK, "k_render_f traversal stack");
                     stk[sp] = make_int2(__float_as_int(flo.w) * 8 + (__float_as_int(fhi.w) + 2), (int)em);
                     ++sp;
                     ca = __float_as_int(nlo.w);
@@ -578,7 +581,9 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, QB_CULL_MINB)
             for (int k = 0; k < 9; ++k) Rw[k] = rotations[9 * c + k];
         }
         const int scene = env_scene ? env_scene[c] : 0;
+        QB_CHECK(scene >= 0 && scene < S.n_scenes, "k_render_cull scene index");
         const int p0 = S.prim_offset[scene], p1 = S.prim_offset[scene + 1];
+        QB_CHECK(p1 - p0 <= CULL_MAX, "k_render_cull scene size");
 
         // ---- 1. camera frustum culling (image frustum, near z >= 0, far z <= max_range)
         int ncand = 0;  // warp-uniform
@@ -599,6 +604,7 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, QB_CULL_MINB)
                     for (int q = 0; q < 6; ++q) k = k && keep(cp[q], rx, ry, rz, c0, a0, a1, a2);
                 }
                 const unsigned m = __ballot_sync(FULL, k);
+                QB_CHECK(!k || nc + __popc(m & lt_mask) < CULL_MAX, "k_render_cull candidate list");
                 if (k) cand[nc + __popc(m & lt_mask)] = p;
                 nc += __popc(m);
             }
@@ -684,6 +690,7 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, QB_CULL_MINB)
                 } else {
                     if (in) {
                         const int pos = nx + __popc(m & lt_mask);
+                        QB_CHECK(pos < XM, "k_render_cull swarm list");
                         xcs_s[wib][pos] = sph;
                         xk_s[wib][pos] = k;
                     }

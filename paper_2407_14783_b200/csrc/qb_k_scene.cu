@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <vector>
 
+#include "qb_checks.cuh"
 #include "qb_internal.h"
 #include "qb_scene_pack.cuh"
 
@@ -125,6 +126,8 @@ __global__ void k_karras(int n, const unsigned long long *keys, int2 *child, int
     const int g = i + s * d + min(d, 0);
     const int first = min(i, j), last = max(i, j);
     const int left = first == g ? n - 1 + g : g, right = last == g + 1 ? n - 1 + g + 1 : g + 1;
+    QB_CHECK(first >= 0 && last < n && first < last && left >= 0 && left < 2 * n - 1 && right >= 0 &&
+                 right < 2 * n - 1 && left != right, "karras hierarchy node");
     child[i] = make_int2(left, right);
     range[i] = make_int2(first, last);
     parent[left] = i;
@@ -209,6 +212,7 @@ __global__ void k_emit(int n, int node_off, int prim_off, const int *order, cons
         const int p = parent[u];
         if (range[p].y - range[p].x + 1 <= LEAF) return;  // inside a collapsed subtree
         slot = 1 + 2 * p + (child[p].x == u ? 0 : 1);
+        QB_CHECK(p >= 0 && p < n - 1 && slot < 2 * n - 1, "emit node slot");
     }
     node_bounds(n, u, order, plo, phi, ib, b);
     if (u >= n - 1) {

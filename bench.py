@@ -521,6 +521,56 @@ def cpu_baseline_env(kind="c3", n_sample=1024, steps=12):
     return n_sample * steps / dt, dt
 
 
+def reference_python_env(kind, n_sample, steps):
+    """The reference ITSELF -- quadsim (numpy + numba) installed unmodified in
+    baseline/_ref (`pip install --no-index --target baseline/_ref`) -- on a
+    bounded sample of the same workload, timed beside the C port (the port
+    is the reference arm; this shows how the port compares with the real
+    thing).  numba's JIT compile (first render / query) is timed separately
+    and excluded.  Returns None when baseline/_ref is absent."""
+    import dataclasses
+
+    ref_dir = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_dir, "quadsim")):
+        return None
+    if ref_dir not in sys.path:
+        sys.path.insert(0, ref_dir)
+    import numba
+    from quadsim.control import CTBR as RCTBR, LV as RLV
+    from quadsim.env.config import EnvConfig as REnvConfig, SensorSpec as RSensorSpec
+    from quadsim.env.tasks import make_env as rmake_env, navigation_config as rnav
+
+    if kind == "c1":
+        cfg = REnvConfig(num_agents=n_sample, command_type="ctbr", episode_max_steps=1000)
+    elif kind == "c3":
+        cfg = rnav(scene_seed=0, num_agents=n_sample)
+        cfg = dataclasses.replace(cfg, sensors=cfg.sensors + (RSensorSpec(kind="segmentation", name="segmentation",
+                                                                          width=64, height=64),))
+    else:
+        return None
+    rng = np.random.default_rng(0)
+
+    def act():
+        if kind == "c1":
+            return RCTBR(np.full(n_sample, 9.81), rng.normal(scale=0.5, size=(n_sample, 3)))
+        return RLV(rng.normal(scale=1.5, size=(n_sample, 3)), rng.uniform(-3, 3, n_sample))
+
+    t = time.perf_counter()
+    env = rmake_env(cfg)
+    env.reset(seed=0)
+    env.step(act())  # numba JIT compile of the render / nearest-point kernels
+    compile_s = time.perf_counter() - t
+    env.step(act())
+    t = time.perf_counter()
+    for _ in range(steps):
+        env.step(act())
+    dt = time.perf_counter() - t
+    return {"value": n_sample * steps / dt, "unit": "env-steps/s", "cores": int(numba.get_num_threads()),
+            "kind": "reference (quadsim, numpy + numba, unmodified, baseline/_ref)",
+            "sample": f"{n_sample} envs x {steps} steps ({dt:.1f} s; numba compile {compile_s:.1f} s excluded)",
+            "threading_layer": str(numba.threading_layer()) if hasattr(numba, "threading_layer") else None}
+
+
 def cpu_baseline_bptt(n_sample=8, T=64):
     """Oracle rollout_grad (dense 17x17 Jacobian chain, gradients.py:218-237)."""
     import oracle
@@ -768,6 +818,13 @@ def main():
             line["sustained"] = sustained_leg(args, rank, world, body)
             if rank == 0:
                 line["parity"] = parity_leg(body, kind)
+                if args.cpu and "cpu_baseline" in line:
+                    try:
+                        rp = reference_python_env("c3", 256, 2)
+                    except Exception as e:  # the reference's own stack is optional here; the port is the baseline
+                        rp = {"unavailable": f"{type(e).__name__}: {e}"[:200]}
+                    if rp:
+                        line["cpu_baseline"]["reference_python"] = rp
     if kind == "c3" and args.sub:
         # every other BASELINE config as a sub-record (same contract keys), so the
         # driver's default run carries each config's number, e2e and CPU baseline
@@ -778,6 +835,13 @@ def main():
         for sk, st in (("c1", 200), ("c2", 100), ("c5", 10)):
             sl = env_line(sk, sub_args(args, sk, st), rank, world, pk, cpu=args.cpu, e2e=args.e2e)
             sl["_r"] = None
+            if sk == "c1" and rank == 0 and args.cpu and "cpu_baseline" in sl:
+                try:
+                    rp = reference_python_env("c1", 100, 300)
+                except Exception as e:
+                    rp = {"unavailable": f"{type(e).__name__}: {e}"[:200]}
+                if rp:
+                    sl["cpu_baseline"]["reference_python"] = rp
             subs[sk] = strip(sl)
             torch.cuda.empty_cache()
         subs["c4"] = bptt_line(sub_args(args, "c4", 10), rank, world, pk, cpu=args.cpu)

@@ -1,0 +1,10 @@
+# A/B of the config-3 render: scripts/_dbg/base.so vs scripts/_dbg/new.so, alternating, 3 runs each
+for r in 1 2 3; do
+  for v in base new; do
+    QB_LIB_PATH=$PWD/scripts/_dbg/$v.so timeout 300 python bench.py --steps 30 --warmup 3 --no-e2e --no-cpu --no-sub > gpurun_out/ab_$v.log 2>&1
+    python -c "
+import json
+l=[x for x in open('gpurun_out/ab_$v.log') if x.startswith('{')]
+d=json.loads(l[-1]); print('$v', 'value %.4g'%d['value'], 'render %.4f ms'%d['kernel_ms']['render_k2'], 'step %.4f'%d['ms_per_step'])"
+  done
+done

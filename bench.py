@@ -214,7 +214,10 @@ def env_workload(kind, rank, world, total):
         cfg = workload_config(kind, total // world)
         return make_env(cfg), cfg
     cfg = workload_config(kind, total)
-    return make_env(cfg, shard=(rank, world)), cfg
+    # config 5's 5e5-triangle hall: built on the device (LBVH + SAH treelet refinement, ~26 ms; its tree
+    # renders as fast as the host binned-SAH tree, which takes ~0.45 s to build)
+    build = "device" if kind == "c5" else "host"
+    return make_env(cfg, shard=(rank, world), scene_build=build), cfg
 
 
 def make_actions(kind, n, count, rank):
@@ -313,7 +316,7 @@ def run_e2e(cfg, rank, world, kind):
 
     from paper_2407_14783_b200 import bindings
 
-    h = bindings.make_env(cfg, shard=(rank, world))
+    h = bindings.make_env(cfg, shard=(rank, world), scene_build="device" if kind == "c5" else "host")
     n = h.num_agents
     K = 6 if n > 4096 else 200
     rng = np.random.default_rng(rank)

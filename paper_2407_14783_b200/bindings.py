@@ -70,7 +70,7 @@ class FlatObservation:
 class FlatEnv:
     """One bindings handle.  Use the module functions or the methods."""
 
-    def __init__(self, config, params=None, sim=None, gains=None, device=None, shard=(0, 1)):
+    def __init__(self, config, params=None, sim=None, gains=None, device=None, shard=(0, 1), scene_build="host"):
         import torch
 
         from .env import EnvConfig, load_env_file, make_env
@@ -82,7 +82,7 @@ class FlatEnv:
             raise ConfigError("the flat bindings do not expose swarm mode")
         self._lock = threading.Lock()
         self._closed = False
-        self.env = make_env(config, params, sim, gains, device=device, shard=shard)
+        self.env = make_env(config, params, sim, gains, device=device, shard=shard, scene_build=scene_build)
         if self.env._custom_hooks:
             raise ConfigError("the flat bindings run the fused task hooks only")
         env, n = self.env, self.env.num_agents
@@ -295,11 +295,12 @@ def _torch_dtype(dt):
 # ---------------------------------------------------------------- module API (SPEC.md names)
 
 
-def make_env(config, params=None, sim=None, gains=None, device=None, shard=(0, 1)) -> FlatEnv:
+def make_env(config, params=None, sim=None, gains=None, device=None, shard=(0, 1), scene_build="host") -> FlatEnv:
     """config: an EnvConfig or the path of an env config file (load_env_file).
     shard=(rank, world): this handle owns the rank's contiguous slice of the
-    config's agents (multi-GPU, one handle per GPU)."""
-    return FlatEnv(config, params, sim, gains, device, shard)
+    config's agents (multi-GPU, one handle per GPU); scene_build "device"
+    builds large meshes on the GPU (as env.make_env)."""
+    return FlatEnv(config, params, sim, gains, device, shard, scene_build)
 
 
 def reset(handle: FlatEnv, seed: int = 0, out=None) -> FlatObservation:

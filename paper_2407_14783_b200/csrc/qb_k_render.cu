@@ -42,6 +42,14 @@ extern "C" int qb_debug_render_stats(unsigned long long *out) {
     return (int)cudaMemcpyFromSymbol(out, g_rf_stats, sizeof(g_rf_stats));
 }
 #endif
+#ifdef QB_CULL_STATS
+// culling renderer (scripts/cull_stats.py): cameras, candidates, tiles, survivors by record type
+// (sphere, AABB, OBB, generic)
+__device__ unsigned long long g_cull_stats[8];
+extern "C" int qb_debug_cull_stats(unsigned long long *out) {
+    return (int)cudaMemcpyFromSymbol(out, g_cull_stats, sizeof(g_cull_stats));
+}
+#endif
 
 namespace {
 
@@ -700,6 +708,12 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, QB_CULL_MINB)
             __syncwarp();
         }
 
+#ifdef QB_CULL_STATS
+        if (lane == 0 && part == 0) {
+            atomicAdd(&g_cull_stats[0], 1ull);
+            atomicAdd(&g_cull_stats[1], (unsigned long long)ncand);
+        }
+#endif
         int cnt = 0, sum_col = 0, sum_row = 0;
         __syncwarp();
         if (lane < 9) rws_s[wib][lane] = Rw[lane];  // (every lane holds the same pose)
@@ -728,6 +742,9 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, QB_CULL_MINB)
                 iL = rsqrtf(1.f + xl * xl); iR = rsqrtf(1.f + xr * xr);
                 iT = rsqrtf(1.f + yt * yt); iB = rsqrtf(1.f + yb * yb);
             }
+#ifdef QB_CULL_STATS
+            if (lane == 0) atomicAdd(&g_cull_stats[2], 1ull);
+#endif
             tx += split;
             while (tx >= tiles_x) {
                 tx -= tiles_x;
@@ -787,6 +804,9 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, QB_CULL_MINB)
                     const int k2 = b + bit;
                     float t[2] = {-1.0f, -1.0f};
                     int oid;
+#ifdef QB_CULL_STATS
+                    if (lane == 0) atomicAdd(&g_cull_stats[3 + (k2 < CREC ? met[k2].x : 3)], 1ull);
+#endif
                     if (k2 < CREC) {
                         const int2 mt2 = met[k2];
                         const float4 s0 = rec[k2][0];

@@ -526,9 +526,14 @@ __device__ __forceinline__ float slab_hit(float nlx, float nly, float nlz, float
     return -1.0f;
 }
 
+// CENT: a pad centroid is reduced inline (landing, split == 1): a compile-time
+// switch, so the common render carries no per-pixel centroid test.
+// EXACT: a 64x64 frame with both outputs (the spec's camera, configs 2-5):
+// compile-time sizes, no per-pixel bounds / null tests, the tile-plane table.
+// S1: split == 1 (large batches: one warp per camera, cameras grid-strided).
 // EXTRA: swarm spheres present (separate instance: no swarm shared memory or
 // registers in the common case)
-template <bool FROM_STATE, bool EXTRA>
+template <bool FROM_STATE, bool EXTRA, bool CENT, bool EXACT, bool S1>
 __global__ void __launch_bounds__(CULL_WARPS * 32, QB_CULL_MINB)
     k_render_cull(DevScene S, CamF cam, long long n, long long ld, const float *state, const float *origins,
                   const float *rotations, const int32_t *env_scene, float *depth, int32_t *seg, int centroid_id,
@@ -551,7 +556,8 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, QB_CULL_MINB)
     const unsigned lt_mask = (1u << lane) - 1u;
     const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
-    const int W = cam.W, H = cam.H;
+    // EXACT: the 64x64 frame of the spec's camera, sizes known at compile time
+    const int W = EXACT ? 64 : cam.W, H = EXACT ? 64 : cam.H;
     const int tiles_x = (W + TILE_W - 1) / TILE_W;
     const float tmin = 1e-9f;
     // pixel-centre image-plane coordinates: x(j) = ((j + 0.5) * 2/W - 1) * th
@@ -559,7 +565,7 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, QB_CULL_MINB)
     constexpr int TH2 = 2 * TILE_H;
     const int tiles_y2 = (H + TH2 - 1) / TH2, n_tiles = tiles_y2 * tiles_x;
     // the tile planes depend on the tile only: one table per block
-    const bool tpl = n_tiles <= TPL_MAX;
+    const bool tpl = EXACT || n_tiles <= TPL_MAX;
     if (tpl) {
         for (int tl = threadIdx.x; tl < n_tiles; tl += blockDim.x) {
             const int i0 = (tl / tiles_x) * TH2, j0 = (tl % tiles_x) * TILE_W;
@@ -574,9 +580,10 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, QB_CULL_MINB)
     __syncthreads();
 
     // small batches: `split` warps share one camera, each taking every split-th tile
+    if (S1) split = 1;
     for (long long wi = warp; wi < n * split; wi += nwarps) {
-        const long long c = wi / split;
-        const int part = (int)(wi % split);
+        const long long c = S1 ? wi : wi / split;
+        const int part = S1 ? 0 : (int)(wi % split);
         float o[3], Rw[9];
         if (FROM_STATE) {
             float p[3] = {state[0 * ld + c], state[1 * ld + c], state[2 * ld + c]};
@@ -745,10 +752,17 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, QB_CULL_MINB)
 #ifdef QB_CULL_STATS
             if (lane == 0) atomicAdd(&g_cull_stats[2], 1ull);
 #endif
-            tx += split;
-            while (tx >= tiles_x) {
-                tx -= tiles_x;
-                ++ty;
+            if (S1) {  // consecutive tiles
+                if (++tx == tiles_x) {
+                    tx = 0;
+                    ++ty;
+                }
+            } else {
+                tx += split;
+                while (tx >= tiles_x) {
+                    tx -= tiles_x;
+                    ++ty;
+                }
             }
             const float x = ((j + 0.5f) * sx - 1.0f) * cam.th;
             float dx[2], dy[2], dz[2], ix[2], iy[2], iz[2], czv[2], tmx[2], best[2];
@@ -902,11 +916,11 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, QB_CULL_MINB)
                 const float t = tt[u];
                 const int oid = to[u];
                 const int out_id = t > 0.0f ? oid : 0;
-                if (j < W && i < H) {
+                if (EXACT || (j < W && i < H)) {
                     const int off = i * W + j;
-                    if (depth_c) depth_c[off] = t > 0.0f ? t * czv[u] : cam.max_range;
-                    if (seg_c) seg_c[off] = out_id;
-                    if (centroid_id > 0 && out_id == centroid_id) {
+                    if (EXACT || depth_c) depth_c[off] = t > 0.0f ? t * czv[u] : cam.max_range;
+                    if (EXACT || seg_c) seg_c[off] = out_id;
+                    if (CENT && out_id == centroid_id) {
                         cnt += 1;
                         sum_col += j;
                         sum_row += i;
@@ -914,7 +928,7 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, QB_CULL_MINB)
                 }
             }
         }
-        if (centroid_id > 0 && split == 1) {
+        if (CENT && split == 1) {
 #pragma unroll
             for (int s2 = 16; s2 > 0; s2 >>= 1) {
                 cnt += __shfl_xor_sync(FULL, cnt, s2);
@@ -1064,16 +1078,35 @@ int launch_render(const qb_scene *s, const qb_camera *cam, int dtype, long long 
             long long blocks = (n * split + CULL_WARPS - 1) / CULL_WARPS;
             long long max_blocks = (long long)sm_count() * 16;
             if (blocks > max_blocks) blocks = max_blocks;
-#define QB_CULL(FS, EX)                                                                                         \
-    k_render_cull<FS, EX><<<(int)blocks, B, 0, st>>>(s->dev, c, n, ld, FS ? (const float *)state : nullptr,         \
-                                                     FS ? nullptr : (const float *)origins,                         \
-                                                     FS ? nullptr : (const float *)rotations, env_scene, (float *)depth, \
-                                                     seg, FS ? centroid_id : 0, FS ? centroid : nullptr,             \
-                                                     (const float *)extra, extra_ids, n_extra, split)
+#define QB_CULL(FS, EX, CE)                                                                                         \
+    if (exact && split == 1)                                                                                            \
+        k_render_cull<FS, EX, CE, true, true><<<(int)blocks, B, 0, st>>>(s->dev, c, n, ld, FS ? (const float *)state : nullptr, \
+                                                         FS ? nullptr : (const float *)origins,                         \
+                                                         FS ? nullptr : (const float *)rotations, env_scene, (float *)depth, \
+                                                         seg, FS ? centroid_id : 0, FS ? centroid : nullptr,             \
+                                                         (const float *)extra, extra_ids, n_extra, split);               \
+    else if (exact)                                                                                                     \
+        k_render_cull<FS, EX, CE, true, false><<<(int)blocks, B, 0, st>>>(s->dev, c, n, ld, FS ? (const float *)state : nullptr, \
+                                                         FS ? nullptr : (const float *)origins,                         \
+                                                         FS ? nullptr : (const float *)rotations, env_scene, (float *)depth, \
+                                                         seg, FS ? centroid_id : 0, FS ? centroid : nullptr,             \
+                                                         (const float *)extra, extra_ids, n_extra, split);               \
+    else                                                                                                                \
+    k_render_cull<FS, EX, CE, false, false><<<(int)blocks, B, 0, st>>>(s->dev, c, n, ld, FS ? (const float *)state : nullptr, \
+                                                         FS ? nullptr : (const float *)origins,                         \
+                                                         FS ? nullptr : (const float *)rotations, env_scene, (float *)depth, \
+                                                         seg, FS ? centroid_id : 0, FS ? centroid : nullptr,             \
+                                                         (const float *)extra, extra_ids, n_extra, split)
+            const bool cent = state && centroid_id > 0 && split == 1;  // inline centroid (else the k_centroid pass)
+            const bool exact = depth && seg && c.W == 64 && c.H == 64;
             if (state) {
-                if (n_extra > 0) QB_CULL(true, true); else QB_CULL(true, false);
+                if (n_extra > 0) {
+                    if (cent) QB_CULL(true, true, true); else QB_CULL(true, true, false);
+                } else {
+                    if (cent) QB_CULL(true, false, true); else QB_CULL(true, false, false);
+                }
             } else {
-                if (n_extra > 0) QB_CULL(false, true); else QB_CULL(false, false);
+                if (n_extra > 0) QB_CULL(false, true, false); else QB_CULL(false, false, false);
             }
 #undef QB_CULL
             int rc = check_launch("render_cull_f32");

@@ -144,7 +144,10 @@ __device__ float4 g_dbg_log[8192];
 #define QB_DBG(on, kind, a, b, c) do {} while (0)
 #endif
 
-template <bool FROM_STATE>
+// EXACT: 64x64 frame, depth + segmentation, no swarm spheres; CENT: inline
+// pad centroid; S1: split == 1 -- compile-time switches of the common
+// launches (config 5: EXACT + CENT + S1), as in the culling renderer
+template <bool FROM_STATE, bool EXACT = false, bool CENT = false, bool S1 = false>
 __global__ void __launch_bounds__(QB_RF_BLOCK, QB_RF_MINB) k_render_f(DevScene S, CamF cam, long long n, long long ld, const float *state,
                                                      const float *origins, const float *rotations, const int32_t *env_scene,
                                                      float *depth, int32_t *seg, int centroid_id, float *centroid,
@@ -160,7 +163,8 @@ __global__ void __launch_bounds__(QB_RF_BLOCK, QB_RF_MINB) k_render_f(DevScene S
     const unsigned lanes_below = (1u << lane) - 1u;
     const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
-    const int W = cam.W, H = cam.H;
+    const int W = EXACT ? 64 : cam.W, H = EXACT ? 64 : cam.H;
+    if (S1) split = 1;
     const int tiles_x = (W + TILE_W - 1) / TILE_W, tiles_y = (H + TILE_H - 1) / TILE_H;
     const float tmin = 1e-9f;
     const float sx = 2.0f / W, sy = 2.0f / H;
@@ -169,8 +173,8 @@ __global__ void __launch_bounds__(QB_RF_BLOCK, QB_RF_MINB) k_render_f(DevScene S
     // small batches: `split` warps share one camera (each builds the camera
     // frontier and takes every split-th tile)
     for (long long wi = warp; wi < n * split; wi += nwarps) {
-        const long long c = wi / split;
-        const int part = (int)(wi % split);
+        const long long c = S1 ? wi : wi / split;
+        const int part = S1 ? 0 : (int)(wi % split);
         float o[3];
         {
             float Rw[9];
@@ -247,7 +251,7 @@ __global__ void __launch_bounds__(QB_RF_BLOCK, QB_RF_MINB) k_render_f(DevScene S
             const int j0 = (tile % tiles_x) * TILE_W, i0 = (tile / tiles_x) * TILE_H;
             const int j = j0 + (lane & 7);
             const int i = i0 + (lane >> 3);
-            const bool valid = (j < W) && (i < H);
+            const bool valid = EXACT || ((j < W) && (i < H));
 #ifdef QB_RF_DEBUG
             const bool dbg = c == g_dbg_target[0] && i == g_dbg_target[1] && j == g_dbg_target[2];
 #else
@@ -424,7 +428,7 @@ __global__ void __launch_bounds__(QB_RF_BLOCK, QB_RF_MINB) k_render_f(DevScene S
 #endif
             float t = hit ? best : -1.0f;
             int oid = hit ? bid : -1;
-            if (n_extra > 0) {  // swarm agents as spheres (kernels.py:438-445)
+            if (!EXACT && n_extra > 0) {  // swarm agents as spheres (kernels.py:438-445)
                 for (int k = 0; k < n_extra; ++k) {
                     const float4 sph = *reinterpret_cast<const float4 *>(extra + (c * n_extra + k) * 4);
                     float ts = ray_sphere_v(sph, sph.w * sph.w, o[0], o[1], o[2], dx, dy, dz, tmin, tmax);
@@ -437,16 +441,16 @@ __global__ void __launch_bounds__(QB_RF_BLOCK, QB_RF_MINB) k_render_f(DevScene S
             const int out_id = t > 0.0f ? oid : 0;
             if (valid) {
                 const long long off = (c * H + i) * (long long)W + j;
-                if (depth) depth[off] = t > 0.0f ? t * rsqrtf(n2) : cam.max_range;
-                if (seg) seg[off] = out_id;
-                if (centroid_id > 0 && out_id == centroid_id) {
+                if (EXACT || depth) depth[off] = t > 0.0f ? t * rsqrtf(n2) : cam.max_range;
+                if (EXACT || seg) seg[off] = out_id;
+                if ((EXACT ? CENT : centroid_id > 0) && out_id == centroid_id) {
                     cnt += 1;
                     sum_col += j;
                     sum_row += i;
                 }
             }
         }
-        if (centroid_id > 0 && split == 1) {  // (split: the k_centroid pass)
+        if ((EXACT ? CENT : centroid_id > 0) && split == 1) {  // (split: the k_centroid pass)
 #pragma unroll
             for (int s = 16; s > 0; s >>= 1) {
                 cnt += __shfl_xor_sync(FULL, cnt, s);
@@ -1129,7 +1133,20 @@ int launch_render(const qb_scene *s, const qb_camera *cam, int dtype, long long 
         if (split > 1 && !seg && centroid_id > 0) split = 1;  // the centroid pass reads seg
         long long blocks = (n * split * 32 + B - 1) / B;
         if (blocks > 0x7fffffffLL) blocks = 0x7fffffffLL;  // grid-stride loop covers the rest
-        if (state)
+        const bool exact = state && depth && seg && n_extra == 0 && c.W == 64 && c.H == 64;
+        if (exact) {
+#define QB_RF_X(CE, S1_)                                                                                              \
+    k_render_f<true, true, CE, S1_><<<(int)blocks, B, 0, st>>>(s->dev, c, n, ld, (const float *)state, nullptr, nullptr, \
+                                                                env_scene, (float *)depth, seg, centroid_id, centroid,   \
+                                                                nullptr, nullptr, 0, split)
+            const bool ce = centroid_id > 0;
+            if (split == 1) {
+                if (ce) QB_RF_X(true, true); else QB_RF_X(false, true);
+            } else {
+                if (ce) QB_RF_X(true, false); else QB_RF_X(false, false);
+            }
+#undef QB_RF_X
+        } else if (state)
             k_render_f<true><<<(int)blocks, B, 0, st>>>(s->dev, c, n, ld, (const float *)state, nullptr, nullptr, env_scene,
                                                         (float *)depth, seg, centroid_id, centroid, (const float *)extra,
                                                         extra_ids, n_extra, split);

@@ -1,7 +1,9 @@
-# A/B of the config-3 render: scripts/_dbg/base.so vs scripts/_dbg/new.so, alternating, 3 runs each
+# A/B of a workload's render (WL=c3 default): scripts/_dbg/base.so vs scripts/_dbg/new.so, alternating
+WL=${WL:-c3}
+STEPS=${STEPS:-30}
 for r in 1 2 3; do
   for v in base new; do
-    QB_LIB_PATH=$PWD/scripts/_dbg/$v.so timeout 300 python bench.py --steps 30 --warmup 3 --no-e2e --no-cpu --no-sub > gpurun_out/ab_$v.log 2>&1
+    QB_LIB_PATH=$PWD/scripts/_dbg/$v.so timeout 300 python bench.py --workload $WL --steps $STEPS --warmup 3 --no-e2e --no-cpu --no-sub > gpurun_out/ab_$v.log 2>&1
     python -c "
 import json
 l=[x for x in open('gpurun_out/ab_$v.log') if x.startswith('{')]

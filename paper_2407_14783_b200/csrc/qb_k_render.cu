@@ -550,6 +550,7 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, QB_CULL_MINB)
     __shared__ float4 rec_s[CULL_WARPS][CREC][4];      // shading records (warp-broadcast reads)
     __shared__ int2 met_s[CULL_WARPS][CREC];           // (record type, object id)
     __shared__ float cul_s[CULL_WARPS][13][CREC];      // culling bounds, SoA (conflict-free lane-parallel reads)
+    __shared__ unsigned tmask_s[EXACT ? CULL_WARPS : 1][EXACT ? CREC : 1];  // EXACT: tile columns | rows << 8 per record
     __shared__ float4 tpl_s[TPL_MAX][2];               // per-tile camera-space planes (xl xr yt yb) (iL iR iT iB)
     const int wib = threadIdx.x >> 5;
     int *cand = cand_s[wib];
@@ -725,6 +726,47 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, QB_CULL_MINB)
             atomicAdd(&g_cull_stats[1], (unsigned long long)ncand);
         }
 #endif
+        // EXACT (64x64 = 8 x 8 tiles): the tile culling below evaluates, per tile, the
+        // record's support against the tile's 4 border-pixel planes; every tile of a
+        // column shares its L / R planes and every tile of a row its T / B planes, so
+        // the same tests are run once per camera for the 8 columns and 8 rows (32
+        // planes) and kept as two 8-bit masks per record -- a tile's test becomes two
+        // bit lookups, with bit-identical decisions
+        if (EXACT) {
+            const int nrec = min(ncand, CREC);
+            for (int b = 0; b < nrec; b += 32) {
+                const int k = b + lane;
+                if (k < nrec) {
+                    const float rr = cul[0][k], ccx = cul[1][k], ccy = cul[2][k], ccz = cul[3][k];
+                    const float a0x = cul[4][k], a0y = cul[5][k], a0z = cul[6][k];
+                    const float a1x = cul[7][k], a1y = cul[8][k], a1z = cul[9][k];
+                    const float a2x = cul[10][k], a2y = cul[11][k], a2z = cul[12][k];
+                    unsigned msk = 0;
+#pragma unroll 1
+                    for (int q = 0; q < 8; ++q) {  // column q: tiles tl = q + 8 r share xl, xr (tpl_s[q])
+                        const float4 pa = tpl_s[q][0], pb = tpl_s[q][1];
+                        const float xl = pa.x, xr = pa.y, iL = pb.x, iR = pb.y;
+                        const float dL = (ccx - xl * ccz) * iL,
+                                    sL = (fabsf(a0x - xl * a0z) + fabsf(a1x - xl * a1z) + fabsf(a2x - xl * a2z)) * iL;
+                        const float dR = (xr * ccz - ccx) * iR,
+                                    sR = (fabsf(xr * a0z - a0x) + fabsf(xr * a1z - a1x) + fabsf(xr * a2z - a2x)) * iR;
+                        if ((dL + sL + rr >= -CULL_EPS) && (dR + sR + rr >= -CULL_EPS)) msk |= 1u << q;
+                    }
+#pragma unroll 1
+                    for (int q = 0; q < 8; ++q) {  // row q: tiles tl = 8 q + c share yt, yb (tpl_s[8 q])
+                        const float4 pa = tpl_s[8 * q][0], pb = tpl_s[8 * q][1];
+                        const float yt = pa.z, yb = pa.w, iT = pb.z, iB = pb.w;
+                        const float dT = (ccy - yt * ccz) * iT,
+                                    sT = (fabsf(a0y - yt * a0z) + fabsf(a1y - yt * a1z) + fabsf(a2y - yt * a2z)) * iT;
+                        const float dB = (yb * ccz - ccy) * iB,
+                                    sB = (fabsf(yb * a0z - a0y) + fabsf(yb * a1z - a1y) + fabsf(yb * a2z - a2y)) * iB;
+                        if ((dT + sT + rr >= -CULL_EPS) && (dB + sB + rr >= -CULL_EPS)) msk |= 1u << (8 + q);
+                    }
+                    tmask_s[EXACT ? wib : 0][EXACT ? k : 0] = msk;
+                }
+            }
+            __syncwarp();
+        }
         int cnt = 0, sum_col = 0, sum_row = 0;
         __syncwarp();
         if (lane < 9) rws_s[wib][lane] = Rw[lane];  // (every lane holds the same pose)
@@ -794,7 +836,16 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, QB_CULL_MINB)
             for (int b = 0; b < ncand; b += 32) {
                 const int k = b + lane;
                 bool kp = false;
-                if (k < ncand) {
+                if (EXACT) {
+                    if (k < ncand) {
+                        if (k < CREC) {
+                            const unsigned msk = tmask_s[EXACT ? wib : 0][EXACT ? k : 0];
+                            kp = ((msk >> (tl & 7)) & (msk >> (8 + (tl >> 3))) & 1u) != 0;
+                        } else {
+                            kp = true;
+                        }
+                    }
+                } else if (k < ncand) {
                     if (k < CREC) {
                         // support = r + sum_k |n . A'_k|; L/R normals (+-1, 0, z), T/B (0, +-1, z)
                         const float rr = cul[0][k], ccx = cul[1][k], ccy = cul[2][k], ccz = cul[3][k];

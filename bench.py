@@ -457,12 +457,13 @@ def run_bptt(args, rank, world):
     target = torch.tensor([1.0, 0.0, 2.0], device="cuda")
     gsum = torch.zeros(T * 4, dtype=torch.float64, device="cuda")
     red = torch.zeros(T * 4 + 1, dtype=torch.float64, device="cpu" if SHARE_GPU else "cuda")
+    # dL/dtrajectory: the loss reads only the final positions, so every other block stays zero (written once)
+    gtraj = torch.zeros((T + 1, 17, n), device="cuda")
 
     def iteration():
         tape, _ = G.rollout_planes(P, "rotor", init, acts)
         d = tape[-1, 0:3] - target[:, None]
         loss = (d * d).sum() / (n * world) + 1e-6 * ((acts - 900.0) ** 2).sum()
-        gtraj = torch.zeros_like(tape)
         gtraj[-1, 0:3] = 2.0 * d / (n * world)
         gsum.zero_()
         ga, gi, _ = G.backward_planes(P, "rotor", tape, acts, gtraj, action_grad_sum=gsum)

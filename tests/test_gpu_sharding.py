@@ -161,3 +161,16 @@ def test_bench_spawns_its_own_ranks():
     assert out.returncode == 0, out.stderr[-2000:]
     line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
     assert line["n_gpus"] == 2 and line["config"]["global_envs"] == 200 and line["value"] > 0
+
+
+def test_bench_two_ranks_end_to_end_leg():
+    """The e2e leg under two ranks: each rank's flat-bindings handle owns its
+    shard (bindings.make_env(shard=...)); the whole-job e2e value counts both."""
+    env = dict(os.environ, QB_BENCH_SHARE_GPU="1")
+    env.pop("WORLD_SIZE", None)
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--workload", "c2a", "--steps", "10",
+                          "--warmup", "3", "--no-cpu"], capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["config"]["global_envs"] == 200
+    assert line["e2e"]["value"] > 0 and line["e2e"]["h2d_bytes_per_step"] == 100 * 16

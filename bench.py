@@ -436,9 +436,10 @@ def run_dynamics_roofline(pk):
 
 def run_bptt(args, rank, world):
     """Config 4: BPTT through the dynamics, horizon 64, 16384 envs/GPU.
-    One iteration = forward rollout (1 launch) + loss gradient + adjoint sweep
-    (1 launch, env-summed shared-action gradient reduced in-kernel) +
-    all_reduce(SUM) of loss and shared gradient over NCCL."""
+    One iteration = forward rollout (1 launch) + loss and its trajectory
+    gradient + adjoint sweep (1 launch) + fixed-order env-sum of the shared
+    action gradient, replayed as one CUDA graph, then all_reduce(SUM) of loss
+    and shared gradient over NCCL."""
     import torch
 
     from paper_2407_14783_b200 import gradients as G
@@ -460,15 +461,34 @@ def run_bptt(args, rank, world):
     # dL/dtrajectory: the loss reads only the final positions, so every other block stays zero (written once)
     gtraj = torch.zeros((T + 1, 17, n), device="cuda")
 
-    def iteration():
+    loss_buf = torch.zeros((), dtype=torch.float64, device="cuda")
+
+    def local():
+        """Everything of an iteration but the collective: forward rollout, loss and
+        its trajectory gradient, adjoint sweep, env-sum of the action gradient."""
         tape, _ = G.rollout_planes(P, "rotor", init, acts)
         d = tape[-1, 0:3] - target[:, None]
-        loss = (d * d).sum() / (n * world) + 1e-6 * ((acts - 900.0) ** 2).sum()
+        loss_buf.copy_((d * d).sum() / (n * world) + 1e-6 * ((acts - 900.0) ** 2).sum())
         gtraj[-1, 0:3] = 2.0 * d / (n * world)
         gsum.zero_()
-        ga, gi, _ = G.backward_planes(P, "rotor", tape, acts, gtraj, action_grad_sum=gsum)
-        reduce_bptt(loss, gsum, out=red)  # one all_reduce(SUM) of [shared grad, loss] over NCCL
-        return ga
+        G.backward_planes(P, "rotor", tape, acts, gtraj, action_grad_sum=gsum)
+
+    for _ in range(2):  # warm-up (allocator, module loading) before capture
+        local()
+    torch.cuda.synchronize()
+    # the iteration's ~15 launches replayed as one CUDA graph (static shapes); the
+    # NCCL all-reduce stays outside the graph
+    graph = torch.cuda.CUDAGraph()
+    cs = torch.cuda.Stream()
+    cs.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(cs):
+        with torch.cuda.graph(graph, stream=cs):
+            local()
+    torch.cuda.current_stream().wait_stream(cs)
+
+    def iteration():
+        graph.replay()
+        reduce_bptt(loss_buf, gsum, out=red)  # one all_reduce(SUM) of [shared grad, loss] over NCCL
 
     for _ in range(args.warmup):
         iteration()
@@ -676,6 +696,7 @@ def bptt_line(args, rank, world, pk, cpu=True):
     line = {"metric": "BPTT env-steps/sec (forward + adjoint), whole box", "value": steps_total / (r["ms"] / 1e3),
             "ms_per_step": r["ms"] / args.steps, "steps": args.steps, "clocks": r["clocks"],
             "scaling": "strong" if args.strong else "weak", "gpu_launches": 3 * args.steps,
+            "graph": "forward + loss + adjoint + env-sum captured as one CUDA graph per iteration",
             "config": {"workload": WORKLOADS["c4"], "envs_per_gpu": r["n"], "horizon": r["T"],
                        "parallelism": f"env shards x{world}, all_reduce(SUM) of loss + shared action grad"},
             "kernel_ms": {"rollout_forward": r["fwd_ms"], "rollout_backward": r["bwd_ms"]}}

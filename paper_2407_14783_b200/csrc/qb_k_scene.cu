@@ -251,7 +251,10 @@ __global__ void k_emit(int n, int node_off, int prim_off, const int *order, cons
 #endif
 constexpr int TL = QB_TREELET > 1 ? QB_TREELET : 2;
 constexpr int TL_MIN = 8;                // restructure nodes of at least this many primitives
-constexpr float SAH_CT = 1.2f, SAH_CI = 1.0f;
+#ifndef QB_SAH_CT
+#define QB_SAH_CT 1.2f  // SAH cost of a node visit relative to one primitive test
+#endif
+constexpr float SAH_CT = QB_SAH_CT, SAH_CI = 1.0f;
 
 // the sweep's tree arrays change under other SMs: read them through L2
 __device__ __forceinline__ int2 ld_child(const int2 *child, int u) { return __ldcg(&child[u]); }

@@ -176,6 +176,7 @@ class FlatEnv:
         self._io.n_copies = len(src) + 1
         self._io.copies = ctypes.cast(self._copies, ctypes.c_void_p)
         self._reset_done = False
+        self._cache = None  # (out dict, its error-count view, the step result built on it)
         self._lib = nat.lib()
         self._stream_ptr = ctypes.c_void_p(self._stream.cuda_stream)
         self._step_fn = self._lib.qb_env_step_io
@@ -240,6 +241,18 @@ class FlatEnv:
 
     def _run(self, step, actions, out):
         env = self.env
+        cached = self._cache
+        if step and out is not None and cached is not None and cached[0] is out:
+            # the caller's buffer set of the previous step again: every pointer in the
+            # io block and every returned view is unchanged -- one native call
+            self._io.host_action = actions.ctypes.data
+            nat.check(self._step_fn(*self._args, self._io_ref, self._stream_ptr), "qb_env_step_io")
+            if cached[1][0] > 0:
+                nfail = int(cached[1][0])
+                env._errors.zero_()
+                raise SpawnFailure(f"{nfail} respawns found no spawn with clearance >= {env.config.min_spawn_clearance}")
+            return cached[2]
+        self._cache = None
         if out is None:  # freshly owned arrays every call (pageable host memory)
             out = {k: np.empty(shape, dtype=dt) for k, _, shape, dt in self._src}
             out["_small"] = np.empty(self._small_nbytes, dtype=np.uint8)
@@ -282,7 +295,10 @@ class FlatEnv:
         flags = v("flags", np.bool_).reshape(7, n)
         info = {"success": flags[3], "collision": flags[4], "out_of_bounds": flags[5], "nonfinite": flags[6],
                 "nearest_distance": v("dist", np.float64), "scene": v("scene", np.int32), "step": v("step", np.int32)}
-        return obs, v("reward", np.float32), flags[1], flags[2], info
+        result = (obs, v("reward", np.float32), flags[1], flags[2], info)
+        if "_pinned" in out:  # a caller-owned set (outputs()): reused calls take the fast path
+            self._cache = (out, small[self._off_err:self._off_err + 4].view(np.int32), result)
+        return result
 
 
 def _torch_dtype(dt):

@@ -6,6 +6,7 @@ import ctypes
 import os
 import re
 import subprocess
+import sys
 
 import numpy as np
 import pytest
@@ -269,3 +270,24 @@ def test_cluttered_mesh_scene_tessellates_the_nav_room():
             assert np.isclose(v[:, 2].min(), c[2] - r) and np.isclose(v[:, 2].max(), c[2] + r)
     t = mesh.arrays
     assert (t.prim_type == 2).all() and len(t) == 2076
+
+
+def test_bench_reference_arm_contract():
+    """`bench.py --impl reference` (the reference's algorithm on the host cores,
+    the driver's reference arm) prints one JSON line with the contract keys, on
+    the same metric / unit / workload as our arm; runs without a GPU."""
+    import json
+
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--workload", "c1",
+                          "--steps", "1", "--warmup", "1"], capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    for k in ("impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "higher_is_better", "config",
+              "cpu_baseline", "e2e"):
+        assert k in line, k
+    assert line["impl"] == "reference" and line["value"] > 0 and line["higher_is_better"] is True
+    assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
+    import bench
+
+    assert line["metric"] == bench.METRIC and line["config"]["workload"] == bench.WORKLOADS["c1"]

@@ -13,7 +13,9 @@
  *   - plain pointers + sizes; all per-step buffers are caller-owned DEVICE
  *     memory, passed with the cudaStream_t (as void*) to enqueue on;
  *   - the library allocates only scene handles (qb_scene_create/destroy) and
- *     never allocates, frees or synchronises inside a per-step call;
+ *     never allocates, frees or synchronises inside a per-step call (the one
+ *     exception: qb_env_step_io, the host-buffer bindings step, may
+ *     synchronise its stream when asked to);
  *   - states are field-major planes: plane k (0..16, dynamics.py:3-8 order
  *     p v q omega rotor) of env i lives at state[k*ld + i];
  *   - every call returns 0 (QB_OK) or a QB_E* status; qb_last_error() gives a

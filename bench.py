@@ -351,6 +351,47 @@ def run_e2e(cfg, rank, world, kind):
                     "uint8 when every id < 256, lossless), stream synchronised before returning"}
 
 
+def run_e2e_device_obs(env, world, kind, K=50):
+    """A GPU-resident policy's loop (Isaac-Gym style): the public env.step
+    with host actions from pinned memory (H2D inside the timed region) and
+    the step's reward / terminated / truncated read back to the host every
+    step (D2H), while the observations stay on the device for the policy.
+    A secondary figure beside `e2e` (which ships every observation back)."""
+    import torch
+
+    from paper_2407_14783_b200.control import CTBR, LV
+
+    n = env.num_agents
+    rng = np.random.default_rng(1)
+    acts = []
+    for _ in range(K + 2):
+        a = torch.empty((n, 4), dtype=torch.float32, pin_memory=True)
+        a[:, :3] = torch.as_tensor(rng.normal(scale=1.5, size=(n, 3)), dtype=torch.float32)
+        a[:, 3] = torch.as_tensor(rng.uniform(-math.pi, math.pi, n), dtype=torch.float32)
+        acts.append(a)
+    host = torch.empty(n * 6, dtype=torch.uint8, pin_memory=True)
+
+    def one(a):
+        cmd = CTBR(a[:, 0] + 9.81, a[:, 1:]) if kind == "c1" else LV(a[:, :3], a[:, 3])
+        r = env.step(cmd)
+        host[:4 * n].view(torch.float32).copy_(r.reward, non_blocking=True)
+        host[4 * n:5 * n].copy_(r.terminated.view(torch.uint8), non_blocking=True)
+        host[5 * n:].copy_(r.truncated.view(torch.uint8), non_blocking=True)
+        torch.cuda.current_stream().synchronize()  # the host reads the step's result
+
+    for k in range(2):
+        one(acts[k])
+    barrier(world)
+    t = time.perf_counter()
+    for k in range(K):
+        one(acts[k + 2])
+    dt = max_over_ranks(time.perf_counter() - t, world)
+    return {"value": n * world * K / dt, "unit": "env-steps/s", "h2d_bytes_per_step": n * 16,
+            "d2h_bytes_per_step": n * 6, "steps": K,
+            "path": "env.step(LV from pinned host actions) -> reward / terminated / truncated read back each step; "
+                    "observations stay on the device (a GPU-resident policy)"}
+
+
 def run_env_step_roofline(pk):
     """K1+K3 fused env step alone (qb_env_step) at 4M envs, free flight in the
     garage: per env-step it reads the state (68 B) + action (16 B) + step
@@ -679,6 +720,8 @@ def env_line(kind, args, rank, world, pk, cpu=True, e2e=True):
                                     "at 4M envs)"}
     if e2e:
         line["e2e"] = run_e2e(r["cfg"], rank, world, kind)
+        if kind == "c3" and r.get("env") is not None:
+            line["e2e_obs_on_device"] = run_e2e_device_obs(r["env"], world, kind)
     if rank == 0 and cpu:
         ns = {"c5": 64, "c3n": 256, "swarm": 256}.get(kind, min(1024, ENVS[kind]))
         steps = {"c5": 2, "swarm": 4}.get(kind, 12 if ns > 100 else 400)

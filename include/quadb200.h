@@ -345,6 +345,17 @@ typedef struct qb_step_io {
 int qb_env_step_io(const qb_params *p, int32_t cmd_kind, const qb_task *task, const qb_scene *s,
                    const qb_env_buffers *b, const qb_step_io *io, void *stream);
 
+/* The same step captured once into a CUDA graph for repeated launches with
+ * the same buffers (small batches are launch-latency-bound): every pointer of
+ * p / task / b / io is fixed at capture; io->host_action must be PINNED host
+ * memory (read in place; its contents change between launches, its address
+ * may not); io->sync is ignored (the launch's `sync` decides). */
+typedef struct qb_step_graph qb_step_graph;
+int qb_env_step_graph_create(const qb_params *p, int32_t cmd_kind, const qb_task *task, const qb_scene *s,
+                             const qb_env_buffers *b, const qb_step_io *io, qb_step_graph **out);
+int qb_env_step_graph_launch(qb_step_graph *g, int32_t sync, void *stream);
+int qb_env_step_graph_destroy(qb_step_graph *g);
+
 /* numpy.random.default_rng(seed + i) seeding for i in [0,n): out (n,4). */
 int qb_rng_seed(uint64_t seed, int64_t n, uint64_t *out, void *stream);
 /* n draws of next_double from each stream (testing hook): out (n, k). */

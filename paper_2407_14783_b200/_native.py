@@ -232,6 +232,10 @@ SIGNATURES = {
     "qb_rng_poissons": ([_I64, _P, _I32, _P, _P, _P], ctypes.c_int),
     "qb_env_observe": ([_PP(QbParams), _PP(QbEnvBuffers), _I32, _P, _P], ctypes.c_int),
     "qb_env_step_io": ([_PP(QbParams), _I32, _PP(QbTask), _P, _PP(QbEnvBuffers), _PP(QbStepIo), _P], ctypes.c_int),
+    "qb_env_step_graph_create": ([_PP(QbParams), _I32, _PP(QbTask), _P, _PP(QbEnvBuffers), _PP(QbStepIo), _PP(_P)],
+                                 ctypes.c_int),
+    "qb_env_step_graph_launch": ([_P, _I32, _P], ctypes.c_int),
+    "qb_env_step_graph_destroy": ([_P], ctypes.c_int),
 }
 
 _lib = None

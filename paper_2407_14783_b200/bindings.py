@@ -44,6 +44,9 @@ from . import _native as nat
 from .errors import ActionShapeMismatch, ConfigError, NotReset, SpawnFailure
 
 
+GRAPH_MAX_AGENTS = 4096  # batches up to this size replay a reused-buffer step as a CUDA graph
+
+
 class HandleClosed(RuntimeError):
     """A call on a handle after close()."""
 
@@ -177,11 +180,34 @@ class FlatEnv:
         self._io.copies = ctypes.cast(self._copies, ctypes.c_void_p)
         self._reset_done = False
         self._cache = None  # (out dict, its error-count view, the step result built on it)
+        self._graph = None  # CUDA graph of the cached step (small batches)
         self._lib = nat.lib()
         self._stream_ptr = ctypes.c_void_p(self._stream.cuda_stream)
         self._step_fn = self._lib.qb_env_step_io
         self._args = (env._P, env._kind, env._task, env.dev_scenes.handle, env._bufs)
         self._io_ref = ctypes.byref(self._io)
+
+    # ------------------------------------------------------------------ step graph
+    def _make_graph(self):
+        import torch
+
+        self._stage = torch.zeros((self.num_agents, 4), dtype=_torch_dtype(self._dt_np), pin_memory=True).numpy()
+        self._io.step = 1
+        self._io.host_action = self._stage.ctypes.data
+        g = ctypes.c_void_p()
+        nat.check(self._lib.qb_env_step_graph_create(*self._args, self._io_ref, ctypes.byref(g)), "qb_env_step_graph_create")
+        self._graph = g
+
+    def _drop_graph(self):
+        if getattr(self, "_graph", None) is not None:
+            self._lib.qb_env_step_graph_destroy(self._graph)
+            self._graph = None
+
+    def __del__(self):
+        try:
+            self._drop_graph()
+        except Exception:
+            pass
 
     # ------------------------------------------------------------------ buffers
     def outputs(self, pinned: bool = True) -> dict:
@@ -207,6 +233,7 @@ class FlatEnv:
     def close(self):
         self._enter()
         try:
+            self._drop_graph()
             self._closed = True
             self.env = None
         finally:
@@ -244,14 +271,23 @@ class FlatEnv:
         cached = self._cache
         if step and out is not None and cached is not None and cached[0] is out:
             # the caller's buffer set of the previous step again: every pointer in the
-            # io block and every returned view is unchanged -- one native call
-            self._io.host_action = actions.ctypes.data
-            nat.check(self._step_fn(*self._args, self._io_ref, self._stream_ptr), "qb_env_step_io")
+            # io block and every returned view is unchanged -- one native call; small
+            # batches (launch-latency-bound) replay the step as a CUDA graph that reads
+            # its actions from a fixed pinned staging buffer
+            if self.num_agents <= GRAPH_MAX_AGENTS:
+                if self._graph is None:
+                    self._make_graph()
+                np.copyto(self._stage, actions)
+                nat.check(self._lib.qb_env_step_graph_launch(self._graph, 1, self._stream_ptr), "qb_env_step_graph_launch")
+            else:
+                self._io.host_action = actions.ctypes.data
+                nat.check(self._step_fn(*self._args, self._io_ref, self._stream_ptr), "qb_env_step_io")
             if cached[1][0] > 0:
                 nfail = int(cached[1][0])
                 env._errors.zero_()
                 raise SpawnFailure(f"{nfail} respawns found no spawn with clearance >= {env.config.min_spawn_clearance}")
             return cached[2]
+        self._drop_graph()
         self._cache = None
         if out is None:  # freshly owned arrays every call (pageable host memory)
             out = {k: np.empty(shape, dtype=dt) for k, _, shape, dt in self._src}

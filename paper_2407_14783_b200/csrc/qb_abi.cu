@@ -567,8 +567,8 @@ int qb_env_observe(const qb_params *p, const qb_env_buffers *b, int32_t n_sensor
     return qb::launch_observe(p, b, n_sensors, sensors, qb::as_stream(stream));
 }
 
-int qb_env_step_io(const qb_params *p, int32_t cmd_kind, const qb_task *task, const qb_scene *s,
-                   const qb_env_buffers *b, const qb_step_io *io, void *stream) {
+static int check_step_io(const qb_params *p, const qb_task *task, const qb_scene *s, const qb_env_buffers *b,
+                         const qb_step_io *io) {
     QB_REQUIRE(p && io, "qb_env_step_io: NULL argument");
     int rc = check_env(task, s, b);
     if (rc) return rc;
@@ -590,10 +590,17 @@ int qb_env_step_io(const qb_params *p, int32_t cmd_kind, const qb_task *task, co
     for (int c = 0; c < io->n_packs; ++c)
         QB_REQUIRE(io->packs[c].bytes >= 0 && (io->packs[c].bytes == 0 || (io->packs[c].src && io->packs[c].dst)),
                    "qb_env_step_io: bad pack %d", c);
-    cudaStream_t st = qb::as_stream(stream);
+    QB_REQUIRE(!io->step || (io->host_action && b->action),
+               "qb_env_step_io: host_action and the device action buffer are required");
+    return QB_OK;
+}
+
+// the step's work, enqueued on st (no synchronisation)
+static int step_io_enqueue(const qb_params *p, int32_t cmd_kind, const qb_task *task, const qb_scene *s,
+                           const qb_env_buffers *b, const qb_step_io *io, cudaStream_t st) {
+    int rc = QB_OK;
     const size_t es = b->dtype == QB_F32 ? 4 : 8;
     if (io->step) {
-        QB_REQUIRE(io->host_action && b->action, "qb_env_step_io: host_action and the device action buffer are required");
         // pinned (page-locked) host actions are read by the step kernel itself
         // through their device mapping (one 16 B load per env over PCIe) instead
         // of a separate H2D copy; pageable ones are copied into b->action
@@ -643,6 +650,16 @@ int qb_env_step_io(const qb_params *p, int32_t cmd_kind, const qb_task *task, co
             return QB_ECUDA;
         }
     }
+    return QB_OK;
+}
+
+int qb_env_step_io(const qb_params *p, int32_t cmd_kind, const qb_task *task, const qb_scene *s,
+                   const qb_env_buffers *b, const qb_step_io *io, void *stream) {
+    int rc = check_step_io(p, task, s, b, io);
+    if (rc) return rc;
+    cudaStream_t st = qb::as_stream(stream);
+    rc = step_io_enqueue(p, cmd_kind, task, s, b, io, st);
+    if (rc) return rc;
     if (io->sync) {
         cudaError_t e = cudaStreamSynchronize(st);
         if (e != cudaSuccess) {
@@ -650,6 +667,66 @@ int qb_env_step_io(const qb_params *p, int32_t cmd_kind, const qb_task *task, co
             return QB_ECUDA;
         }
     }
+    return QB_OK;
+}
+
+struct qb_step_graph {
+    cudaGraphExec_t exec;
+};
+
+int qb_env_step_graph_create(const qb_params *p, int32_t cmd_kind, const qb_task *task, const qb_scene *s,
+                             const qb_env_buffers *b, const qb_step_io *io, qb_step_graph **out) {
+    QB_REQUIRE(out, "qb_env_step_graph_create: NULL out");
+    *out = nullptr;
+    int rc = check_step_io(p, task, s, b, io);
+    if (rc) return rc;
+    if (io->step) {  // the graph reads the actions in place: a fixed pinned staging buffer
+        cudaPointerAttributes attr;
+        const bool pinned = cudaPointerGetAttributes(&attr, io->host_action) == cudaSuccess &&
+                            attr.type == cudaMemoryTypeHost && attr.devicePointer;
+        cudaGetLastError();
+        QB_REQUIRE(pinned, "qb_env_step_graph_create: host_action must be pinned host memory");
+    }
+    cudaStream_t cs;
+    if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) {
+        qb::set_error("qb_env_step_graph_create: %s", cudaGetErrorString(cudaGetLastError()));
+        return QB_ECUDA;
+    }
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    cudaError_t e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed);
+    if (e == cudaSuccess) {
+        rc = step_io_enqueue(p, cmd_kind, task, s, b, io, cs);
+        e = cudaStreamEndCapture(cs, &g);
+        if (rc == QB_OK && e == cudaSuccess) e = cudaGraphInstantiate(&exec, g, 0);
+    }
+    if (g) cudaGraphDestroy(g);
+    cudaStreamDestroy(cs);
+    if (rc) return rc;
+    if (e != cudaSuccess) {
+        qb::set_error("qb_env_step_graph_create: %s", cudaGetErrorString(e));
+        return QB_ECUDA;
+    }
+    *out = new qb_step_graph{exec};
+    return QB_OK;
+}
+
+int qb_env_step_graph_launch(qb_step_graph *g, int32_t sync, void *stream) {
+    QB_REQUIRE(g, "qb_env_step_graph_launch: NULL graph");
+    cudaStream_t st = qb::as_stream(stream);
+    cudaError_t e = cudaGraphLaunch(g->exec, st);
+    if (e == cudaSuccess && sync) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+        qb::set_error("qb_env_step_graph_launch: %s", cudaGetErrorString(e));
+        return QB_ECUDA;
+    }
+    return QB_OK;
+}
+
+int qb_env_step_graph_destroy(qb_step_graph *g) {
+    if (!g) return QB_OK;
+    cudaGraphExecDestroy(g->exec);
+    delete g;
     return QB_OK;
 }
 

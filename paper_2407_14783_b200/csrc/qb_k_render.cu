@@ -550,7 +550,6 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, QB_CULL_MINB)
     __shared__ float4 rec_s[CULL_WARPS][CREC][4];      // shading records (warp-broadcast reads)
     __shared__ int2 met_s[CULL_WARPS][CREC];           // (record type, object id)
     __shared__ float cul_s[CULL_WARPS][13][CREC];      // culling bounds, SoA (conflict-free lane-parallel reads)
-    __shared__ unsigned tmask_s[EXACT ? CULL_WARPS : 1][EXACT ? CREC : 1];  // EXACT: tile columns | rows << 8 per record
     __shared__ float4 tpl_s[TPL_MAX][2];               // per-tile camera-space planes (xl xr yt yb) (iL iR iT iB)
     const int wib = threadIdx.x >> 5;
     int *cand = cand_s[wib];
@@ -732,6 +731,8 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, QB_CULL_MINB)
         // the same tests are run once per camera for the 8 columns and 8 rows (32
         // planes) and kept as two 8-bit masks per record -- a tile's test becomes two
         // bit lookups, with bit-identical decisions
+        static_assert(CREC <= 64, "the EXACT tile masks live in two registers per lane");
+        unsigned tm0 = 0, tm1 = 0;  // EXACT: the tile masks of records lane and lane + 32, in registers
         if (EXACT) {
             const int nrec = min(ncand, CREC);
             for (int b = 0; b < nrec; b += 32) {
@@ -762,10 +763,12 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, QB_CULL_MINB)
                                     sB = (fabsf(yb * a0z - a0y) + fabsf(yb * a1z - a1y) + fabsf(yb * a2z - a2y)) * iB;
                         if ((dT + sT + rr >= -CULL_EPS) && (dB + sB + rr >= -CULL_EPS)) msk |= 1u << (8 + q);
                     }
-                    tmask_s[EXACT ? wib : 0][EXACT ? k : 0] = msk;
+                    if (b == 0) tm0 = msk; else tm1 = msk;
                 }
             }
-            __syncwarp();
+            // records beyond the budget (no culling data): every tile; none past ncand
+            if (lane >= nrec && lane < ncand) tm0 = 0xffffu;
+            if (lane + 32 >= nrec && lane + 32 < ncand) tm1 = 0xffffu;
         }
         int cnt = 0, sum_col = 0, sum_row = 0;
         __syncwarp();
@@ -837,14 +840,8 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, QB_CULL_MINB)
                 const int k = b + lane;
                 bool kp = false;
                 if (EXACT) {
-                    if (k < ncand) {
-                        if (k < CREC) {
-                            const unsigned msk = tmask_s[EXACT ? wib : 0][EXACT ? k : 0];
-                            kp = ((msk >> (tl & 7)) & (msk >> (8 + (tl >> 3))) & 1u) != 0;
-                        } else {
-                            kp = true;
-                        }
-                    }
+                    const unsigned msk = b == 0 ? tm0 : (b == 32 ? tm1 : (k < ncand ? 0xffffu : 0u));
+                    kp = ((msk >> (tl & 7)) & (msk >> (8 + (tl >> 3))) & 1u) != 0;
                 } else if (k < ncand) {
                     if (k < CREC) {
                         // support = r + sum_k |n . A'_k|; L/R normals (+-1, 0, z), T/B (0, +-1, z)

@@ -147,7 +147,7 @@ __device__ float4 g_dbg_log[8192];
 // EXACT: 64x64 frame, depth + segmentation, no swarm spheres; CENT: inline
 // pad centroid; S1: split == 1 -- compile-time switches of the common
 // launches (config 5: EXACT + CENT + S1), as in the culling renderer
-template <bool FROM_STATE, bool EXACT = false, bool CENT = false, bool S1 = false>
+template <bool FROM_STATE, bool EXACT = false, bool CENT = false, bool S1 = false, bool SEGP = true>
 __global__ void __launch_bounds__(QB_RF_BLOCK, QB_RF_MINB) k_render_f(DevScene S, CamF cam, long long n, long long ld, const float *state,
                                                      const float *origins, const float *rotations, const int32_t *env_scene,
                                                      float *depth, int32_t *seg, int centroid_id, float *centroid,
@@ -442,7 +442,7 @@ __global__ void __launch_bounds__(QB_RF_BLOCK, QB_RF_MINB) k_render_f(DevScene S
             if (valid) {
                 const long long off = (c * H + i) * (long long)W + j;
                 if (EXACT || depth) depth[off] = t > 0.0f ? t * rsqrtf(n2) : cam.max_range;
-                if (EXACT || seg) seg[off] = out_id;
+                if (EXACT ? SEGP : seg != nullptr) seg[off] = out_id;
                 if ((EXACT ? CENT : centroid_id > 0) && out_id == centroid_id) {
                     cnt += 1;
                     sum_col += j;
@@ -537,7 +537,7 @@ __device__ __forceinline__ float slab_hit(float nlx, float nly, float nlz, float
 // S1: split == 1 (large batches: one warp per camera, cameras grid-strided).
 // EXTRA: swarm spheres present (separate instance: no swarm shared memory or
 // registers in the common case)
-template <bool FROM_STATE, bool EXTRA, bool CENT, bool EXACT, bool S1>
+template <bool FROM_STATE, bool EXTRA, bool CENT, bool EXACT, bool S1, bool SEGP = true>
 __global__ void __launch_bounds__(CULL_WARPS * 32, QB_CULL_MINB)
     k_render_cull(DevScene S, CamF cam, long long n, long long ld, const float *state, const float *origins,
                   const float *rotations, const int32_t *env_scene, float *depth, int32_t *seg, int centroid_id,
@@ -733,7 +733,9 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, QB_CULL_MINB)
         // bit lookups, with bit-identical decisions
         static_assert(CREC <= 64, "the EXACT tile masks live in two registers per lane");
         unsigned tm0 = 0, tm1 = 0;  // EXACT: the tile masks of records lane and lane + 32, in registers
-        if (EXACT) {
+        // (only when one warp renders all 64 tiles of the camera: a warp that takes
+        // a few tiles of a split camera is better off testing its tiles directly)
+        if (EXACT && S1) {
             const int nrec = min(ncand, CREC);
             for (int b = 0; b < nrec; b += 32) {
                 const int k = b + lane;
@@ -839,7 +841,7 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, QB_CULL_MINB)
             for (int b = 0; b < ncand; b += 32) {
                 const int k = b + lane;
                 bool kp = false;
-                if (EXACT) {
+                if (EXACT && S1) {
                     const unsigned msk = b == 0 ? tm0 : (b == 32 ? tm1 : (k < ncand ? 0xffffu : 0u));
                     kp = ((msk >> (tl & 7)) & (msk >> (8 + (tl >> 3))) & 1u) != 0;
                 } else if (k < ncand) {
@@ -971,7 +973,7 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, QB_CULL_MINB)
                 if (EXACT || (j < W && i < H)) {
                     const int off = i * W + j;
                     if (EXACT || depth_c) depth_c[off] = t > 0.0f ? t * czv[u] : cam.max_range;
-                    if (EXACT || seg_c) seg_c[off] = out_id;
+                    if (EXACT ? SEGP : seg_c != nullptr) seg_c[off] = out_id;
                     if (CENT && out_id == centroid_id) {
                         cnt += 1;
                         sum_col += j;
@@ -1097,6 +1099,45 @@ __global__ void k_raycast(DevScene S, const int32_t *env_scene, long long n, con
 
 }  // namespace
 
+namespace {
+struct CullLaunch {
+    const qb_scene *s;
+    CamF c;
+    long long n, ld;
+    const float *state, *origins, *rotations;
+    const int32_t *env_scene;
+    float *depth;
+    int32_t *seg;
+    int centroid_id;
+    float *centroid;
+    const float *extra;
+    const int32_t *extra_ids;
+    int n_extra, split, blocks, B;
+    cudaStream_t st;
+    bool exact;
+};
+
+template <bool FS, bool EX, bool CE, bool EXACT, bool S1, bool SEGP> void cull_kernel(const CullLaunch &L) {
+    k_render_cull<FS, EX, CE, EXACT, S1, SEGP><<<L.blocks, L.B, 0, L.st>>>(
+        L.s->dev, L.c, L.n, L.ld, FS ? L.state : nullptr, FS ? nullptr : L.origins, FS ? nullptr : L.rotations,
+        L.env_scene, L.depth, L.seg, FS ? L.centroid_id : 0, FS ? L.centroid : nullptr, L.extra, L.extra_ids, L.n_extra,
+        L.split);
+}
+
+// compile-time variants: 64x64 frames (EXACT) with / without segmentation, split == 1
+template <bool FS, bool EX, bool CE> void launch_cull(const CullLaunch &L) {
+    if (L.exact && L.split == 1) {
+        if (L.seg) cull_kernel<FS, EX, CE, true, true, true>(L);
+        else cull_kernel<FS, EX, false, true, true, false>(L);
+    } else if (L.exact) {
+        if (L.seg) cull_kernel<FS, EX, CE, true, false, true>(L);
+        else cull_kernel<FS, EX, false, true, false, false>(L);
+    } else {
+        cull_kernel<FS, EX, CE, false, false, true>(L);
+    }
+}
+}  // namespace
+
 namespace qb {
 
 int launch_render(const qb_scene *s, const qb_camera *cam, int dtype, long long n, long long ld, const void *state,
@@ -1130,37 +1171,20 @@ int launch_render(const qb_scene *s, const qb_camera *cam, int dtype, long long 
             long long blocks = (n * split + CULL_WARPS - 1) / CULL_WARPS;
             long long max_blocks = (long long)sm_count() * 16;
             if (blocks > max_blocks) blocks = max_blocks;
-#define QB_CULL(FS, EX, CE)                                                                                         \
-    if (exact && split == 1)                                                                                            \
-        k_render_cull<FS, EX, CE, true, true><<<(int)blocks, B, 0, st>>>(s->dev, c, n, ld, FS ? (const float *)state : nullptr, \
-                                                         FS ? nullptr : (const float *)origins,                         \
-                                                         FS ? nullptr : (const float *)rotations, env_scene, (float *)depth, \
-                                                         seg, FS ? centroid_id : 0, FS ? centroid : nullptr,             \
-                                                         (const float *)extra, extra_ids, n_extra, split);               \
-    else if (exact)                                                                                                     \
-        k_render_cull<FS, EX, CE, true, false><<<(int)blocks, B, 0, st>>>(s->dev, c, n, ld, FS ? (const float *)state : nullptr, \
-                                                         FS ? nullptr : (const float *)origins,                         \
-                                                         FS ? nullptr : (const float *)rotations, env_scene, (float *)depth, \
-                                                         seg, FS ? centroid_id : 0, FS ? centroid : nullptr,             \
-                                                         (const float *)extra, extra_ids, n_extra, split);               \
-    else                                                                                                                \
-    k_render_cull<FS, EX, CE, false, false><<<(int)blocks, B, 0, st>>>(s->dev, c, n, ld, FS ? (const float *)state : nullptr, \
-                                                         FS ? nullptr : (const float *)origins,                         \
-                                                         FS ? nullptr : (const float *)rotations, env_scene, (float *)depth, \
-                                                         seg, FS ? centroid_id : 0, FS ? centroid : nullptr,             \
-                                                         (const float *)extra, extra_ids, n_extra, split)
             const bool cent = state && centroid_id > 0 && split == 1;  // inline centroid (else the k_centroid pass)
-            const bool exact = depth && seg && c.W == 64 && c.H == 64;
+            const bool exact = depth && c.W == 64 && c.H == 64;
+            const CullLaunch L{s, c, n, ld, (const float *)state, (const float *)origins, (const float *)rotations,
+                               env_scene, (float *)depth, seg, centroid_id, centroid, (const float *)extra, extra_ids,
+                               n_extra, split, (int)blocks, B, st, exact};
             if (state) {
                 if (n_extra > 0) {
-                    if (cent) QB_CULL(true, true, true); else QB_CULL(true, true, false);
+                    if (cent) launch_cull<true, true, true>(L); else launch_cull<true, true, false>(L);
                 } else {
-                    if (cent) QB_CULL(true, false, true); else QB_CULL(true, false, false);
+                    if (cent) launch_cull<true, false, true>(L); else launch_cull<true, false, false>(L);
                 }
             } else {
-                if (n_extra > 0) QB_CULL(false, true, false); else QB_CULL(false, false, false);
+                if (n_extra > 0) launch_cull<false, true, false>(L); else launch_cull<false, false, false>(L);
             }
-#undef QB_CULL
             int rc = check_launch("render_cull_f32");
             if (rc || split == 1 || centroid_id <= 0) return rc;
             k_centroid<<<env_grid(n, 128), 128, 0, st>>>(n, c.W, c.H, seg, centroid_id, centroid);
@@ -1181,17 +1205,19 @@ int launch_render(const qb_scene *s, const qb_camera *cam, int dtype, long long 
         if (split > 1 && !seg && centroid_id > 0) split = 1;  // the centroid pass reads seg
         long long blocks = (n * split * 32 + B - 1) / B;
         if (blocks > 0x7fffffffLL) blocks = 0x7fffffffLL;  // grid-stride loop covers the rest
-        const bool exact = state && depth && seg && n_extra == 0 && c.W == 64 && c.H == 64;
+        const bool exact = state && depth && n_extra == 0 && c.W == 64 && c.H == 64;
         if (exact) {
-#define QB_RF_X(CE, S1_)                                                                                              \
-    k_render_f<true, true, CE, S1_><<<(int)blocks, B, 0, st>>>(s->dev, c, n, ld, (const float *)state, nullptr, nullptr, \
-                                                                env_scene, (float *)depth, seg, centroid_id, centroid,   \
-                                                                nullptr, nullptr, 0, split)
-            const bool ce = centroid_id > 0;
-            if (split == 1) {
-                if (ce) QB_RF_X(true, true); else QB_RF_X(false, true);
+#define QB_RF_X(CE, S1_, SG)                                                                                          \
+    k_render_f<true, true, CE, S1_, SG><<<(int)blocks, B, 0, st>>>(s->dev, c, n, ld, (const float *)state, nullptr,     \
+                                                                    nullptr, env_scene, (float *)depth, seg,          \
+                                                                    centroid_id, centroid, nullptr, nullptr, 0, split)
+            const bool ce = centroid_id > 0 && seg;
+            if (!seg) {
+                if (split == 1) QB_RF_X(false, true, false); else QB_RF_X(false, false, false);
+            } else if (split == 1) {
+                if (ce) QB_RF_X(true, true, true); else QB_RF_X(false, true, true);
             } else {
-                if (ce) QB_RF_X(true, false); else QB_RF_X(false, false);
+                if (ce) QB_RF_X(true, false, true); else QB_RF_X(false, false, true);
             }
 #undef QB_RF_X
         } else if (state)

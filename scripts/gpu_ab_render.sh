@@ -7,6 +7,6 @@ for r in 1 2 3; do
     python -c "
 import json
 l=[x for x in open('gpurun_out/ab_$v.log') if x.startswith('{')]
-d=json.loads(l[-1]); print('$v', 'value %.4g'%d['value'], 'render %.4f ms'%d['kernel_ms']['render_k2'], 'step %.4f'%d['ms_per_step'])"
+d=json.loads(l[-1]); print('$v', 'value %.4g'%d['value'], 'render %.4f ms'%d.get('kernel_ms', {}).get('render_k2', -1), 'step %.4f'%d['ms_per_step'])"
   done
 done

@@ -133,10 +133,16 @@ class Info(Sequence):
 
     _KEYS = ("success", "collision", "out_of_bounds", "nonfinite", "nearest_distance", "scene", "step")
 
-    def __init__(self, data: dict, n: int):
-        self.data = data
+    def __init__(self, data, n: int):
+        self._data = data  # a dict, or a callable building it on first use (per-step views are not free)
         self._n = n
         self._host = None
+
+    @property
+    def data(self) -> dict:
+        if callable(self._data):
+            self._data = self._data()
+        return self._data
 
     def __len__(self):
         return self._n
@@ -213,6 +219,9 @@ class QuadEnvBase:
         self.sim = sim if sim is not None else SimConfig()
         self.gains = gains if gains is not None else ControllerGains()
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        if self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
+        self._dev_idx = self.device.index
         self.dtype = dtype or torch.float32
         rank, world = shard
         total = config.num_agents
@@ -240,6 +249,28 @@ class QuadEnvBase:
         self._post_stream = None
 
     # ------------------------------------------------------------------ setup
+    def _cur_stream(self):
+        """The device's current torch Stream, re-fetched only when the raw
+        current stream changed (torch.cuda.current_stream() costs ~10 us)."""
+        import torch
+
+        raw = torch._C._cuda_getCurrentRawStream(self._dev_idx)
+        if raw != getattr(self, "_stream_raw", None):
+            self._stream_obj = torch.cuda.current_stream(self.device)
+            self._stream_raw = raw
+        return self._stream_obj
+
+    def _devctx(self):
+        """torch.cuda.device(self.device) unless it is already current (the
+        context manager costs several microseconds per step)."""
+        import contextlib
+
+        import torch
+
+        if torch._C._cuda_getDevice() == self._dev_idx:
+            return contextlib.nullcontext()
+        return torch.cuda.device(self.device)
+
     def _has_custom_hooks(self) -> bool:
         # a user subclass overriding the Lst-1 hooks gets them called after
         # the fused kernel (flags are then recombined on the device)
@@ -258,10 +289,12 @@ class QuadEnvBase:
         # refilled once the device has consumed its previous copy (event), so
         # a host loop may run ahead of the GPU without corrupting actions
         self._action_host = [torch.zeros((n, 4), dtype=dt, pin_memory=True) for _ in range(2)]
+        self._action_host_np = [b.numpy() for b in self._action_host]  # (host-side writes without torch ops)
         self._action_host_ev = [None, None]
         self._action_host_i = 0
         # per-step outputs in ONE allocation: a StepResult snapshots them with one copy
         self._outblk = z(self._outblk_bytes(n))
+        self._outblk_lay = self._outblk_layout(n)[0]
         self._out_views(self._outblk, self)
         self._reset_counts = z(n, dtype=torch.int32)
         self._rng = z(n, 4, dtype=torch.int64)
@@ -481,10 +514,10 @@ class QuadEnvBase:
         if self._action_host_ev[k] is not None:
             self._action_host_ev[k].synchronize()
         buf = self._action_host[k]
-        buf.copy_(torch.as_tensor(np.asarray(arr), dtype=self.dtype))
+        np.copyto(self._action_host_np[k], np.asarray(arr), casting="unsafe")
         self._action.copy_(buf, non_blocking=True)
         ev = self._action_host_ev[k] or torch.cuda.Event()
-        ev.record()
+        ev.record(self._cur_stream())
         self._action_host_ev[k] = ev
         return self._action
 
@@ -499,7 +532,7 @@ class QuadEnvBase:
         self._check_async_errors()
         a = self._stage_action(action)
         self._bufs.action = a.data_ptr()
-        with torch.cuda.device(self.device):
+        with self._devctx():
             if self.split_step:
                 join = self._launch_split_dynamics()
                 try:
@@ -519,16 +552,22 @@ class QuadEnvBase:
             truncated = ~terminated & (self.step_counts >= self.config.episode_max_steps)
             self._needs_respawn.copy_((terminated | truncated).to(torch.uint8))
         # this step's outputs, snapshotted with one device copy: the reference
-        # returns fresh arrays per step (base.py:186-210)
-        snap = self._out_views(self._outblk.clone(), _Snapshot())
+        # returns fresh arrays per step (base.py:186-210); the Info views are
+        # built on first use
+        blk = self._outblk.clone()
+        n = self.num_agents
+        lay = self._outblk_lay
+        flags = blk[lay["flags"][0]:lay["flags"][1]].view(7, n).view(torch.bool)
         if not self._custom_hooks:
-            success, reward = snap._success.view(torch.bool), snap._reward
-            terminated, truncated = snap._terminated.view(torch.bool), snap._truncated.view(torch.bool)
-        info = Info({"success": success, "collision": snap._collision.view(torch.bool),
-                     "out_of_bounds": snap._oob.view(torch.bool), "nonfinite": snap._nonfinite.view(torch.bool),
-                     "nearest_distance": snap.nearest_dist, "scene": snap.agent_scene, "step": snap.step_counts},
-                    self.num_agents)
-        return StepResult(obs, reward, terminated, truncated, info)
+            success, reward = flags[3], blk[lay["reward"][0]:lay["reward"][1]].view(torch.float32)
+            terminated, truncated = flags[1], flags[2]
+
+        def info_views(blk=blk, flags=flags, success=success):
+            snap = self._out_views(blk, _Snapshot())
+            return {"success": success, "collision": flags[4], "out_of_bounds": flags[5], "nonfinite": flags[6],
+                    "nearest_distance": snap.nearest_dist, "scene": snap.agent_scene, "step": snap.step_counts}
+
+        return StepResult(obs, reward, terminated, truncated, Info(info_views, n))
 
     def _record_async_errors(self):
         import torch
@@ -537,7 +576,7 @@ class QuadEnvBase:
             self._err_host = torch.zeros(1, dtype=torch.int32, pin_memory=True)
             self._err_event = torch.cuda.Event()
         self._err_host.copy_(self._errors, non_blocking=True)
-        self._err_event.record()
+        self._err_event.record(self._cur_stream())
         self._pending_errors = True
 
     def _check_async_errors(self):

@@ -40,11 +40,15 @@ def _actions(cfg, n, rng):
 
 
 @pytest.mark.parametrize("name,pinned", [("hover", False), ("hover", True), ("nav", False), ("nav", True),
-                                         ("nav_big", False), ("landing", True), ("noisy", False)])
+                                         ("nav_big", False), ("nav_big", True), ("landing", True), ("noisy", False),
+                                         ("noisy", True)])
 def test_bindings_equal_env_step(name, pinned):
     """pinned: actions from page-locked memory (read in place by the step
     kernel) and results into a reused pinned set (small results written by
-    the pack kernel straight into host memory)."""
+    the pack kernel straight into host memory); from the second step on the
+    reused set takes the fast path -- a CUDA-graph replay for batches of
+    <= 4096 envs (noise chains and RNG streams included), one native call
+    above."""
     cfg = _cfgs()[name]
     h = bindings.make_env(cfg)
     out = h.outputs() if pinned else None

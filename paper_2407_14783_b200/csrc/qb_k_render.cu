@@ -23,6 +23,8 @@
 
 #include "qb_dynamics.cuh"
 #include "qb_geometry.cuh"
+#include <mutex>
+
 #include "qb_checks.cuh"
 #include "qb_internal.h"
 
@@ -51,6 +53,15 @@ extern "C" int qb_debug_cull_stats(unsigned long long *out) {
 }
 #endif
 
+// dynamic camera scheduling of the culling renderer's large launches: one
+// claim counter per CUDA stream (slot chosen on the host per stream, zeroed
+// in stream order before each launch), so launches on one stream are
+// serialised on their counter and launches on different streams never share
+// one (up to QB_CULL_SLOTS streams; beyond that slots are shared round-robin)
+#ifndef QB_CULL_SLOTS
+#define QB_CULL_SLOTS 256
+#endif
+__device__ unsigned int g_cull_next[QB_CULL_SLOTS];
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
@@ -541,7 +552,8 @@ template <bool FROM_STATE, bool EXTRA, bool CENT, bool EXACT, bool S1, bool SEGP
 __global__ void __launch_bounds__(CULL_WARPS * 32, QB_CULL_MINB)
     k_render_cull(DevScene S, CamF cam, long long n, long long ld, const float *state, const float *origins,
                   const float *rotations, const int32_t *env_scene, float *depth, int32_t *seg, int centroid_id,
-                  float *centroid, const float *extra, const int32_t *extra_ids, int n_extra, int split) {
+                  float *centroid, const float *extra, const int32_t *extra_ids, int n_extra, int split,
+                  unsigned int *claim) {
     __shared__ int cand_s[CULL_WARPS][CULL_MAX];
     constexpr int XM = EXTRA ? XMAX : 1;
     __shared__ float rws_s[CULL_WARPS][9];               // camera rotation for the tile loop (out of registers)
@@ -585,7 +597,10 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, QB_CULL_MINB)
 
     // small batches: `split` warps share one camera, each taking every split-th tile
     if (S1) split = 1;
-    for (long long wi = warp; wi < n * split; wi += nwarps) {
+    // large batches (S1): after its first camera a warp claims the next
+    // unclaimed one from the launch's counter -- per-camera costs vary (a wall
+    // at 1 m vs a cluttered room), and static striding left SMs idle at the end
+    for (long long wi = warp; wi < n * split;) {
         const long long c = S1 ? wi : wi / split;
         const int part = S1 ? 0 : (int)(wi % split);
         float o[3], Rw[9];
@@ -995,6 +1010,13 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, QB_CULL_MINB)
             }
         }
         __syncwarp();
+        if (S1 && claim) {
+            long long nx = 0;
+            if (lane == 0) nx = (long long)atomicAdd(claim, 1u) + nwarps;
+            wi = __shfl_sync(FULL, nx, 0);
+        } else {
+            wi += nwarps;
+        }
     }
 }
 
@@ -1117,11 +1139,51 @@ struct CullLaunch {
     bool exact;
 };
 
+// the claim counter of a stream (host side: a small stream -> slot table)
+unsigned int *claim_counter(cudaStream_t st) {
+    static std::mutex mu;
+    static cudaStream_t keys[QB_CULL_SLOTS];
+    static int used = 0;
+    int slot = -1;
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        for (int i = 0; i < used; ++i)
+            if (keys[i] == st) slot = i;
+        if (slot < 0) {
+            slot = used < QB_CULL_SLOTS ? used++ : (int)(reinterpret_cast<uintptr_t>(st) % QB_CULL_SLOTS);
+            keys[slot] = st;
+        }
+    }
+    // the array's address on the current device, looked up once per device (also
+    // keeps the lookup out of stream captures after the first launch)
+    static void *base_of[64] = {nullptr};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    void *base = dev < 64 ? base_of[dev] : nullptr;
+    if (!base) {
+        if (cudaGetSymbolAddress(&base, g_cull_next) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;  // (static striding)
+        }
+        std::lock_guard<std::mutex> lock(mu);
+        if (dev < 64) base_of[dev] = base;
+    }
+    return static_cast<unsigned int *>(base) + slot;
+}
+
 template <bool FS, bool EX, bool CE, bool EXACT, bool S1, bool SEGP> void cull_kernel(const CullLaunch &L) {
+    unsigned int *claim = nullptr;
+    if (S1) {
+        claim = claim_counter(L.st);
+        if (claim && cudaMemsetAsync(claim, 0, sizeof(unsigned int), L.st) != cudaSuccess) {
+            cudaGetLastError();
+            claim = nullptr;
+        }
+    }
     k_render_cull<FS, EX, CE, EXACT, S1, SEGP><<<L.blocks, L.B, 0, L.st>>>(
         L.s->dev, L.c, L.n, L.ld, FS ? L.state : nullptr, FS ? nullptr : L.origins, FS ? nullptr : L.rotations,
         L.env_scene, L.depth, L.seg, FS ? L.centroid_id : 0, FS ? L.centroid : nullptr, L.extra, L.extra_ids, L.n_extra,
-        L.split);
+        L.split, claim);
 }
 
 // compile-time variants: 64x64 frames (EXACT) with / without segmentation, split == 1

@@ -341,7 +341,11 @@ typedef struct qb_step_io {
  * actions to host results: H2D of the actions, the fused env step
  * (qb_env_step), every view's render, the sensor pass, one pack kernel (state
  * rows + gathers), the uint8 segmentation copies, then the D2H copies.  Not
- * for swarm tasks. */
+ * for swarm tasks.  Batches of >= 16,384 envs without a sensor pass render in
+ * 8 camera slices; a copy that reads one whole per-camera output of a view
+ * (depth, seg, seg_u8) is issued per slice on a side stream as soon as the
+ * slice is rendered, so the PCIe read-back overlaps the remaining renders
+ * (the caller's stream waits for it; results are identical). */
 int qb_env_step_io(const qb_params *p, int32_t cmd_kind, const qb_task *task, const qb_scene *s,
                    const qb_env_buffers *b, const qb_step_io *io, void *stream);
 

@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "qb_internal.h"
@@ -595,6 +596,64 @@ static int check_step_io(const qb_params *p, const qb_task *task, const qb_scene
     return QB_OK;
 }
 
+// Large batches overlap the frames' read-back with the renders: the cameras
+// are rendered in IO_CHUNKS slices on the caller's stream and each slice's
+// D2H copies run on a side stream as soon as the slice is done, so PCIe (the
+// bound for a host-side consumer: ~56 GB/s against the ~500 GB/s of frames
+// the renderer produces) starts after the first slice instead of after the
+// whole batch.  Frames are per camera, so a slice's output is bit-identical.
+namespace {
+constexpr int IO_CHUNKS = 8;
+constexpr long long IO_CHUNK_MIN = 2048;  // cameras per slice at least
+constexpr int IO_MAX_DEV = 64;
+struct IoSide {
+    cudaStream_t st = nullptr;
+    cudaEvent_t ev[IO_CHUNKS + 1] = {};
+};
+std::mutex g_io_mu;  // guards g_io_side and orders the event reuse of concurrent callers
+IoSide g_io_side[IO_MAX_DEV];
+
+// bytes per camera of copy cp when it reads one whole per-camera output of a view, else 0
+long long per_camera_bytes(const qb_io_copy &cp, const qb_step_io *io, long long n, size_t es) {
+    for (int v = 0; v < io->n_views; ++v) {
+        const qb_io_view &vw = io->views[v];
+        const long long hw = (long long)vw.cam.width * vw.cam.height;
+        const long long cands[3][2] = {{(long long)(uintptr_t)vw.depth, hw * (long long)es},
+                                       {(long long)(uintptr_t)vw.seg_u8, hw},
+                                       {(long long)(uintptr_t)vw.seg, hw * 4}};
+        for (auto &c : cands)
+            if (c[0] && (long long)(uintptr_t)cp.src == c[0] && cp.bytes == n * c[1]) return c[1];
+    }
+    return 0;
+}
+}  // namespace
+
+static int io_fail(const char *what, cudaError_t e) {
+    qb::set_error("qb_env_step_io: %s: %s", what, cudaGetErrorString(e));
+    return QB_ECUDA;
+}
+
+// renders (+ uint8 narrowing) of cameras [c0, c1) of every view
+static int io_render_slice(const qb_scene *s, const qb_env_buffers *b, const qb_step_io *io, long long c0, long long c1,
+                           cudaStream_t st) {
+    const size_t es = b->dtype == QB_F32 ? 4 : 8;
+    for (int v = 0; v < io->n_views; ++v) {
+        const qb_io_view &vw = io->views[v];
+        const long long hw = (long long)vw.cam.width * vw.cam.height;
+        int rc = qb::launch_render(
+            s, &vw.cam, b->dtype, c1 - c0, b->ld, static_cast<const char *>(b->state) + c0 * es, nullptr, nullptr,
+            b->agent_scene ? b->agent_scene + c0 : nullptr, vw.depth ? static_cast<char *>(vw.depth) + c0 * hw * es : nullptr,
+            vw.seg ? vw.seg + c0 * hw : nullptr, vw.centroid_id, vw.centroid ? vw.centroid + 2 * c0 : nullptr, nullptr,
+            nullptr, 0, st);
+        if (rc) return rc;
+        if (vw.seg_u8) {
+            rc = qb::launch_narrow_u8((c1 - c0) * hw, vw.seg + c0 * hw, vw.seg_u8 + c0 * hw, st);
+            if (rc) return rc;
+        }
+    }
+    return QB_OK;
+}
+
 // the step's work, enqueued on st (no synchronisation)
 static int step_io_enqueue(const qb_params *p, int32_t cmd_kind, const qb_task *task, const qb_scene *s,
                            const qb_env_buffers *b, const qb_step_io *io, cudaStream_t st) {
@@ -620,6 +679,58 @@ static int step_io_enqueue(const qb_params *p, int32_t cmd_kind, const qb_task *
         }
         rc = qb::launch_env(1, p, cmd_kind, task, s, &bb, 0, st);
         if (rc) return rc;
+    }
+    // the pipelined read-back (above): no sensor pass (it reads the whole
+    // frames), not under stream capture (the graph path is for small batches)
+    bool slices = io->n_views > 0 && io->n_sensors == 0 && b->n >= IO_CHUNKS * IO_CHUNK_MIN;
+    if (slices) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) slices = false;
+        cudaGetLastError();
+    }
+    bool any_sliced = false;
+    for (int c = 0; slices && c < io->n_copies; ++c) any_sliced |= per_camera_bytes(io->copies[c], io, b->n, es) > 0;
+    if (slices && any_sliced) {
+        int dev = 0;
+        cudaError_t e = cudaGetDevice(&dev);
+        if (e != cudaSuccess || dev < 0 || dev >= IO_MAX_DEV) return io_fail("device", e);
+        std::lock_guard<std::mutex> lk(g_io_mu);
+        IoSide &sd = g_io_side[dev];
+        if (!sd.st) {
+            e = cudaStreamCreateWithFlags(&sd.st, cudaStreamNonBlocking);
+            for (int k = 0; e == cudaSuccess && k <= IO_CHUNKS; ++k)
+                e = cudaEventCreateWithFlags(&sd.ev[k], cudaEventDisableTiming);
+            if (e != cudaSuccess) return io_fail("side stream", e);
+        }
+        for (int j = 0; j < IO_CHUNKS; ++j) {
+            const long long c0 = b->n * j / IO_CHUNKS, c1 = b->n * (j + 1) / IO_CHUNKS;
+            rc = io_render_slice(s, b, io, c0, c1, st);
+            if (rc) return rc;
+            if ((e = cudaEventRecord(sd.ev[j], st)) != cudaSuccess || (e = cudaStreamWaitEvent(sd.st, sd.ev[j], 0)) != cudaSuccess)
+                return io_fail("slice event", e);
+            for (int c = 0; c < io->n_copies; ++c) {
+                const qb_io_copy &cp = io->copies[c];
+                const long long pc = per_camera_bytes(cp, io, b->n, es);
+                if (!pc) continue;
+                e = cudaMemcpyAsync(static_cast<char *>(cp.dst) + c0 * pc, static_cast<const char *>(cp.src) + c0 * pc,
+                                    (size_t)((c1 - c0) * pc), cudaMemcpyDeviceToHost, sd.st);
+                if (e != cudaSuccess) return io_fail("result copy", e);
+            }
+        }
+        if (io->state_rows || io->n_packs) {
+            rc = qb::launch_io_pack(b->dtype, b->n, b->ld, b->state, io->state_rows, io->n_packs, io->packs, st);
+            if (rc) return rc;
+        }
+        for (int c = 0; c < io->n_copies; ++c) {
+            const qb_io_copy &cp = io->copies[c];
+            if (!cp.bytes || per_camera_bytes(cp, io, b->n, es)) continue;
+            e = cudaMemcpyAsync(cp.dst, cp.src, (size_t)cp.bytes, cudaMemcpyDeviceToHost, st);
+            if (e != cudaSuccess) return io_fail("result copy", e);
+        }
+        if ((e = cudaEventRecord(sd.ev[IO_CHUNKS], sd.st)) != cudaSuccess ||
+            (e = cudaStreamWaitEvent(st, sd.ev[IO_CHUNKS], 0)) != cudaSuccess)
+            return io_fail("join", e);
+        return QB_OK;
     }
     for (int v = 0; v < io->n_views; ++v) {
         const qb_io_view &vw = io->views[v];

@@ -27,8 +27,9 @@ def _cfgs():
         SensorSpec(kind="segmentation", name="segmentation", noise=(NoiseSpec("saltpepper", p=0.02),)),
         SensorSpec(kind="imu", name="imu", noise=(NoiseSpec("normal", sigma=0.05),))))
     return {"hover": EnvConfig(num_agents=100, command_type="ctbr", episode_max_steps=30),
-            "nav": nav, "nav_big": dataclasses.replace(nav, num_agents=12000),
-            "landing": dataclasses.replace(landing_config(64), episode_max_steps=30), "noisy": noisy}
+            "nav": nav, "nav_big": dataclasses.replace(nav, num_agents=16500),
+            "landing": dataclasses.replace(landing_config(64), episode_max_steps=30), "noisy": noisy,
+            "landing_big": dataclasses.replace(landing_config(16400), episode_max_steps=30)}
 
 
 def _actions(cfg, n, rng):
@@ -40,15 +41,17 @@ def _actions(cfg, n, rng):
 
 
 @pytest.mark.parametrize("name,pinned", [("hover", False), ("hover", True), ("nav", False), ("nav", True),
-                                         ("nav_big", False), ("nav_big", True), ("landing", True), ("noisy", False),
-                                         ("noisy", True)])
+                                         ("nav_big", False), ("nav_big", True), ("landing", True), ("landing_big", True),
+                                         ("noisy", False), ("noisy", True)])
 def test_bindings_equal_env_step(name, pinned):
     """pinned: actions from page-locked memory (read in place by the step
     kernel) and results into a reused pinned set (small results written by
     the pack kernel straight into host memory); from the second step on the
     reused set takes the fast path -- a CUDA-graph replay for batches of
     <= 4096 envs (noise chains and RNG streams included), one native call
-    above."""
+    above.  nav_big / landing_big (>= 16,384 envs) take the sliced renders
+    whose read-back overlaps the next slice (ragged slice bounds; the
+    landing centroid per slice)."""
     cfg = _cfgs()[name]
     h = bindings.make_env(cfg)
     out = h.outputs() if pinned else None

@@ -348,8 +348,8 @@ def run_e2e(cfg, rank, world, kind):
             "steps": K, "ms_per_step": dt / K * 1e3, "dtypes": seg,
             "path": "bindings.step(handle, pinned (N,4) actions) -> qb_env_step_io: action read in place, env step, "
                     "render, state rows + flags/reward packed into pinned host memory, images D2H (segmentation as "
-                    "uint8 when every id < 256, lossless; >= 16,384 envs: rendered in 8 camera slices, each "
-                    "slice's D2H overlapping the next slice's render), stream synchronised before returning"}
+                    "uint8 when every id < 256, lossless; >= 4,096 envs: rendered in up to 16 camera slices, each "
+                    "slice's D2H overlapping the next slices' renders), stream synchronised before returning"}
 
 
 def run_e2e_device_obs(env, world, kind, K=50):

@@ -341,8 +341,9 @@ typedef struct qb_step_io {
  * actions to host results: H2D of the actions, the fused env step
  * (qb_env_step), every view's render, the sensor pass, one pack kernel (state
  * rows + gathers), the uint8 segmentation copies, then the D2H copies.  Not
- * for swarm tasks.  Batches of >= 16,384 envs without a sensor pass render in
- * 8 camera slices; a copy that reads one whole per-camera output of a view
+ * for swarm tasks.  Batches of >= 4,096 envs without a sensor pass render in
+ * up to 16 camera slices (>= 2,048 cameras each) alternating over two
+ * streams; a copy that reads one whole per-camera output of a view
  * (depth, seg, seg_u8) is issued per slice on a side stream as soon as the
  * slice is rendered, so the PCIe read-back overlaps the remaining renders
  * (the caller's stream waits for it; results are identical). */

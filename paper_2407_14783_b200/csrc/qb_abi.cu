@@ -3,6 +3,7 @@
 // (host binned-SAH BVH + float/double device copies) and the launch calls.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -597,19 +598,32 @@ static int check_step_io(const qb_params *p, const qb_task *task, const qb_scene
 }
 
 // Large batches overlap the frames' read-back with the renders: the cameras
-// are rendered in IO_CHUNKS slices on the caller's stream and each slice's
+// are rendered in io_slices() slices on the caller's stream and each slice's
 // D2H copies run on a side stream as soon as the slice is done, so PCIe (the
 // bound for a host-side consumer: ~56 GB/s against the ~500 GB/s of frames
 // the renderer produces) starts after the first slice instead of after the
-// whole batch.  Frames are per camera, so a slice's output is bit-identical.
+// whole batch.  Slices alternate between the caller's stream and a second
+// render stream so one slice's last wave (its slowest cameras) runs beside
+// the next slice's first.  Frames are per camera, so a slice's output is
+// bit-identical.
 namespace {
-constexpr int IO_CHUNKS = 8;
+constexpr int IO_CHUNKS_MAX = 32;
 constexpr long long IO_CHUNK_MIN = 2048;  // cameras per slice at least
 constexpr int IO_MAX_DEV = 64;
 struct IoSide {
-    cudaStream_t st = nullptr;
-    cudaEvent_t ev[IO_CHUNKS + 1] = {};
+    cudaStream_t st = nullptr;   // the D2H copies
+    cudaStream_t rs = nullptr;   // odd slices' renders (a slice's tail overlaps the next slice's start)
+    cudaEvent_t ev[IO_CHUNKS_MAX] = {}, ev_step = nullptr, ev_rs = nullptr, ev_done = nullptr;
 };
+// slices per step at most: 16 (QB_IO_SLICES overrides for experiments; 1 = no overlap)
+int io_slices() {
+    static const int v = [] {
+        const char *e = std::getenv("QB_IO_SLICES");
+        const int k = e ? std::atoi(e) : 16;
+        return k < 1 ? 1 : (k > IO_CHUNKS_MAX ? IO_CHUNKS_MAX : k);
+    }();
+    return v;
+}
 std::mutex g_io_mu;  // guards g_io_side and orders the event reuse of concurrent callers
 IoSide g_io_side[IO_MAX_DEV];
 
@@ -682,7 +696,8 @@ static int step_io_enqueue(const qb_params *p, int32_t cmd_kind, const qb_task *
     }
     // the pipelined read-back (above): no sensor pass (it reads the whole
     // frames), not under stream capture (the graph path is for small batches)
-    bool slices = io->n_views > 0 && io->n_sensors == 0 && b->n >= IO_CHUNKS * IO_CHUNK_MIN;
+    const int nsl = (int)std::min<long long>(io_slices(), b->n / IO_CHUNK_MIN);
+    bool slices = nsl > 1 && io->n_views > 0 && io->n_sensors == 0;
     if (slices) {
         cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
         if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) slices = false;
@@ -698,15 +713,22 @@ static int step_io_enqueue(const qb_params *p, int32_t cmd_kind, const qb_task *
         IoSide &sd = g_io_side[dev];
         if (!sd.st) {
             e = cudaStreamCreateWithFlags(&sd.st, cudaStreamNonBlocking);
-            for (int k = 0; e == cudaSuccess && k <= IO_CHUNKS; ++k)
+            if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&sd.rs, cudaStreamNonBlocking);
+            for (int k = 0; e == cudaSuccess && k < IO_CHUNKS_MAX; ++k)
                 e = cudaEventCreateWithFlags(&sd.ev[k], cudaEventDisableTiming);
-            if (e != cudaSuccess) return io_fail("side stream", e);
+            for (cudaEvent_t *x : {&sd.ev_step, &sd.ev_rs, &sd.ev_done})
+                if (e == cudaSuccess) e = cudaEventCreateWithFlags(x, cudaEventDisableTiming);
+            if (e != cudaSuccess) return io_fail("side streams", e);
         }
-        for (int j = 0; j < IO_CHUNKS; ++j) {
-            const long long c0 = b->n * j / IO_CHUNKS, c1 = b->n * (j + 1) / IO_CHUNKS;
-            rc = io_render_slice(s, b, io, c0, c1, st);
+        // the second render stream starts after the env step
+        if ((e = cudaEventRecord(sd.ev_step, st)) != cudaSuccess || (e = cudaStreamWaitEvent(sd.rs, sd.ev_step, 0)) != cudaSuccess)
+            return io_fail("step event", e);
+        for (int j = 0; j < nsl; ++j) {
+            const long long c0 = b->n * j / nsl, c1 = b->n * (j + 1) / nsl;
+            cudaStream_t r = (j & 1) ? sd.rs : st;
+            rc = io_render_slice(s, b, io, c0, c1, r);
             if (rc) return rc;
-            if ((e = cudaEventRecord(sd.ev[j], st)) != cudaSuccess || (e = cudaStreamWaitEvent(sd.st, sd.ev[j], 0)) != cudaSuccess)
+            if ((e = cudaEventRecord(sd.ev[j], r)) != cudaSuccess || (e = cudaStreamWaitEvent(sd.st, sd.ev[j], 0)) != cudaSuccess)
                 return io_fail("slice event", e);
             for (int c = 0; c < io->n_copies; ++c) {
                 const qb_io_copy &cp = io->copies[c];
@@ -727,8 +749,8 @@ static int step_io_enqueue(const qb_params *p, int32_t cmd_kind, const qb_task *
             e = cudaMemcpyAsync(cp.dst, cp.src, (size_t)cp.bytes, cudaMemcpyDeviceToHost, st);
             if (e != cudaSuccess) return io_fail("result copy", e);
         }
-        if ((e = cudaEventRecord(sd.ev[IO_CHUNKS], sd.st)) != cudaSuccess ||
-            (e = cudaStreamWaitEvent(st, sd.ev[IO_CHUNKS], 0)) != cudaSuccess)
+        if ((e = cudaEventRecord(sd.ev_rs, sd.rs)) != cudaSuccess || (e = cudaStreamWaitEvent(st, sd.ev_rs, 0)) != cudaSuccess ||
+            (e = cudaEventRecord(sd.ev_done, sd.st)) != cudaSuccess || (e = cudaStreamWaitEvent(st, sd.ev_done, 0)) != cudaSuccess)
             return io_fail("join", e);
         return QB_OK;
     }

@@ -506,7 +506,13 @@ constexpr int CULL_MAX = 256;   // primitives per scene
 constexpr int CULL_WARPS = QB_CULL_WARPS;  // warps (cameras) per block
 constexpr int XMAX = 32;  // swarm spheres kept per camera after frustum culling (more: every sphere per ray)
 constexpr int CREC = QB_CREC;   // precomputed records per camera (nav room: mean 21, max 58); more use the generic path (56 keeps 6 blocks/SM in shared memory)
-enum { REC_SPHERE = 0, REC_AABB = 1, REC_OBB = 2, REC_GENERIC = 3 };
+// record word rec[k][1].w: a type flag in the top bits over the object id
+// (flag bits, not an enum: an if-chain on distinct bits stays a chain of
+// predicate tests, where an enum compare chain compiles to a jump table --
+// a constant-bank load and an indirect branch per survivor); a record
+// without a flag (triangles, ids >= 2^29) holds its primitive index in
+// rec[k][1].x and takes the generic test
+constexpr unsigned REC_AABB = 1u << 31, REC_OBB = 1u << 30, REC_SPHERE = 1u << 29, REC_ID = REC_SPHERE - 1u;
 
 struct Plane {
     float x, y, z, off;
@@ -560,13 +566,11 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, QB_CULL_MINB)
     __shared__ float4 xcs_s[CULL_WARPS][XM];             // swarm spheres in the frustum: camera-space centre, r
     __shared__ int xk_s[CULL_WARPS][XM];                 // ... and their index k (ascending)
     __shared__ float4 rec_s[CULL_WARPS][CREC][4];      // shading records (warp-broadcast reads)
-    __shared__ int2 met_s[CULL_WARPS][CREC];           // (record type, object id)
     __shared__ float cul_s[CULL_WARPS][13][CREC];      // culling bounds, SoA (conflict-free lane-parallel reads)
     __shared__ float4 tpl_s[TPL_MAX][2];               // per-tile camera-space planes (xl xr yt yb) (iL iR iT iB)
     const int wib = threadIdx.x >> 5;
     int *cand = cand_s[wib];
     float4 (*rec)[4] = rec_s[wib];
-    int2 *met = met_s[wib];
     float (*cul)[CREC] = cul_s[wib];
     const int lane = threadIdx.x & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
@@ -657,7 +661,7 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, QB_CULL_MINB)
                 };
                 const float3 cc = cs(rx, ry, rz), A0 = cs(a0.x, a0.y, a0.z), A1 = cs(a1.x, a1.y, a1.z),
                              A2 = cs(a2.x, a2.y, a2.z);
-                int type = REC_GENERIC;
+                unsigned type = 0;  // generic
                 float4 s0 = make_float4(0.f, 0.f, 0.f, 0.f), s1 = s0, s2 = s0, s3 = s0;
                 const float4 *pr = S.primf + 4 * p;
                 if (mt.x == QB_SPHERE) {
@@ -681,7 +685,9 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, QB_CULL_MINB)
                     s3 = make_float4(pc.z, pe.y, pc.x, pc.w);
                     s1.z = pe.z;
                 }
-                met[k] = make_int2(type, mt.y);
+                if ((unsigned)mt.y > REC_ID) type = 0;  // (the id does not fit the word: generic)
+                s1.w = __uint_as_float(type ? type | (unsigned)mt.y : 0u);
+                if (!type) s1.x = __int_as_float(p);
                 rec[k][0] = s0;
                 rec[k][1] = s1;
                 rec[k][2] = s2;
@@ -888,19 +894,23 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, QB_CULL_MINB)
                     float t[2] = {-1.0f, -1.0f};
                     int oid;
 #ifdef QB_CULL_STATS
-                    if (lane == 0) atomicAdd(&g_cull_stats[3 + (k2 < CREC ? met[k2].x : 3)], 1ull);
+                    if (lane == 0) {
+                        const unsigned tw = k2 < CREC ? __float_as_uint(rec[k2][1].w) : 0u;
+                        atomicAdd(&g_cull_stats[3 + ((tw & REC_SPHERE) ? 0 : (tw & REC_AABB) ? 1 : (tw & REC_OBB) ? 2 : 3)], 1ull);
+                    }
 #endif
+                    int p = -1;  // generic: the primitive's own test
                     if (k2 < CREC) {
-                        const int2 mt2 = met[k2];
-                        const float4 s0 = rec[k2][0];
-                        oid = mt2.y;
-                        if (mt2.x == REC_AABB) {
-                            const float4 s1 = rec[k2][1];
+                        // both words at once: the flag (s1.w) selects the test, no dependent load
+                        const float4 s0 = rec[k2][0], s1 = rec[k2][1];
+                        const unsigned tw = __float_as_uint(s1.w);
+                        oid = (int)(tw & REC_ID);
+                        if (tw & REC_AABB) {
 #pragma unroll
                             for (int u = 0; u < 2; ++u)
                                 t[u] = slab_hit(s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, ix[u], iy[u], iz[u], tmin, best[u]);
-                        } else if (mt2.x == REC_OBB) {
-                            const float4 s1 = rec[k2][1], s2 = rec[k2][2], s3 = rec[k2][3];
+                        } else if (tw & REC_OBB) {
+                            const float4 s2 = rec[k2][2], s3 = rec[k2][3];
                             // local direction = R^T d: columns (s2.x s2.y s2.z) (s2.w s3.x s3.y) (s3.z s3.w s1.z)
 #pragma unroll
                             for (int u = 0; u < 2; ++u) {
@@ -910,7 +920,7 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, QB_CULL_MINB)
                                 t[u] = slab_hit(s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, rcp_approx(lx), rcp_approx(ly),
                                                 rcp_approx(lz), tmin, best[u]);
                             }
-                        } else if (mt2.x == REC_SPHERE) {
+                        } else if (tw & REC_SPHERE) {
 #pragma unroll
                             for (int u = 0; u < 2; ++u) {
                                 const float bb = s0.x * dx[u] + s0.y * dy[u] + s0.z * dz[u];
@@ -923,13 +933,12 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, QB_CULL_MINB)
                                 }
                             }
                         } else {
-#pragma unroll
-                            for (int u = 0; u < 2; ++u)
-                                t[u] = ray_triangle_call(kz, S.primf + 4 * cand[k2], o[0], o[1], o[2], dx[u], dy[u], dz[u], tmin,
-                                                      best[u]);
+                            p = __float_as_int(s1.x);
                         }
                     } else {
-                        const int p = cand[k2];
+                        p = cand[k2];
+                    }
+                    if (p >= 0) {  // triangles, records beyond the budget, ids too large for the word
                         const int2 mt = __ldg(S.meta + p);
                         oid = mt.y;
                         const float4 *pr = S.primf + 4 * p;

@@ -49,7 +49,7 @@ def test_bindings_equal_env_step(name, pinned):
     the pack kernel straight into host memory); from the second step on the
     reused set takes the fast path -- a CUDA-graph replay for batches of
     <= 4096 envs (noise chains and RNG streams included), one native call
-    above.  nav_big / landing_big (>= 16,384 envs) take the sliced renders
+    above.  nav_big / landing_big (8 slices of ~2k envs) take the sliced renders
     whose read-back overlaps the next slice (ragged slice bounds; the
     landing centroid per slice)."""
     cfg = _cfgs()[name]

@@ -306,8 +306,10 @@ typedef struct qb_io_view {
     qb_camera cam;
     void *depth;        /* (n,H,W) dtype */
     int32_t *seg;       /* (n,H,W) int32 object ids */
-    uint8_t *seg_u8;    /* optional (n,H,W) uint8 copy of seg for the host (ids < 256: lossless) */
-    int32_t centroid_id, pad_;
+    void *seg_small;    /* optional (n,H,W) narrowed copy of seg for the host: uint8 or uint16 by
+                           seg_small_bytes (lossless when every id < 256 / 65536) */
+    int32_t centroid_id;
+    int32_t seg_small_bytes; /* 1 (also 0) = uint8, 2 = uint16 */
     float *centroid;    /* (n,2) when centroid_id > 0 */
 } qb_io_view;
 
@@ -340,11 +342,11 @@ typedef struct qb_step_io {
 /* QuadEnvBase.step (base.py:156-210) + get_observation (:287-310) from host
  * actions to host results: H2D of the actions, the fused env step
  * (qb_env_step), every view's render, the sensor pass, one pack kernel (state
- * rows + gathers), the uint8 segmentation copies, then the D2H copies.  Not
+ * rows + gathers), the narrowed segmentation copies, then the D2H copies.  Not
  * for swarm tasks.  Batches of >= 4,096 envs without a sensor pass render in
  * up to 16 camera slices (>= 2,048 cameras each) alternating over two
  * streams; a copy that reads one whole per-camera output of a view
- * (depth, seg, seg_u8) is issued per slice on a side stream as soon as the
+ * (depth, seg, seg_small) is issued per slice on a side stream as soon as the
  * slice is rendered, so the PCIe read-back overlaps the remaining renders
  * (the caller's stream waits for it; results are identical). */
 int qb_env_step_io(const qb_params *p, int32_t cmd_kind, const qb_task *task, const qb_scene *s,

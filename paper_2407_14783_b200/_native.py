@@ -170,9 +170,9 @@ class QbIoView(ctypes.Structure):
         ("cam", QbCamera),
         ("depth", _P),
         ("seg", _P),
-        ("seg_u8", _P),
+        ("seg_small", _P),
         ("centroid_id", ctypes.c_int32),
-        ("pad_", ctypes.c_int32),
+        ("seg_small_bytes", ctypes.c_int32),
         ("centroid", _P),
     ]
 

@@ -11,7 +11,7 @@ boundary:
 Here a handle owns one batched GPU env (`env.make_env`) and a step is ONE
 native call, `qb_env_step_io` (include/quadb200.h): the host actions are
 copied to the device, the fused env step and every camera render run, the
-state rows / uint8 segmentation are packed on the device, and the results are
+state rows / narrowed (uint8 or uint16) segmentation are packed on the device, and the results are
 copied back into host arrays before the call returns.  No torch op runs per
 step, so the host cost of a step is one ctypes call (about 10-20 us at
 100 envs) instead of the batched Python env's tensor bookkeeping.
@@ -23,8 +23,9 @@ Semantics (SPEC.md "bindings"):
     buffers), unless the caller passes `out=` buffers (`handle.outputs()`,
     pinned host memory, reused step after step -- the zero-copy path);
   * float width: state / depth / rewards are float32 (the reference's are
-    float64), segmentation is uint8 when every object id of the scenes fits
-    in a byte and int32 otherwise ("documented float-width conversion");
+    float64), segmentation is uint8 / uint16 when every object id of the
+    scenes fits in one / two bytes and int32 otherwise (lossless; "documented
+    float-width conversion");
   * a handle is single-owner: a call while another call on the same handle
     is running raises; calls after close() raise.
 
@@ -94,7 +95,9 @@ class FlatEnv:
         dt_np = np.float32 if env.dtype == torch.float32 else np.float64
         self._dt_np = dt_np
         max_id = max((int(s.arrays.prim_object_id.max()) if s.arrays.prim_object_id.size else 0) for s in env.scenes)
-        self.seg_dtype = np.uint8 if max_id < 256 else np.int32
+        min_id = min((int(s.arrays.prim_object_id.min()) if s.arrays.prim_object_id.size else 0) for s in env.scenes)
+        # lossless narrowing of the segmentation ids for the read-back (the bytes PCIe carries)
+        self.seg_dtype = (np.int32 if min_id < 0 or max_id >= 65536 else np.uint8 if max_id < 256 else np.uint16)
         # the small per-step results travel as ONE device block and ONE D2H copy:
         # [state rows (n,13) | output block (flags, reward, counters, nearest point) | spawn-failure count]
         es = 4 if dt_np == np.float32 else 8
@@ -123,9 +126,10 @@ class FlatEnv:
                 v.centroid_id = int(cid)
                 v.centroid = nat.ptr(slot["centroid_pair"][0]) if cid else None
                 seg_host = None
-                if seg is not None and self.seg_dtype == np.uint8:
-                    seg_host = torch.zeros(seg.shape, dtype=torch.uint8, device=self._dev)
-                    v.seg_u8 = nat.ptr(seg_host)
+                if seg is not None and self.seg_dtype != np.int32:
+                    w = np.dtype(self.seg_dtype).itemsize
+                    seg_host = torch.zeros(seg.shape, dtype=torch.uint8 if w == 1 else torch.int16, device=self._dev)
+                    v.seg_small, v.seg_small_bytes = nat.ptr(seg_host), w
                 slot["_io"] = {"depth": depth, "seg": seg_host if seg_host is not None else seg,
                                "centroid": slot["centroid_pair"][0] if cid else None}
                 views.append(v)
@@ -216,7 +220,8 @@ class FlatEnv:
         step stay valid until the caller passes the same set again."""
         import torch
 
-        out = {k: torch.empty(shape, dtype=_torch_dtype(dt), pin_memory=pinned).numpy() for k, _, shape, dt in self._src}
+        out = {k: torch.empty(shape, dtype=_torch_dtype(dt), pin_memory=pinned).numpy().view(dt)
+               for k, _, shape, dt in self._src}
         small = torch.empty(self._small_nbytes + 16, dtype=torch.uint8, pin_memory=pinned)
         off = (-small.data_ptr()) % 16  # 16-byte aligned: the pack kernel writes it with vector stores
         out["_small"] = small.numpy()[off:off + self._small_nbytes]
@@ -341,7 +346,7 @@ def _torch_dtype(dt):
     import torch
 
     return {np.dtype(np.float32): torch.float32, np.dtype(np.float64): torch.float64, np.dtype(np.uint8): torch.uint8,
-            np.dtype(np.int32): torch.int32}[np.dtype(dt)]
+            np.dtype(np.uint16): torch.int16, np.dtype(np.int32): torch.int32}[np.dtype(dt)]  # (uint16: same bytes)
 
 
 # ---------------------------------------------------------------- module API (SPEC.md names)

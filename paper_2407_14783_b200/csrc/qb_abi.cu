@@ -582,7 +582,9 @@ static int check_step_io(const qb_params *p, const qb_task *task, const qb_scene
         rc = check_cam(&io->views[v].cam);
         if (rc) return rc;
         QB_REQUIRE(io->views[v].centroid_id <= 0 || io->views[v].centroid, "qb_env_step_io: centroid buffer missing");
-        QB_REQUIRE(!io->views[v].seg_u8 || io->views[v].seg, "qb_env_step_io: seg_u8 needs seg");
+        QB_REQUIRE(!io->views[v].seg_small || io->views[v].seg, "qb_env_step_io: seg_small needs seg");
+        QB_REQUIRE(io->views[v].seg_small_bytes >= 0 && io->views[v].seg_small_bytes <= 2,
+                   "qb_env_step_io: seg_small_bytes must be 1 or 2");
     }
     for (int c = 0; c < io->n_copies; ++c)
         QB_REQUIRE(io->copies[c].bytes >= 0 && (io->copies[c].bytes == 0 || (io->copies[c].src && io->copies[c].dst)),
@@ -627,13 +629,15 @@ int io_slices() {
 std::mutex g_io_mu;  // guards g_io_side and orders the event reuse of concurrent callers
 IoSide g_io_side[IO_MAX_DEV];
 
+int small_bytes(const qb_io_view &vw) { return vw.seg_small_bytes == 2 ? 2 : 1; }
+
 // bytes per camera of copy cp when it reads one whole per-camera output of a view, else 0
 long long per_camera_bytes(const qb_io_copy &cp, const qb_step_io *io, long long n, size_t es) {
     for (int v = 0; v < io->n_views; ++v) {
         const qb_io_view &vw = io->views[v];
         const long long hw = (long long)vw.cam.width * vw.cam.height;
         const long long cands[3][2] = {{(long long)(uintptr_t)vw.depth, hw * (long long)es},
-                                       {(long long)(uintptr_t)vw.seg_u8, hw},
+                                       {(long long)(uintptr_t)vw.seg_small, hw * small_bytes(vw)},
                                        {(long long)(uintptr_t)vw.seg, hw * 4}};
         for (auto &c : cands)
             if (c[0] && (long long)(uintptr_t)cp.src == c[0] && cp.bytes == n * c[1]) return c[1];
@@ -660,8 +664,9 @@ static int io_render_slice(const qb_scene *s, const qb_env_buffers *b, const qb_
             vw.seg ? vw.seg + c0 * hw : nullptr, vw.centroid_id, vw.centroid ? vw.centroid + 2 * c0 : nullptr, nullptr,
             nullptr, 0, st);
         if (rc) return rc;
-        if (vw.seg_u8) {
-            rc = qb::launch_narrow_u8((c1 - c0) * hw, vw.seg + c0 * hw, vw.seg_u8 + c0 * hw, st);
+        if (vw.seg_small) {
+            rc = qb::launch_narrow((c1 - c0) * hw, vw.seg + c0 * hw,
+                                   static_cast<char *>(vw.seg_small) + c0 * hw * small_bytes(vw), small_bytes(vw), st);
             if (rc) return rc;
         }
     }
@@ -770,8 +775,8 @@ static int step_io_enqueue(const qb_params *p, int32_t cmd_kind, const qb_task *
     }
     for (int v = 0; v < io->n_views; ++v) {
         const qb_io_view &vw = io->views[v];
-        if (!vw.seg_u8) continue;
-        rc = qb::launch_narrow_u8((long long)b->n * vw.cam.width * vw.cam.height, vw.seg, vw.seg_u8, st);
+        if (!vw.seg_small) continue;
+        rc = qb::launch_narrow((long long)b->n * vw.cam.width * vw.cam.height, vw.seg, vw.seg_small, small_bytes(vw), st);
         if (rc) return rc;
     }
     for (int c = 0; c < io->n_copies; ++c) {

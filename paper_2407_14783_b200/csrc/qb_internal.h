@@ -84,5 +84,5 @@ int launch_observe(const qb_params *p, const qb_env_buffers *b, int n_sensors, c
                    cudaStream_t st);
 int launch_io_pack(int dtype, long long n, long long ld, const void *planes, void *rows, int n_packs,
                    const qb_io_copy *packs, cudaStream_t st);
-int launch_narrow_u8(long long count, const int32_t *seg, uint8_t *out, cudaStream_t st);
+int launch_narrow(long long count, const int32_t *seg, void *out, int bytes, cudaStream_t st);
 }  // namespace qb

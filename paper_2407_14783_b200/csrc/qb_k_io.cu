@@ -43,27 +43,34 @@ __global__ void __launch_bounds__(256) k_io_pack(long long n, long long ld, cons
     }
 }
 
-// 16 ids -> 16 bytes per thread: four int4 loads, one uint4 store
-__global__ void __launch_bounds__(256) k_narrow_u8(long long count, const int32_t *seg, uint8_t *out) {
-    const long long vec = count / 16;
+// 16 output bytes per thread (16 uint8 or 8 uint16 ids): int4 loads, one uint4 store
+template <typename U>
+__global__ void __launch_bounds__(256) k_narrow(long long count, const int32_t *seg, U *out) {
+    constexpr int PER = 16 / sizeof(U);  // ids per thread
+    const long long vec = count / PER;
     const int4 *src = reinterpret_cast<const int4 *>(seg);
     uint4 *dst = reinterpret_cast<uint4 *>(out);
     for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < vec;
          v += (long long)gridDim.x * blockDim.x) {
         unsigned w[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int4 a = __ldcs(src + 4 * v + q);  // streamed once: do not keep in L2
-            w[q] = (unsigned)(a.x & 0xff) | ((unsigned)(a.y & 0xff) << 8) | ((unsigned)(a.z & 0xff) << 16) |
-                   ((unsigned)(a.w & 0xff) << 24);
+        for (int q = 0; q < PER / 4; ++q) {
+            const int4 a = __ldcs(src + (PER / 4) * v + q);  // streamed once: do not keep in L2
+            if (sizeof(U) == 1) {
+                w[q] = (unsigned)(a.x & 0xff) | ((unsigned)(a.y & 0xff) << 8) | ((unsigned)(a.z & 0xff) << 16) |
+                       ((unsigned)(a.w & 0xff) << 24);
+            } else {
+                w[2 * q] = (unsigned)(a.x & 0xffff) | ((unsigned)(a.y & 0xffff) << 16);
+                w[2 * q + 1] = (unsigned)(a.z & 0xffff) | ((unsigned)(a.w & 0xffff) << 16);
+            }
         }
         dst[v] = make_uint4(w[0], w[1], w[2], w[3]);
     }
-    // tail (count not a multiple of 16)
-    const long long t0 = vec * 16;
+    // tail (count not a multiple of PER)
+    const long long t0 = vec * PER;
     for (long long e = t0 + (long long)blockIdx.x * blockDim.x + threadIdx.x; e < count;
          e += (long long)gridDim.x * blockDim.x)
-        out[e] = (uint8_t)seg[e];
+        out[e] = (U)seg[e];
 }
 
 int stream_grid(long long work, int block) {
@@ -96,15 +103,18 @@ int launch_io_pack(int dtype, long long n, long long ld, const void *planes, voi
     return check_launch("io_pack");
 }
 
-int launch_narrow_u8(long long count, const int32_t *seg, uint8_t *out, cudaStream_t st) {
+int launch_narrow(long long count, const int32_t *seg, void *out, int bytes, cudaStream_t st) {
     if (count == 0) return QB_OK;
     if ((reinterpret_cast<uintptr_t>(seg) & 15) || (reinterpret_cast<uintptr_t>(out) & 15)) {
-        set_error("narrow_u8: seg / seg_u8 must be 16-byte aligned");
+        set_error("narrow: seg / seg_small must be 16-byte aligned");
         return QB_EINVAL;
     }
     const int B = 256;
-    k_narrow_u8<<<stream_grid(count / 16 + 1, B), B, 0, st>>>(count, seg, out);
-    return check_launch("narrow_u8");
+    if (bytes == 2)
+        k_narrow<uint16_t><<<stream_grid(count / 8 + 1, B), B, 0, st>>>(count, seg, static_cast<uint16_t *>(out));
+    else
+        k_narrow<uint8_t><<<stream_grid(count / 16 + 1, B), B, 0, st>>>(count, seg, static_cast<uint8_t *>(out));
+    return check_launch("narrow");
 }
 
 }  // namespace qb

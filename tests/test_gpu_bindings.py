@@ -12,7 +12,8 @@ import pytest
 
 from paper_2407_14783_b200 import bindings
 from paper_2407_14783_b200.control import CTBR, LV
-from paper_2407_14783_b200.env import EnvConfig, SensorSpec, landing_config, make_env, navigation_config
+from paper_2407_14783_b200.env import (DistSpec, EnvConfig, InitRandomization, SceneSpec, SensorSpec, landing_config,
+                                       make_env, navigation_config)
 from paper_2407_14783_b200.errors import ActionShapeMismatch, NotReset
 from paper_2407_14783_b200.sensing import NoiseSpec
 
@@ -29,7 +30,15 @@ def _cfgs():
     return {"hover": EnvConfig(num_agents=100, command_type="ctbr", episode_max_steps=30),
             "nav": nav, "nav_big": dataclasses.replace(nav, num_agents=16500),
             "landing": dataclasses.replace(landing_config(64), episode_max_steps=30), "noisy": noisy,
-            "landing_big": dataclasses.replace(landing_config(16400), episode_max_steps=30)}
+            "landing_big": dataclasses.replace(landing_config(16400), episode_max_steps=30),
+            # config 5's 5e5-triangle hall: object ids up to 509 -> uint16 segmentation
+            "hall": EnvConfig(num_agents=4500, task="landing", command_type="lv", episode_max_steps=30,
+                              scenes=(SceneSpec(kind="indoor", seed=0),),
+                              randomization=InitRandomization(position=DistSpec("uniform", low=[-12, -12, 1.0],
+                                                                                high=[12, 12, 4.5])),
+                              min_spawn_clearance=0.3,
+                              sensors=(SensorSpec(kind="depth", name="depth", orientation="down"),
+                                       SensorSpec(kind="segmentation", name="vision", orientation="down")))}
 
 
 def _actions(cfg, n, rng):
@@ -42,7 +51,7 @@ def _actions(cfg, n, rng):
 
 @pytest.mark.parametrize("name,pinned", [("hover", False), ("hover", True), ("nav", False), ("nav", True),
                                          ("nav_big", False), ("nav_big", True), ("landing", True), ("landing_big", True),
-                                         ("noisy", False), ("noisy", True)])
+                                         ("noisy", False), ("noisy", True), ("hall", False), ("hall", True)])
 def test_bindings_equal_env_step(name, pinned):
     """pinned: actions from page-locked memory (read in place by the step
     kernel) and results into a reused pinned set (small results written by
@@ -51,7 +60,7 @@ def test_bindings_equal_env_step(name, pinned):
     <= 4096 envs (noise chains and RNG streams included), one native call
     above.  nav_big / landing_big (8 slices of ~2k envs) take the sliced renders
     whose read-back overlaps the next slice (ragged slice bounds; the
-    landing centroid per slice)."""
+    landing centroid per slice); hall: uint16 segmentation (ids up to 509)."""
     cfg = _cfgs()[name]
     h = bindings.make_env(cfg)
     out = h.outputs() if pinned else None
@@ -82,6 +91,8 @@ def test_bindings_equal_env_step(name, pinned):
             assert got.shape == want.shape, (t, k)
             if got.dtype == np.uint8:
                 assert want.max() < 256
+            if name == "hall" and k == "vision":
+                assert got.dtype == np.uint16
             assert np.array_equal(got.astype(want.dtype), want), (t, k)
         assert np.array_equal(rew, r.reward.cpu().numpy()), t
         assert np.array_equal(term, r.terminated.cpu().numpy()), t

@@ -285,6 +285,7 @@ __global__ void __launch_bounds__(QB_RF_BLOCK, QB_RF_MINB) k_render_f(DevScene S
             // the triangle test's shear axis: the dominant axis of a ray near the
             // tile centre, warp-uniform (a tile spans ~11 deg, so |d[kz]| >= 0.38)
             const int kz = __shfl_sync(FULL, dominant_axis(dx, dy, dz), 12);
+            const Shear sh = ray_shear(kz, dx, dy, dz);  // per ray, once per tile (not per triangle test)
 
             // lanes outside the image carry best = -1: they never want a box
             float best = valid ? tmax : -1.0f;
@@ -381,7 +382,7 @@ __global__ void __launch_bounds__(QB_RF_BLOCK, QB_RF_MINB) k_render_f(DevScene S
                         const int2 m = __ldg(S.meta + p);
                         float t;
                         if (m.x == QB_TRIANGLE)
-                            t = ray_triangle_v(kz, ra, rb, rc, o[0], o[1], o[2], dx, dy, dz, tmin, best);
+                            t = ray_triangle_v(kz, ra, rb, rc, o[0], o[1], o[2], sh, tmin, best);
                         else if (m.x == QB_BOX)
                             t = ray_box_v(ra, rb, rc, __ldg(pr + 3), o[0], o[1], o[2], dx, dy, dz, tmin, best);
                         else

@@ -361,6 +361,7 @@ int qb_scene_create(int32_t n_scenes, const int64_t *prim_offsets, const int64_t
     d.meta = qb::dev_upload(sc, meta);
     d.prim_offset = qb::dev_upload(sc, prim_offset);
     d.primc = qb::dev_upload(sc, primc);
+    d.tri_only = std::all_of(meta.begin(), meta.end(), [](const int2 &m) { return m.x == QB_TRIANGLE; });
     if (!d.root || !d.bounds || !d.nodef || !d.noded || !d.nodei || !d.primf || !d.primd || !d.meta || !d.prim_offset ||
         !d.primc) {
         qb::set_error("scene upload failed: %s", cudaGetErrorString(cudaGetLastError()));

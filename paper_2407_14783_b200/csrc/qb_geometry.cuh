@@ -31,6 +31,7 @@ struct DevScene {
     const int *prim_offset; // [S+1] first primitive of each scene (BVH order)
     const float4 *primc;    // [P][4] culling bounds: (centre, r) (A0, 0) (A1, 0) (A2, 0);
                             // support along unit n = r + sum_k |n . A_k| (A_k = box half-axes)
+    int tri_only;           // every primitive is a triangle (meshes: no per-primitive type dispatch)
 };
 
 #ifdef __CUDACC__

@@ -289,7 +289,7 @@ __global__ void __launch_bounds__(QB_RF_BLOCK, QB_RF_MINB) k_render_f(DevScene S
 
             // lanes outside the image carry best = -1: they never want a box
             float best = valid ? tmax : -1.0f;
-            int bid = -1;
+            int bp = -1;  // nearest primitive so far; its object id is read once, after the traversal
             bool hit = false;
 #ifdef QB_RF_STATS
             unsigned st_visit = 0, st_prim = 0, st_active = __popc(__ballot_sync(FULL, valid));
@@ -376,21 +376,26 @@ __global__ void __launch_bounds__(QB_RF_BLOCK, QB_RF_MINB) k_render_f(DevScene S
                     st_prim += cb;
 #endif
                     for (int p = ca; p < ca + cb; ++p) {
-                        // record and metadata loads issued together (no type-dependent load)
+                        // record (and, for mixed scenes, type) loads issued together
                         const float4 *pr = S.primf + 4 * p;
                         const float4 ra = __ldg(pr), rb = __ldg(pr + 1), rc = __ldg(pr + 2);
-                        const int2 m = __ldg(S.meta + p);
                         float t;
-                        if (m.x == QB_TRIANGLE)
+                        if (S.tri_only) {  // meshes: no type load, no dispatch
                             t = ray_triangle_v(kz, ra, rb, rc, o[0], o[1], o[2], sh, tmin, best);
-                        else if (m.x == QB_BOX)
-                            t = ray_box_v(ra, rb, rc, __ldg(pr + 3), o[0], o[1], o[2], dx, dy, dz, tmin, best);
-                        else
-                            t = ray_sphere_v(ra, rb.x, o[0], o[1], o[2], dx, dy, dz, tmin, best);
+                        } else {
+                            const int ty = __ldg(&S.meta[p].x);
+                            if (ty == QB_TRIANGLE)
+                                t = ray_triangle_v(kz, ra, rb, rc, o[0], o[1], o[2], sh, tmin, best);
+                            else if (ty == QB_BOX)
+                                t = ray_box_v(ra, rb, rc, __ldg(pr + 3), o[0], o[1], o[2], dx, dy, dz, tmin, best);
+                            else
+                                t = ray_sphere_v(ra, rb.x, o[0], o[1], o[2], dx, dy, dz, tmin, best);
+                        }
                         QB_DBG(dbg, 5, p, t, best);
-                        if (t > 0.0f && (t < best || !hit || (t == best && m.y < bid))) {
+                        // tests return t <= best; ties (rare) go to the lower object id
+                        if (t > 0.0f && (t < best || !hit || __ldg(&S.meta[p].y) < __ldg(&S.meta[bp].y))) {
                             best = t;
-                            bid = m.y;
+                            bp = p;
                             hit = true;
                         }
                     }
@@ -439,7 +444,7 @@ __global__ void __launch_bounds__(QB_RF_BLOCK, QB_RF_MINB) k_render_f(DevScene S
             }
 #endif
             float t = hit ? best : -1.0f;
-            int oid = hit ? bid : -1;
+            int oid = hit ? __ldg(&S.meta[bp].y) : -1;
             if (!EXACT && n_extra > 0) {  // swarm agents as spheres (kernels.py:438-445)
                 for (int k = 0; k < n_extra; ++k) {
                     const float4 sph = *reinterpret_cast<const float4 *>(extra + (c * n_extra + k) * 4);

@@ -51,6 +51,7 @@ __global__ void k_scene_bounds(int cnt, const int64_t *type, const int64_t *oid,
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
         if (type[i] < 0 || type[i] > 2) atomicOr(bad, 1);
         if (oid[i] <= 0 || oid[i] >= (1LL << 31)) atomicOr(bad, 2);
+        if (type[i] != QB_TRIANGLE) atomicOr(bad, 8);  // (not an error: the scene is not triangles only)
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
             const double l = lo[3 * i + k], h = hi[3 * i + k];
@@ -693,6 +694,7 @@ int scene_create_device(int n_scenes, const int64_t *prim_offsets, const int64_t
     sc->n_prims = P;
     sc->max_depth = max_depth;
     sc->max_scene_prims = (int)max_cnt;
+    d.tri_only = !(ints[0] & 8);
     *out = sc;
     return QB_OK;
 }

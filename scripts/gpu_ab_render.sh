@@ -7,6 +7,6 @@ for r in 1 2 3; do
     python -c "
 import json
 l=[x for x in open('gpurun_out/ab_$v.log') if x.startswith('{')]
-d=json.loads(l[-1]); print('$v', 'value %.4g'%d['value'], 'render %.4f ms'%d.get('kernel_ms', {}).get('render_k2', -1), 'step %.4f'%d['ms_per_step'])"
+d=json.loads(l[-1]); km=d.get('kernel_ms', {}); print('$v', 'value %.4g'%d['value'], 'render %.4f ms'%km.get('render_k2', -1), 'step %.4f'%d['ms_per_step'], ' '.join('%s %.4f'%(k, x) for k, x in km.items() if k != 'render_k2'))"
   done
 done

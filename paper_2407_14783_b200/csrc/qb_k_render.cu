@@ -1165,7 +1165,8 @@ unsigned int *claim_counter(cudaStream_t st) {
         for (int i = 0; i < used; ++i)
             if (keys[i] == st) slot = i;
         if (slot < 0) {
-            slot = used < QB_CULL_SLOTS ? used++ : (int)(reinterpret_cast<uintptr_t>(st) % QB_CULL_SLOTS);
+            if (used == QB_CULL_SLOTS) return nullptr;  // (static striding: a shared counter would race)
+            slot = used++;
             keys[slot] = st;
         }
     }
@@ -1189,7 +1190,12 @@ unsigned int *claim_counter(cudaStream_t st) {
 template <bool FS, bool EX, bool CE, bool EXACT, bool S1, bool SEGP> void cull_kernel(const CullLaunch &L) {
     unsigned int *claim = nullptr;
     if (S1) {
-        claim = claim_counter(L.st);
+        // not inside a stream capture: a graph replays on any stream, possibly
+        // beside a direct launch that uses the same stream's counter
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(L.st, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone)
+            claim = claim_counter(L.st);
+        cudaGetLastError();
         if (claim && cudaMemsetAsync(claim, 0, sizeof(unsigned int), L.st) != cudaSuccess) {
             cudaGetLastError();
             claim = nullptr;

@@ -547,15 +547,32 @@ def run_bptt(args, rank, world):
     torch.cuda.synchronize()
     clocks = clk.stop()
     ms = max_over_ranks(t0.elapsed_time(t1), world)
-    # per-kernel timing of one iteration
-    e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-    e[0].record()
-    tape, _ = G.rollout_planes(P, "rotor", init, acts)
-    e[1].record()
-    G.backward_planes(P, "rotor", tape, acts, torch.zeros_like(tape), action_grad_sum=gsum)
-    e[2].record()
-    torch.cuda.synchronize()
-    return dict(n=n, T=T, ms=ms, clocks=clocks, fwd_ms=e[0].elapsed_time(e[1]), bwd_ms=e[1].elapsed_time(e[2]))
+    # per-kernel device time: each direction captured alone in a CUDA graph and
+    # replayed back to back (an eager call's host overhead and allocations
+    # would otherwise be timed with a 0.05 ms kernel)
+    tape_s, _ = G.rollout_planes(P, "rotor", init, acts)
+    gz = torch.zeros_like(tape_s)
+
+    def graph_ms(fn, R=20):
+        gr, s = torch.cuda.CUDAGraph(), torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            fn()  # warm-up outside the capture
+            with torch.cuda.graph(gr, stream=s):
+                fn()
+        torch.cuda.current_stream().wait_stream(s)
+        gr.replay()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(R):
+            gr.replay()
+        b.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / R
+
+    fwd_ms = graph_ms(lambda: G.rollout_planes(P, "rotor", init, acts))
+    bwd_ms = graph_ms(lambda: G.backward_planes(P, "rotor", tape_s, acts, gz, action_grad_sum=gsum))
+    return dict(n=n, T=T, ms=ms, clocks=clocks, fwd_ms=fwd_ms, bwd_ms=bwd_ms)
 
 
 def cpu_baseline_env(kind="c3", n_sample=1024, steps=12):

@@ -257,15 +257,34 @@ __global__ void __launch_bounds__(64) k_rollout_bwd_tr(DynConsts<float> C, long 
         const float *gl = g_traj + (long long)T * block;
 #pragma unroll
         for (int k = 0; k < 6; ++k) lam[k] = gl[k * ld + ii];
+        // step t's inputs (tape p, v and the loss gradient) are loaded one
+        // iteration ahead: at 7 warps per SM nothing else hides their latency
+        float pvn[6], gtn[6];
+        if (T > 0) {
+#pragma unroll
+            for (int k = 0; k < 6; ++k) {
+                pvn[k] = tape[(long long)(T - 1) * block + k * ld + ii];
+                gtn[k] = g_traj[(long long)(T - 1) * block + k * ld + ii];
+            }
+        }
         __syncthreads();  // R's forward of step T-1
         for (int t = T - 1; t >= -1; --t) {
             if (t >= 0) {
                 const int bf = t & 1;
-                const float *xs = tape + (long long)t * block;
                 float vs[NS][NK][3];  // v at each stage argument
-                float pv[6];
+                float pv[6], gtc[6];
 #pragma unroll
-                for (int k = 0; k < 6; ++k) pv[k] = xs[k * ld + ii];
+                for (int k = 0; k < 6; ++k) {
+                    pv[k] = pvn[k];
+                    gtc[k] = gtn[k];
+                }
+                if (t >= 1) {
+#pragma unroll
+                    for (int k = 0; k < 6; ++k) {
+                        pvn[k] = tape[(long long)(t - 1) * block + k * ld + ii];
+                        gtn[k] = g_traj[(long long)(t - 1) * block + k * ld + ii];
+                    }
+                }
                 // forward recompute of the translational stages
 #pragma unroll
                 for (int s = 0; s < NS; ++s) {
@@ -331,9 +350,8 @@ __global__ void __launch_bounds__(64) k_rollout_bwd_tr(DynConsts<float> C, long 
 #pragma unroll
                     for (int c = 0; c < 6; ++c) lam[c] = yb[c];
                 }
-                const float *gt = g_traj + (long long)t * block;
 #pragma unroll
-                for (int k = 0; k < 6; ++k) lam[k] += gt[k * ld + ii];
+                for (int k = 0; k < 6; ++k) lam[k] += gtc[k];
             }
             __syncthreads();
         }
@@ -353,16 +371,18 @@ __global__ void __launch_bounds__(64) k_rollout_bwd_tr(DynConsts<float> C, long 
         for (int k = 0; k < 11; ++k) lam[k] = gl[(6 + k) * ld + ii];
     }
     // forward recompute of the rotational stages of step t into buffer t & 1
-    auto forward = [&](int t) {
-        const int bf = t & 1;
+    // (x, a: step t's tape row and action, loaded by the caller ahead of time)
+    auto load_step = [&](int t, float *x, float *a) {
         const float *xs = tape + (long long)t * block;
-        float x[17];
 #pragma unroll
         for (int k = 0; k < 17; ++k) x[k] = xs[k * ld + ii];
-        float a[4], cmd[4];
         const float *ap = actions + ((long long)t * n + ii) * 4;
 #pragma unroll
         for (int k = 0; k < 4; ++k) a[k] = ap[k];
+    };
+    auto forward = [&](int t, float *x, const float *a) {
+        const int bf = t & 1;
+        float cmd[4];
         command_to_speeds<float, KIND>(C, x, a, cmd);
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
@@ -434,10 +454,26 @@ __global__ void __launch_bounds__(64) k_rollout_bwd_tr(DynConsts<float> C, long 
             for (int k = 0; k < 4; ++k) rot[k] = w[k];
         }
     };
-    if (T > 0) forward(T - 1);
+    if (T > 0) {
+        float x[17], a[4];
+        load_step(T - 1, x, a);
+        forward(T - 1, x, a);
+    }
     __syncthreads();
     for (int t = T - 1; t >= -1; --t) {
         const int tb = t + 1;  // the step whose reverse sweep R finishes now (T processed it last iteration)
+        // this iteration's global inputs, issued before the sweep hides their latency:
+        // the next forward's tape row / action, step tb's action and loss gradient
+        float xn[17], an[4], atb[4], gtb[11];
+        if (t >= 1) load_step(t - 1, xn, an);
+        if (tb <= T - 1) {
+            const float *ap = actions + ((long long)tb * n + ii) * 4;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) atb[k] = ap[k];
+            const float *gt = g_traj + (long long)tb * block;
+#pragma unroll
+            for (int k = 0; k < 11; ++k) gtb[k] = gt[(6 + k) * ld + ii];
+        }
         if (tb <= T - 1) {
             const int bf = tb & 1;
             float cb[4] = {0.f, 0.f, 0.f, 0.f};
@@ -512,10 +548,7 @@ __global__ void __launch_bounds__(64) k_rollout_bwd_tr(DynConsts<float> C, long 
                 float cbm[4];
 #pragma unroll
                 for (int k = 0; k < 4; ++k) cbm[k] = clip_mask(sm.craw[bf][k][lane], C.rlo, C.rhi, flag) * cb[k];
-                const float *ap = actions + ((long long)tb * n + ii) * 4;
-                float a[4];
-#pragma unroll
-                for (int k = 0; k < 4; ++k) a[k] = ap[k];
+                const float *a = atb;
                 if constexpr (KIND == QB_CMD_ROTOR) {
 #pragma unroll
                     for (int k = 0; k < 4; ++k) ga[k] = cbm[k];
@@ -542,11 +575,10 @@ __global__ void __launch_bounds__(64) k_rollout_bwd_tr(DynConsts<float> C, long 
 #pragma unroll
                 for (int k = 0; k < 4; ++k) gp[k] = ga[k];
             }
-            const float *gt = g_traj + (long long)tb * block;
 #pragma unroll
-            for (int k = 0; k < 11; ++k) lam[k] += gt[(6 + k) * ld + ii];
+            for (int k = 0; k < 11; ++k) lam[k] += gtb[k];
         }
-        if (t >= 1) forward(t - 1);
+        if (t >= 1) forward(t - 1, xn, an);
         __syncthreads();
     }
     if (live) {

@@ -24,6 +24,7 @@
 #include "qb_dynamics.cuh"
 #include "qb_geometry.cuh"
 #include <mutex>
+#include <type_traits>
 
 #include "qb_checks.cuh"
 #include "qb_internal.h"
@@ -375,28 +376,47 @@ __global__ void __launch_bounds__(QB_RF_BLOCK, QB_RF_MINB) k_render_f(DevScene S
 #ifdef QB_RF_STATS
                     st_prim += cb;
 #endif
-                    for (int p = ca; p < ca + cb; ++p) {
-                        // record (and, for mixed scenes, type) loads issued together
-                        const float4 *pr = S.primf + 4 * p;
-                        const float4 ra = __ldg(pr), rb = __ldg(pr + 1), rc = __ldg(pr + 2);
-                        float t;
-                        if (S.tri_only) {  // meshes: no type load, no dispatch
-                            t = ray_triangle_v(kz, ra, rb, rc, o[0], o[1], o[2], sh, tmin, best);
-                        } else {
+                    // tests return t <= best; ties (rare) go to the lower object id
+                    auto take = [&](float t, int p) {
+                        if (t > 0.0f && (t < best || !hit || __ldg(&S.meta[p].y) < __ldg(&S.meta[bp].y))) {
+                            best = t;
+                            bp = p;
+                            hit = true;
+                        }
+                    };
+                    if (S.tri_only) {
+                        // meshes: no type load or dispatch, and the tile's shear axis is
+                        // resolved once per leaf instead of per triangle
+                        auto leaf = [&](auto kzc) {
+                            constexpr int KZ = decltype(kzc)::value;
+                            for (int p = ca; p < ca + cb; ++p) {
+                                const float4 *pr = S.primf + 4 * p;
+                                take(ray_triangle_wt<KZ>(__ldg(pr), __ldg(pr + 1), __ldg(pr + 2), o[0], o[1], o[2], sh, tmin,
+                                                         best),
+                                     p);
+                            }
+                        };
+                        if (kz == 2)
+                            leaf(std::integral_constant<int, 2>{});
+                        else if (kz == 1)
+                            leaf(std::integral_constant<int, 1>{});
+                        else
+                            leaf(std::integral_constant<int, 0>{});
+                    } else {
+                        for (int p = ca; p < ca + cb; ++p) {
+                            // record and type loads issued together
+                            const float4 *pr = S.primf + 4 * p;
+                            const float4 ra = __ldg(pr), rb = __ldg(pr + 1), rc = __ldg(pr + 2);
                             const int ty = __ldg(&S.meta[p].x);
+                            float t;
                             if (ty == QB_TRIANGLE)
                                 t = ray_triangle_v(kz, ra, rb, rc, o[0], o[1], o[2], sh, tmin, best);
                             else if (ty == QB_BOX)
                                 t = ray_box_v(ra, rb, rc, __ldg(pr + 3), o[0], o[1], o[2], dx, dy, dz, tmin, best);
                             else
                                 t = ray_sphere_v(ra, rb.x, o[0], o[1], o[2], dx, dy, dz, tmin, best);
-                        }
-                        QB_DBG(dbg, 5, p, t, best);
-                        // tests return t <= best; ties (rare) go to the lower object id
-                        if (t > 0.0f && (t < best || !hit || __ldg(&S.meta[p].y) < __ldg(&S.meta[bp].y))) {
-                            best = t;
-                            bp = p;
-                            hit = true;
+                            QB_DBG(dbg, 5, p, t, best);
+                            take(t, p);
                         }
                     }
                     ca = -1;

@@ -1,8 +1,8 @@
-# A/B of a workload's render (WL=c3 default): scripts/_dbg/base.so vs scripts/_dbg/new.so, alternating
+# A/B of a workload (WL=c3 default) between library builds in scripts/_dbg (VARIANTS, default "base new"), alternating
 WL=${WL:-c3}
 STEPS=${STEPS:-30}
 for r in 1 2 3; do
-  for v in base new; do
+  for v in ${VARIANTS:-base new}; do
     QB_LIB_PATH=$PWD/scripts/_dbg/$v.so timeout 300 python bench.py --workload $WL --steps $STEPS --warmup 3 --no-e2e --no-cpu --no-sub > gpurun_out/ab_$v.log 2>&1
     python -c "
 import json

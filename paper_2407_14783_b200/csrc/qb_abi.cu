@@ -745,6 +745,10 @@ static int step_io_enqueue(const qb_params *p, int32_t cmd_kind, const qb_task *
                 if (e != cudaSuccess) return io_fail("result copy", e);
             }
         }
+        // every render done before the packs and the other copies (they may read a
+        // view's outputs, e.g. the landing centroids), then the side copies
+        if ((e = cudaEventRecord(sd.ev_rs, sd.rs)) != cudaSuccess || (e = cudaStreamWaitEvent(st, sd.ev_rs, 0)) != cudaSuccess)
+            return io_fail("join", e);
         if (io->state_rows || io->n_packs) {
             rc = qb::launch_io_pack(b->dtype, b->n, b->ld, b->state, io->state_rows, io->n_packs, io->packs, st);
             if (rc) return rc;
@@ -755,8 +759,7 @@ static int step_io_enqueue(const qb_params *p, int32_t cmd_kind, const qb_task *
             e = cudaMemcpyAsync(cp.dst, cp.src, (size_t)cp.bytes, cudaMemcpyDeviceToHost, st);
             if (e != cudaSuccess) return io_fail("result copy", e);
         }
-        if ((e = cudaEventRecord(sd.ev_rs, sd.rs)) != cudaSuccess || (e = cudaStreamWaitEvent(st, sd.ev_rs, 0)) != cudaSuccess ||
-            (e = cudaEventRecord(sd.ev_done, sd.st)) != cudaSuccess || (e = cudaStreamWaitEvent(st, sd.ev_done, 0)) != cudaSuccess)
+        if ((e = cudaEventRecord(sd.ev_done, sd.st)) != cudaSuccess || (e = cudaStreamWaitEvent(st, sd.ev_done, 0)) != cudaSuccess)
             return io_fail("join", e);
         return QB_OK;
     }

@@ -883,8 +883,6 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, QB_CULL_MINB)
                 best[u] = tmx[u];
                 bid[u] = 0x7fffffff;
             }
-            // triangle shear axis, warp-uniform (see k_render_f)
-            const int kz = __shfl_sync(FULL, dominant_axis(dx[0], dy[0], dz[0]), 12);
             for (int b = 0; b < ncand; b += 32) {
                 const int k = b + lane;
                 bool kp = false;
@@ -965,6 +963,9 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, QB_CULL_MINB)
                         p = cand[k2];
                     }
                     if (p >= 0) {  // triangles, records beyond the budget, ids too large for the word
+                        // triangle shear axis of the tile, warp-uniform (see k_render_f); taken
+                        // here, where every lane is (this branch depends on the survivor only)
+                        const int kz = __shfl_sync(FULL, dominant_axis(dx[0], dy[0], dz[0]), 12);
                         const int2 mt = __ldg(S.meta + p);
                         oid = mt.y;
                         const float4 *pr = S.primf + 4 * p;

@@ -863,8 +863,12 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, QB_CULL_MINB)
                 }
             }
             const float x = ((j + 0.5f) * sx - 1.0f) * cam.th;
-            float dx[2], dy[2], dz[2], ix[2], iy[2], iz[2], czv[2], tmx[2], best[2];
-            int bid[2];  // INT_MAX: no hit yet
+            float dx[2], dy[2], dz[2], ix[2], iy[2], iz[2], czv[2], tmx[2];
+            // nearest hit so far as one key, (t bits) << 32 | object id: for t > 0 the
+            // float bits order like t, so one unsigned min is "nearer, ties to the lower
+            // id"; a miss (-1.0f) never wins; id INT_MAX: no hit yet
+            unsigned long long bk[2];
+            auto best_of = [&](int u) { return __uint_as_float((unsigned)(bk[u] >> 32)); };
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
                 const float y = ((ii[u] + 0.5f) * sy - 1.0f) * cam.tv;
@@ -880,8 +884,7 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, QB_CULL_MINB)
                 iz[u] = rcp_approx(dz[u]);
                 czv[u] = cz;
                 tmx[u] = cam.max_range * (n2 * cz);  // max_range / cos(angle to the axis)
-                best[u] = tmx[u];
-                bid[u] = 0x7fffffff;
+                bk[u] = ((unsigned long long)__float_as_uint(tmx[u]) << 32) | 0x7fffffffull;
             }
             for (int b = 0; b < ncand; b += 32) {
                 const int k = b + lane;
@@ -932,7 +935,7 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, QB_CULL_MINB)
                         if (tw & REC_AABB) {
 #pragma unroll
                             for (int u = 0; u < 2; ++u)
-                                t[u] = slab_hit(s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, ix[u], iy[u], iz[u], tmin, best[u]);
+                                t[u] = slab_hit(s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, ix[u], iy[u], iz[u], tmin, best_of(u));
                         } else if (tw & REC_OBB) {
                             const float4 s2 = rec[k2][2], s3 = rec[k2][3];
                             // local direction = R^T d: columns (s2.x s2.y s2.z) (s2.w s3.x s3.y) (s3.z s3.w s1.z)
@@ -942,7 +945,7 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, QB_CULL_MINB)
                                 const float ly = s2.w * dx[u] + s3.x * dy[u] + s3.y * dz[u];
                                 const float lz = s3.z * dx[u] + s3.w * dy[u] + s1.z * dz[u];
                                 t[u] = slab_hit(s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, rcp_approx(lx), rcp_approx(ly),
-                                                rcp_approx(lz), tmin, best[u]);
+                                                rcp_approx(lz), tmin, best_of(u));
                             }
                         } else if (tw & REC_SPHERE) {
 #pragma unroll
@@ -953,7 +956,8 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, QB_CULL_MINB)
                                 if (disc >= 0.0f) {
                                     const float sq = sqrtf(disc);
                                     const float ta = -bb - sq, tb = -bb + sq;
-                                    t[u] = (ta > tmin && ta <= best[u]) ? ta : ((tb > tmin && tb <= best[u]) ? tb : -1.0f);
+                                    const float bu = best_of(u);
+                                    t[u] = (ta > tmin && ta <= bu) ? ta : ((tb > tmin && tb <= bu) ? tb : -1.0f);
                                 }
                             }
                         } else {
@@ -971,26 +975,23 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, QB_CULL_MINB)
                         const float4 *pr = S.primf + 4 * p;
 #pragma unroll
                         for (int u = 0; u < 2; ++u)
-                            t[u] = mt.x == QB_SPHERE ? ray_sphere_f(pr, o[0], o[1], o[2], dx[u], dy[u], dz[u], tmin, best[u])
-                                   : mt.x == QB_BOX  ? ray_box_f(pr, o[0], o[1], o[2], dx[u], dy[u], dz[u], tmin, best[u])
-                                                     : ray_triangle_call(kz, pr, o[0], o[1], o[2], dx[u], dy[u], dz[u], tmin, best[u]);
+                            t[u] = mt.x == QB_SPHERE ? ray_sphere_f(pr, o[0], o[1], o[2], dx[u], dy[u], dz[u], tmin, best_of(u))
+                                   : mt.x == QB_BOX  ? ray_box_f(pr, o[0], o[1], o[2], dx[u], dy[u], dz[u], tmin, best_of(u))
+                                                     : ray_triangle_call(kz, pr, o[0], o[1], o[2], dx[u], dy[u], dz[u], tmin, best_of(u));
                     }
 #pragma unroll
                     for (int u = 0; u < 2; ++u)
                         // tests return t <= best; ties go to the lowest object id
-                        if (t[u] > 0.0f && (t[u] < best[u] || oid < bid[u])) {
-                            best[u] = t[u];
-                            bid[u] = oid;
-                        }
+                        bk[u] = min(bk[u], ((unsigned long long)__float_as_uint(t[u]) << 32) | (unsigned)oid);
                 }
             }
             float tt[2];
             int to[2];
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
-                const bool hit = bid[u] != 0x7fffffff;
-                tt[u] = hit ? best[u] : -1.0f;
-                to[u] = hit ? bid[u] : -1;
+                const bool hit = (unsigned)bk[u] != 0x7fffffffu;
+                tt[u] = hit ? best_of(u) : -1.0f;
+                to[u] = hit ? (int)(unsigned)bk[u] : -1;
             }
             // swarm agents as spheres after the scene (kernels.py:438-445): a
             // sphere replaces the scene hit only when strictly nearer

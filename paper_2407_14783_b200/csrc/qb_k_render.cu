@@ -568,9 +568,8 @@ __device__ __forceinline__ float slab_hit(float nlx, float nly, float nlz, float
     const float t0 = fmaxf(fmaxf(fminf(tax, tbx), fminf(tay, tby)), fmaxf(fminf(taz, tbz), tmin));
     const float t1 = fminf(fminf(fmaxf(tax, tbx), fmaxf(tay, tby)), fminf(fmaxf(taz, tbz), tmax));
     if (t0 > t1) return -1.0f;
-    if (t0 > tmin && t0 <= tmax) return t0;
-    if (t1 > tmin && t1 <= tmax) return t1;
-    return -1.0f;
+    // (t0 <= t1 <= tmax here: only the tmin tests remain)
+    return t0 > tmin ? t0 : (t1 > tmin ? t1 : -1.0f);
 }
 
 // CENT: a pad centroid is reduced inline (landing, split == 1): a compile-time
@@ -956,8 +955,8 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, QB_CULL_MINB)
                                 if (disc >= 0.0f) {
                                     const float sq = sqrtf(disc);
                                     const float ta = -bb - sq, tb = -bb + sq;
-                                    const float bu = best_of(u);
-                                    t[u] = (ta > tmin && ta <= bu) ? ta : ((tb > tmin && tb <= bu) ? tb : -1.0f);
+                                    // (a root beyond the nearest hit loses the key min below)
+                                    t[u] = ta > tmin ? ta : (tb > tmin ? tb : -1.0f);
                                 }
                             }
                         } else {

@@ -611,12 +611,16 @@ static int check_step_io(const qb_params *p, const qb_task *task, const qb_scene
 // bit-identical.
 namespace {
 constexpr int IO_CHUNKS_MAX = 32;
+#ifndef QB_IO_RSTREAMS
+#define QB_IO_RSTREAMS 2
+#endif
+constexpr int IO_RSTREAMS = QB_IO_RSTREAMS;  // render streams, the caller's included
 constexpr long long IO_CHUNK_MIN = 2048;  // cameras per slice at least
 constexpr int IO_MAX_DEV = 64;
 struct IoSide {
     cudaStream_t st = nullptr;   // the D2H copies
-    cudaStream_t rs = nullptr;   // odd slices' renders (a slice's tail overlaps the next slice's start)
-    cudaEvent_t ev[IO_CHUNKS_MAX] = {}, ev_step = nullptr, ev_rs = nullptr, ev_done = nullptr;
+    cudaStream_t rs[IO_RSTREAMS - 1] = {};  // renders of slices j % IO_RSTREAMS != 0 (a slice's tail overlaps the next slices' start)
+    cudaEvent_t ev[IO_CHUNKS_MAX] = {}, ev_step = nullptr, ev_rs[IO_RSTREAMS - 1] = {}, ev_done = nullptr;
 };
 // slices per step at most: 16 (QB_IO_SLICES overrides for experiments; 1 = no overlap)
 int io_slices() {
@@ -719,19 +723,23 @@ static int step_io_enqueue(const qb_params *p, int32_t cmd_kind, const qb_task *
         IoSide &sd = g_io_side[dev];
         if (!sd.st) {
             e = cudaStreamCreateWithFlags(&sd.st, cudaStreamNonBlocking);
-            if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&sd.rs, cudaStreamNonBlocking);
+            for (int k = 0; e == cudaSuccess && k < IO_RSTREAMS - 1; ++k) {
+                e = cudaStreamCreateWithFlags(&sd.rs[k], cudaStreamNonBlocking);
+                if (e == cudaSuccess) e = cudaEventCreateWithFlags(&sd.ev_rs[k], cudaEventDisableTiming);
+            }
             for (int k = 0; e == cudaSuccess && k < IO_CHUNKS_MAX; ++k)
                 e = cudaEventCreateWithFlags(&sd.ev[k], cudaEventDisableTiming);
-            for (cudaEvent_t *x : {&sd.ev_step, &sd.ev_rs, &sd.ev_done})
+            for (cudaEvent_t *x : {&sd.ev_step, &sd.ev_done})
                 if (e == cudaSuccess) e = cudaEventCreateWithFlags(x, cudaEventDisableTiming);
             if (e != cudaSuccess) return io_fail("side streams", e);
         }
         // the second render stream starts after the env step
-        if ((e = cudaEventRecord(sd.ev_step, st)) != cudaSuccess || (e = cudaStreamWaitEvent(sd.rs, sd.ev_step, 0)) != cudaSuccess)
-            return io_fail("step event", e);
+        if ((e = cudaEventRecord(sd.ev_step, st)) != cudaSuccess) return io_fail("step event", e);
+        for (int k = 0; k < IO_RSTREAMS - 1; ++k)
+            if ((e = cudaStreamWaitEvent(sd.rs[k], sd.ev_step, 0)) != cudaSuccess) return io_fail("step event", e);
         for (int j = 0; j < nsl; ++j) {
             const long long c0 = b->n * j / nsl, c1 = b->n * (j + 1) / nsl;
-            cudaStream_t r = (j & 1) ? sd.rs : st;
+            cudaStream_t r = j % IO_RSTREAMS ? sd.rs[j % IO_RSTREAMS - 1] : st;
             rc = io_render_slice(s, b, io, c0, c1, r);
             if (rc) return rc;
             if ((e = cudaEventRecord(sd.ev[j], r)) != cudaSuccess || (e = cudaStreamWaitEvent(sd.st, sd.ev[j], 0)) != cudaSuccess)
@@ -747,8 +755,10 @@ static int step_io_enqueue(const qb_params *p, int32_t cmd_kind, const qb_task *
         }
         // every render done before the packs and the other copies (they may read a
         // view's outputs, e.g. the landing centroids), then the side copies
-        if ((e = cudaEventRecord(sd.ev_rs, sd.rs)) != cudaSuccess || (e = cudaStreamWaitEvent(st, sd.ev_rs, 0)) != cudaSuccess)
-            return io_fail("join", e);
+        for (int k = 0; k < IO_RSTREAMS - 1; ++k)
+            if ((e = cudaEventRecord(sd.ev_rs[k], sd.rs[k])) != cudaSuccess ||
+                (e = cudaStreamWaitEvent(st, sd.ev_rs[k], 0)) != cudaSuccess)
+                return io_fail("join", e);
         if (io->state_rows || io->n_packs) {
             rc = qb::launch_io_pack(b->dtype, b->n, b->ld, b->state, io->state_rows, io->n_packs, io->packs, st);
             if (rc) return rc;

@@ -862,6 +862,10 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, QB_CULL_MINB)
                 }
             }
             const float x = ((j + 0.5f) * sx - 1.0f) * cam.th;
+            // d = cz (x R0 + y R1 + R2) with R0..R2 the rotation's columns; the column
+            // part x R0 + R2 is shared by the lane's two rays
+            const float *Rs = rws_s[wib];
+            const float ax = fmaf(x, Rs[0], Rs[2]), ay = fmaf(x, Rs[3], Rs[5]), az = fmaf(x, Rs[6], Rs[8]);
             float dx[2], dy[2], dz[2], ix[2], iy[2], iz[2], czv[2], tmx[2];
             // nearest hit so far as one key, (t bits) << 32 | object id: for t > 0 the
             // float bits order like t, so one unsigned min is "nearer, ties to the lower
@@ -873,11 +877,9 @@ __global__ void __launch_bounds__(CULL_WARPS * 32, QB_CULL_MINB)
                 const float y = ((ii[u] + 0.5f) * sy - 1.0f) * cam.tv;
                 const float n2 = x * x + y * y + 1.0f;
                 const float cz = rsqrtf(n2);
-                const float cx = x * cz, cy = y * cz;
-                const float *Rs = rws_s[wib];
-                dx[u] = Rs[0] * cx + Rs[1] * cy + Rs[2] * cz;
-                dy[u] = Rs[3] * cx + Rs[4] * cy + Rs[5] * cz;
-                dz[u] = Rs[6] * cx + Rs[7] * cy + Rs[8] * cz;
+                dx[u] = cz * fmaf(y, Rs[1], ax);
+                dy[u] = cz * fmaf(y, Rs[4], ay);
+                dz[u] = cz * fmaf(y, Rs[7], az);
                 ix[u] = rcp_approx(dx[u]);
                 iy[u] = rcp_approx(dy[u]);
                 iz[u] = rcp_approx(dz[u]);
